@@ -1,0 +1,96 @@
+"""Zip-up (decomposition) algorithm, §3.2 (lines 253-275), window N = 1.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Follows the paper's order:
+
+  1. "the tensor trains that are part of the operation shift their normalization
+     center to the left end"  -> right_orthonormalize every operand,
+     the MPO included as a TT over (d_out*d_in) (SURVEY.md c-A2).
+  2. "the first N-cores ... are contracted exactly according to some calculation rule"
+     (Eq. einsum) -> site matrix T_q with rows (chi, i)
+     and columns (w', r') (xi = mu nu).
+  3. "splitting C(i_1..i_N) into C(i_1) C(i_2..i_N) with some kind of approximate matrix
+     decomposition" -- the SVD of Fig. decomposition_algorithm
+      -- here LAPACK gesdd applied directly to T_q, truncated by the rule
+     of SPEC.md:299 (oracle.tt.truncation_rank).
+  4. the left factor U_k is the output core (left-orthonormal, so no normalisation
+     restore is needed, SURVEY.md c-A6); the remainder diag(s_k) Vh_k is carried and
+     "extended ... using A(i_{N+1}) and B(i_{N+1})".
+  5. "repeated until no more cores can be added, after which the super-core is fully
+     decomposed": the last T is the last core (SURVEY.md c-A7).
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from .tt import right_orthonormalize, tail_sum, truncation_rank
+
+
+def _svd(M: np.ndarray):
+    try:
+        return np.linalg.svd(M, full_matrices=False)
+    except np.linalg.LinAlgError:  # gesdd did not converge: fall back to gesvd
+        import scipy.linalg
+        return scipy.linalg.svd(M, full_matrices=False, lapack_driver="gesvd")
+
+
+def site_matrix(kind: str, G: np.ndarray, Xq: np.ndarray, Oq: Optional[np.ndarray]) -> np.ndarray:
+    """Exact local contraction of the carry G (chi, w, r) with the operand cores
+    (Eq. einsum).  Returns T (chi, i, w', r')."""
+    if kind == "matvec":     # 'ij,j->i': sum over r and j, w
+        return np.einsum("cwr,rjs,wijv->civs", G, Xq, Oq)
+    if kind == "hadamard":   # 'i,i->i': i shared, not summed
+        return np.einsum("cab,bis,aiv->civs", G, Xq, Oq)
+    if kind == "truncate":   # identity operation (PAPER.md:710 truncate)
+        return np.einsum("cr,ris->cis", G[:, 0, :], Xq)[:, :, None, :]
+    raise ValueError(kind)
+
+
+def zipup(kind: str, op: Optional[Sequence[np.ndarray]], x: Sequence[np.ndarray], eps: float,
+          max_rank: int, orth_operator: bool = True, force_ranks: Optional[Sequence[int]] = None):
+    """Returns a dict with
+      cores   : output cores C_q (chi_q, d_q, chi_{q+1})
+      ranks   : [1, chi_1, ..., chi_{L-1}, 1]
+      delta2  : discarded sum of squares per split (L-1 values)
+      sigmas  : singular values of every T_q (q < L-1), descending
+      norm    : ||y||_F = ||C_{L-1}||_F (left-canonical output)
+    """
+    X = right_orthonormalize([np.asarray(c, dtype=np.float64) for c in x])       # step 1
+    if kind == "truncate":
+        O = None
+    else:
+        O = [np.asarray(c, dtype=np.float64) for c in op]
+        if orth_operator:
+            O = right_orthonormalize(O)
+    L = len(X)
+    G = np.ones((1, 1, 1))                    # carry (chi, w, r)
+    cores: List[np.ndarray] = []
+    delta2: List[float] = []
+    sigmas: List[np.ndarray] = []
+    ranks = [1]
+    for q in range(L):
+        T = site_matrix(kind, G, X[q], None if O is None else O[q])              # step 2
+        chi, d, v, s = T.shape
+        M = T.reshape(chi * d, v * s)
+        if q == L - 1:                                                            # step 5
+            cores.append(T.reshape(chi, d, 1))
+            ranks.append(1)
+            break
+        U, sig, Vh = _svd(M)                                                      # step 3
+        if float(np.sum(sig * sig)) == 0.0:
+            # all-zero site matrix (SPEC.md:324 / SURVEY.md c-A10): k = 1, U e_0, zero carry
+            k = 1
+            U = np.zeros((M.shape[0], 1)); U[0, 0] = 1.0
+            sig = np.zeros(1); Vh = np.zeros((1, M.shape[1]))
+        else:
+            k = truncation_rank(sig, eps, max_rank)
+        if force_ranks is not None:
+            k = int(force_ranks[q + 1])
+        delta2.append(tail_sum(sig, k))
+        sigmas.append(sig.copy())
+        cores.append(U[:, :k].reshape(chi, d, k))                                 # step 4
+        G = (sig[:k, None] * Vh[:k]).reshape(k, v, s)
+        ranks.append(k)
+    norm = float(np.linalg.norm(cores[-1]))
+    return {"cores": cores, "ranks": ranks, "delta2": delta2, "sigmas": sigmas, "norm": norm}
