@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 zip-up hot path (BASELINE.json metric: zip-up site-contractions/sec
+and FP64 TFLOP/s, 1-8 GPUs) on the batched workload configs[4] (cfg5): per GPU 512
+independent zip-ups, L=40 sites of size 2, state rank 64, random rank-4 MPO, max rank 64,
+eps 1e-10, fp64; weak scaling (512 members per GPU, 4096 at 8 GPUs) with one NCCL
+all-reduce of the batch error budget per step.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload cfgK]
+
+Prints ONE JSON line on rank 0.  A "step" = one qtt_zipup over this GPU's members (a1..a7)
++ the a8 summary + the cross-GPU all-reduce.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2602_20226_b200 import gen  # noqa: E402
+
+METRIC = "zip-up site-contractions/sec"
+UNIT = "site-steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--members-per-gpu", type=int, default=512)
+    ap.add_argument("--cpu-members", type=int, default=8, help="oracle sample size (members) for cpu_baseline")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- workload
+
+def build_workload(args, rank):
+    """Returns (subscripts, kind, problems (list of gen.Problem for this rank), x_stack, op_stack, cfg dict)."""
+    if args.workload == "cfg5":
+        M = args.members_per_gpu
+        members = list(range(rank * M, (rank + 1) * M))
+        probs, xs, ops = gen.cfg5_batch_arrays(members)
+        p0 = probs[0]
+        cfg = {"workload": "configs[4] cfg5: batch of independent zip-ups, L=40 d=2, state rank 64 N(0,1/64), "
+                           "random rank-4 MPO N(0,1/4), max rank 64, eps 1e-10",
+               "members_per_gpu": M, "global_batch": M * args.gpus, "L": 40, "rank": 64, "mpo_rank": 4,
+               "max_rank": 64, "eps": 1e-10, "parallelism": f"dp{args.gpus} (members sharded, 1 all-reduce/step)"}
+        return "ij,j->i", "matvec", probs, xs, ops, cfg
+    mk = {"cfg1": lambda: gen.cfg1(), "cfg2": lambda: gen.cfg2(), "cfg3": lambda: gen.cfg3(),
+          "cfg4": lambda: gen.cfg4()}[args.workload]
+    p = mk()
+    xs = [c[None] for c in p.x.cores]
+    ops = None if p.op is None else [c[None] for c in p.op.cores]
+    subs = {"matvec": "ij,j->i", "hadamard": "i,i->i", "truncate": "i->i"}[p.kind]
+    cfg = {"workload": f"{args.workload} ({p.name})", "members_per_gpu": 1, "global_batch": args.gpus,
+           "max_rank": p.max_rank, "eps": p.eps, "parallelism": f"replicas x{args.gpus}"}
+    return subs, p.kind, [p], xs, ops, cfg
+
+
+def site_flops(kind, ranks_y, xr, orr, d, dj, sweeps):
+    """Per-site algorithmic flops for one member:
+    contract / qr / carry / jacobi (executed sweeps x p(p-1)/2 pairs x 12 m)."""
+    L = len(d)
+    out = []
+    for q in range(L):
+        chi, r, r2 = ranks_y[q], xr[q], xr[q + 1]
+        w, w2 = (orr[q], orr[q + 1]) if kind != "truncate" else (1, 1)
+        m, n = chi * d[q], w2 * r2
+        if kind == "matvec":
+            fc = 2 * chi * w * r * dj[q] * r2 + 2 * chi * d[q] * w2 * r2 * w * dj[q]
+        elif kind == "hadamard":
+            fc = 2 * chi * w * r * d[q] * r2 + 2 * chi * d[q] * r2 * w * w2
+        else:
+            fc = 2 * chi * r * d[q] * r2
+        if q == L - 1:
+            out.append((fc, 0.0, 0.0, 0.0))
+            continue
+        k = ranks_y[q + 1]
+        p = min(m, n)
+        fq = (2.0 * n * m * m - (2.0 / 3.0) * m ** 3) if m <= n else 0.0
+        fk = 2.0 * k * m * n
+        fj = float(sweeps[q]) * p * (p - 1) / 2 * 12 * m
+        out.append((float(fc), fq, fk, fj))
+    return out
+
+
+# ----------------------------------------------------------------------------- peaks / clocks
+
+def fp64_peaks(torch, stream):
+    """Measure DFMA and DMMA (mma.sync f64) peaks on this GPU (MEASURED_PEAKS.json has none)."""
+    import ctypes
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_2602_20226_b200", "lib", "libqttprobe.so"))
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    out = torch.zeros(4096, dtype=torch.float64, device="cuda")
+    res = {}
+    for name, fn, per in (("dfma", lib.qtt_probe_dfma, 256 * 16 * 8 * 2), ("dmma", lib.qtt_probe_dmma, 8 * 8 * 4 * 512)):
+        blocks, iters = sms * 4, 2000
+        fn(ctypes.c_void_p(out.data_ptr()), blocks, iters, ctypes.c_void_p(stream.cuda_stream))
+        torch.cuda.synchronize()
+        best = 0.0
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn(ctypes.c_void_p(out.data_ptr()), blocks, iters, ctypes.c_void_p(stream.cuda_stream))
+            e1.record(stream)
+            torch.cuda.synchronize()
+            best = max(best, blocks * iters * per / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+        res[name + "_tflops"] = round(best, 2)
+    return res
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + ",".join(self.FIELDS),
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0])); mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle leg
+
+def oracle_sample(kind, probs, n_members):
+    """Time the oracle, as it stands, on the host cores over a bounded sample."""
+    from oracle.zipup import zipup as ozip
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"] or [1])
+    except Exception:
+        cores = os.cpu_count()
+    n = min(n_members, len(probs))
+    t0 = time.perf_counter()
+    results = []
+    for p in probs[:n]:
+        results.append(ozip(kind, None if p.op is None else p.op.cores, p.x.cores, p.eps, p.max_rank))
+    dt = time.perf_counter() - t0
+    steps = sum(len(p.x.cores) for p in probs[:n])
+    return {"value": steps / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{n} members x {len(probs[0].x.cores)} sites of this rank's workload, {dt:.1f} s wall, "
+                      f"NumPy fp64 + LAPACK gesdd (host {os.cpu_count()} cores)"}, results
+
+
+# ----------------------------------------------------------------------------- main
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2602_20226_b200 import qtt
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+
+    subs, kind, probs, xs, ops, cfg = build_workload(args, rank)
+    mpo = kind == "matvec"
+    xd = qtt.to_device(xs)
+    od = None if ops is None else qtt.to_device(ops, mpo=mpo)
+    p0 = probs[0]
+    plan = qtt.ZipupPlan(subs, od, xd, p0.eps, p0.max_rank, sweeps=True)
+    L = xd.n_sites
+    B = xd.batch
+    summary = torch.zeros(4, dtype=torch.float64, device="cuda")
+
+    def step(events=None):
+        res = plan.run(od, xd, events=events)
+        s = qtt.summary(res)
+        if world > 1:
+            dist.all_reduce(s)
+        summary.copy_(s)
+        return res
+
+    peaks = fp64_peaks(torch, stream)
+    for _ in range(max(args.warmup, 3)):
+        res = step()
+    torch.cuda.synchronize()
+    assert int(res.status.item()) == 0, f"device status {int(res.status.item())}"
+
+    # ---------------- timed region (device time, max over ranks)
+    ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * (L + 1))] for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.25)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for k in range(args.steps):
+        step(ev_sets[k])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1) / args.steps
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+
+    # per-kernel device time of the dominant kernel (k_site) from the live events
+    site_ms = sum(ev[2 + 2 * q].elapsed_time(ev[3 + 2 * q]) for ev in ev_sets for q in range(L))
+    orth_ms = sum(ev[0].elapsed_time(ev[1]) for ev in ev_sets)
+    ranks = res.ranks.cpu().numpy()
+    sweeps = res.sweeps.cpu().numpy()
+    d = xd.d_out if kind != "matvec" else od.d_out
+    dj = xd.d_out
+    tot = np.zeros(4)
+    for b in range(B):
+        f = site_flops(kind, list(ranks[b]), xd.ranks, od.ranks if od is not None else None, d, dj, sweeps[b])
+        tot += np.sum(np.array(f), axis=0)
+    flops_alg = tot[0] + tot[1] + tot[2]
+    flops_all = flops_alg + tot[3]
+    site_s = site_ms * 1e-3 / args.steps
+    fp64_peak = max(peaks["dfma_tflops"], peaks["dmma_tflops"])
+    achieved = flops_all / site_s / 1e12
+    launches_per_step = L + 2 + (1 if kind != "truncate" else 0)   # L site kernels, a1 (x[, op]), summary
+
+    units = world * B * L
+    value = units / (ms_max * 1e-3)
+
+    # ---------------- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        hx = [c.detach().cpu().pin_memory() for c in xd.cores]
+        ho = [c.detach().cpu().pin_memory() for c in od.cores] if od is not None else []
+        hout = [c.detach().cpu().pin_memory() for c in plan.out.cores]
+        hr = torch.empty_like(plan.ranks, device="cpu").pin_memory()
+        hd = torch.empty_like(plan.delta2, device="cpu").pin_memory()
+        hn = torch.empty_like(plan.norm2, device="cpu").pin_memory()
+        h2d = sum(t.numel() * 8 for t in hx + ho)
+        d2h = sum(t.numel() * 8 for t in hout) + hr.numel() * 4 + hd.numel() * 8 + hn.numel() * 8
+
+        def e2e_step():
+            for dst, src in zip(xd.cores, hx):
+                dst.copy_(src, non_blocking=True)
+            if od is not None:
+                for dst, src in zip(od.cores, ho):
+                    dst.copy_(src, non_blocking=True)
+            r = step()
+            for dst, src in zip(hout, plan.out.cores):
+                dst.copy_(src, non_blocking=True)
+            hr.copy_(r.ranks, non_blocking=True); hd.copy_(r.delta2, non_blocking=True)
+            hn.copy_(r.norm2, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ems = torch.tensor([a0.elapsed_time(a1) / args.steps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e2e = {"value": units / (float(ems.item()) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(float(ems.item()), 3)}
+
+    # ---------------- CPU oracle baseline + sampled parity (rank 0, N=1 only)
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu, refs = oracle_sample(kind, probs, args.cpu_members)
+        from oracle import tt
+        worst = 0.0
+        for b, ref in enumerate(refs):
+            rk = [int(v) for v in ranks[b]]
+            if rk != ref["ranks"]:
+                worst = float("inf")
+                break
+            yg = qtt.member_cores(plan.out, rk, b)
+            worst = max(worst, tt.diff_norm(yg, ref["cores"]) / tt.qr_norm(ref["cores"]))
+        parity = {"members": len(refs), "max_rel_fro": worst, "ranks_equal": worst != float("inf")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": round(ms_max, 3), "higher_is_better": True,
+            "scaling": "weak" if args.workload == "cfg5" else "replicas", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators, BASELINE.json configs)",
+            "config": dict(cfg, l2="inputs %.2f GB/GPU > 126 MB L2: no flush needed" %
+                           (sum(c.numel() for c in xd.cores) * 8 / 1e9)),
+            "alg_tflops": round(world * flops_alg / (ms_max * 1e-3) / 1e12, 3),
+            "alg_tflops_note": "contraction+QR+carry flops (SURVEY.md §8(d)); Jacobi excluded",
+            "roofline": {"kernel": "k_site (a2-a7 fused site step; Jacobi-dominated)", "bound": "fp64",
+                         "achieved": round(achieved, 3), "peak": fp64_peak, "unit": "TFLOP/s",
+                         "frac": round(achieved / fp64_peak, 4), "traffic": None,
+                         "peak_source": "measured in this run by csrc/probe/peak.cu (MEASURED_PEAKS.json has no FP64)",
+                         "flops_per_step": flops_all, "kernel_ms_per_step": round(site_ms / args.steps, 3),
+                         "share_of_step": round(site_ms / args.steps / ms, 4),
+                         "flop_split": {"contract": tot[0], "qr": tot[1], "carry": tot[2], "jacobi": tot[3]},
+                         "prepass_ms_per_step": round(orth_ms / args.steps, 3)},
+            "fp64_peaks": peaks,
+            "jacobi_sweeps": {"mean": float(sweeps[:, :-1].mean()), "max": int(sweeps.max())},
+            "cpu_baseline": cpu, "parity_sample": parity, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps, "clocks": clk,
+            "summary": {"sum_delta2": float(summary[0]), "sum_norm2": float(summary[1]),
+                        "rel_trunc_est": math.sqrt(float(summary[0]) / max(float(summary[1]), 1e-300))},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle (as it stands) on the host cores, same workload/metric."""
+    if rank != 0:
+        return
+    args.members_per_gpu = max(1, args.cpu_members // 4) if args.workload == "cfg5" else 1
+    subs, kind, probs, xs, ops, cfg = build_workload(args, 0)
+    for _ in range(args.warmup):
+        oracle_sample(kind, probs, 1)
+    vals = []
+    t0 = time.perf_counter()
+    info = None
+    for _ in range(args.steps):
+        info, _ = oracle_sample(kind, probs, len(probs))
+        vals.append(info["value"])
+    dt = time.perf_counter() - t0
+    value = statistics.median(vals)
+    L = len(probs[0].x.cores)
+    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": cfg,
+            "cpu_baseline": dict(info, value=round(value, 3),
+                                 sample=f"each step: {len(probs)} members x {L} sites of the workload (oracle)"),
+            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

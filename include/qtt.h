@@ -1,0 +1,166 @@
+/* qtt.h -- C-ABI of the B200 zip-up library (libqtt.so).
+ *
+ * Hot path of arXiv 2602.20226 ("trainsum"): the decomposition / zip-up algorithm of
+ * PAPER.md §3.2 (lines 253-275) applying an einsum-style linear map to a quantics tensor
+ * train and truncating ranks while it sweeps, plus the exact operations it is checked with
+ * (Eq. einsum, inner products SPEC.md:241-249, dense conversion
+ * SPEC.md:211-219).  The paper's context-manager options become
+ * explicit arguments (eps = ``cutoff``, max_rank), as SPEC.md:416 prescribes.
+ *
+ * Conventions (all entry points):
+ *   - Every core / result pointer is a DEVICE pointer owned by the caller.  The library
+ *     never allocates on the hot path (all scratch comes from the caller's workspace) and
+ *     never frees caller memory.  Inputs are never modified.
+ *   - Layout: MPS core q is row-major (r_q, d_q, r_{q+1}); MPO core q is row-major
+ *     (w_q, d_out_q, d_in_q, w_{q+1}).  Digits are big-endian: core 0 holds
+ *     the most significant digit (Eq. quantization).
+ *   - Batches: a qtt_trains_t describes `batch` members with identical shapes; member b's
+ *     core q starts at cores[q] + b * core_elems(q) elements, where
+ *     core_elems(q) = ranks[q] * d_out[q] * (d_in[q] if n_legs == 2) * ranks[q+1].
+ *     For OUTPUT trains `ranks` are the bond CAPACITIES; every member's core is written
+ *     packed at its actual ranks inside its capacity-sized slot.
+ *   - dtype: IEEE float64 throughout (the paper's precision).
+ *   - Calls are stream-ordered on `stream` (a cudaStream_t passed as void*), asynchronous
+ *     (no host synchronisation) and reentrant; there is no global mutable state except
+ *     the thread-local error string.
+ *   - Errors: a non-QTT_OK status leaves outputs unspecified; qtt_last_error() gives a
+ *     human-readable reason for the calling thread.  Numerical failures detected on the
+ *     device (non-finite input, Jacobi non-convergence) are reported through the
+ *     `status` device word of qtt_zipup (0 = ok) because the call does not synchronise.
+ */
+#ifndef QTT_H_
+#define QTT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  QTT_OK = 0,
+  QTT_EINVAL = 1,        /* bad argument (NULL pointer, eps outside [0,1), ...)          */
+  QTT_ESHAPE = 2,        /* rank chain or extent mismatch                   */
+  QTT_ECONFORM = 3,      /* operands do not conform for the subscripts */
+  QTT_ENUMERIC = 4,      /* non-finite values / no convergence              */
+  QTT_ECAPACITY = 5,     /* output capacity or workspace too small                        */
+  QTT_EGUARD = 6,        /* dense size refused                          */
+  QTT_ECUDA = 7,         /* CUDA runtime error                                            */
+  QTT_EUNSUPPORTED = 8   /* subscript pattern or size not supported by this build         */
+} qtt_status_t;
+
+typedef struct {
+  int32_t n_sites;        /* L >= 1                                                       */
+  int32_t n_legs;         /* 1: MPS core (r, d, r');  2: MPO core (w, d_out, d_in, w')     */
+  int32_t batch;          /* B >= 1 members of identical shape                             */
+  const int32_t *d_out;   /* host [L] digit sizes (the b_q of Eq. quantization)            */
+  const int32_t *d_in;    /* host [L] input digit sizes (MPO) or NULL                       */
+  const int32_t *ranks;   /* host [L+1] bond dims (inputs) / bond capacities (outputs);
+                             ranks[0] == ranks[L] == 1                                     */
+  void *const *cores;     /* host [L] device pointers, batch-strided as described above    */
+} qtt_trains_t;
+
+/* Flags for qtt_zipup. */
+enum {
+  QTT_NO_OPERATOR_ORTH = 1u << 0  /* do not right-orthonormalise the operator (SURVEY c-A2) */
+};
+
+/* ---------------------------------------------------------------------------------------
+ * qtt_zipup_capacity -- output bond capacities for qtt_zipup (host only, no GPU work).
+ *   cap[0] = 1; cap[q+1] = min(cap[q]*d_q, w_{q+1}*r_{q+1}, max_rank>0 ? max_rank : inf);
+ *   cap[L] = 1.  (The zip-up rank after site q is k <= min(m, n) of its site matrix.)
+ *   cap: host [L+1].
+ */
+qtt_status_t qtt_zipup_capacity(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                                int32_t max_rank, int32_t *cap);
+
+/* qtt_zipup_workspace_bytes -- device scratch needed by qtt_zipup for these shapes. */
+size_t qtt_zipup_workspace_bytes(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                                 const qtt_trains_t *out);
+
+/* ---------------------------------------------------------------------------------------
+ * qtt_zipup -- y = op(x) truncated by the zip-up sweep (window N = 1).
+ *
+ *   subscripts : "ij,j->i"  op is an MPO (w, d_out, d_in, w'), x an MPS   (matrix-vector)
+ *                "i,i->i"   op is an MPS of the same digit shape as x      (Hadamard)
+ *                "i->i"     op must be NULL: pure truncation of x (PAPER.md:710 truncate)
+ *   Steps per member:
+ *     a1 right-orthonormalise every operand by Householder QR;
+ *     for q = 0..L-1:
+ *       a2 T_q[(chi,i),(w',r')] = sum_{w,r,j} G[chi,w,r] x_q[r,j,r'] op_q[w,i,j,w']
+ *          (Hadamard: j == i and op_q[w,i,i,w'] := a_q[w,i,w'])  (Eq. einsum);
+ *       a3 R = QR(T^H) when m <= n, else T itself;
+ *       a4 one-sided Jacobi SVD -> sigma (descending), U;
+ *       a5 k = min(max_rank, smallest k>=1 with sqrt(sum_{j>k} s_j^2) <= eps*||s||)
+ *          (SPEC.md:299), delta2_q = sum_{j>k} s_j^2;
+ *       a6 C_q = U[:, :k] (chi, d, k);  G <- U_k^T T_q;
+ *       a7 last site: C_{L-1} = T_{L-1};  norm2 = ||C_{L-1}||_F^2.
+ *   eps        : relative cutoff in [0, 1).       max_rank: <= 0 means unbounded.
+ *   out        : output trains, n_legs = 1, ranks[] = capacities (>= qtt_zipup_capacity).
+ *   out_ranks  : device int32 [B*(L+1)] actual ranks per member (written).
+ *   delta2     : device f64 [B*L]: discarded sum of squares of split q (last entry 0).
+ *   norm2      : device f64 [B]: ||y_b||_F^2.
+ *   diag       : optional diagnostics (NULL for none), see qtt_zipup_diag_t.
+ *   status     : device int32 [1]: 0 on success; bit 1 = non-finite value seen,
+ *                bit 2 = Jacobi did not converge (the host status cannot know: no sync).
+ *   workspace  : device scratch of >= qtt_zipup_workspace_bytes bytes, 256-byte aligned.
+ */
+typedef struct {
+  double *sigma;          /* device f64 [B*(L-1)*sigma_stride]: singular values of every site
+                             matrix, descending, zero padded; NULL to skip                    */
+  int32_t sigma_stride;
+  int32_t *sweeps;        /* device int32 [B*L]: Jacobi sweeps run at every site; NULL to skip */
+  void *const *events;    /* host [2*(L+1)] cudaEvent_t recorded on `stream`: events[0]/[1]
+                             bracket the a1 pre-pass, events[2+2q]/[3+2q] the site-q kernel;
+                             NULL to skip (used by bench.py to time the dominant kernel)     */
+} qtt_zipup_diag_t;
+
+qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                       double eps, int32_t max_rank, uint32_t flags, const qtt_trains_t *out,
+                       int32_t *out_ranks, double *delta2, double *norm2, int32_t *status,
+                       const qtt_zipup_diag_t *diag, void *workspace, size_t workspace_bytes,
+                       void *stream);
+
+/* qtt_zipup_summary -- the per-batch scalars that are all-reduced across GPUs
+ * (SURVEY.md §8(a) a8): summary4 (device f64 [4]) = [sum_b sum_q delta2, sum_b norm2,
+ * sum_b sum_q out_ranks[b][q+1] (q < L-1), B].  Deterministic fixed-order sums. */
+qtt_status_t qtt_zipup_summary(int32_t batch, int32_t n_sites, const int32_t *out_ranks,
+                               const double *delta2, const double *norm2, double *summary4, void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * qtt_einsum_exact -- exact einsum by local summation (Eq. einsum):
+ *   "ij,j->i": C_q[(w,r), i, (w',r')] = sum_j a_q[w,i,j,w'] b_q[r,j,r']
+ *   "i,i->i" : C_q[(a,b), i, (a',b')] = a_q[a,i,a'] b_q[b,i,b']
+ * Bond indices are flattened first-operand-slow (xi = mu nu).  out->ranks must equal the
+ * products of the operand ranks; out->n_legs = 1.
+ */
+qtt_status_t qtt_einsum_exact(const char *subscripts, const qtt_trains_t *a, const qtt_trains_t *b,
+                              const qtt_trains_t *out, void *stream);
+
+/* qtt_inner -- <a, b> for every member (left-to-right environments);
+ * a and b must be addition-compatible (same n_legs and digit sizes).  result: device
+ * f64 [B].  workspace: >= qtt_inner_workspace_bytes(a, b). */
+size_t qtt_inner_workspace_bytes(const qtt_trains_t *a, const qtt_trains_t *b);
+qtt_status_t qtt_inner(const qtt_trains_t *a, const qtt_trains_t *b, double *result,
+                       void *workspace, size_t workspace_bytes, void *stream);
+
+/* qtt_to_dense -- dense tensor of every member, row-major over the
+ * original (unfactorised) dimensions: leg_dim[q] (host [L], or NULL = all one dimension)
+ * names the dimension of site q's digit; digits of one dimension appear in order, most
+ * significant first.  MPS only.  out: device f64 [B * prod(d)].  Refuses with QTT_EGUARD
+ * when prod(d) > max_elems (inclusive guard; max_elems <= 0 means 2^24, SURVEY c-A30). */
+size_t qtt_to_dense_workspace_bytes(const qtt_trains_t *t);
+qtt_status_t qtt_to_dense(const qtt_trains_t *t, const int32_t *leg_dim, double *out, int64_t max_elems,
+                          void *workspace, size_t workspace_bytes, void *stream);
+
+/* Thread-local description of the last error on this thread ("" if none). */
+const char *qtt_last_error(void);
+
+/* Library version string. */
+const char *qtt_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QTT_H_ */

@@ -1,0 +1,112 @@
+// common.cuh -- shared helpers for libqtt (sm_100a, float64).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+#include <cfloat>
+
+#include "../../include/qtt.h"
+
+namespace qtt {
+
+constexpr int kThreads = 256;     // CTA size of every per-member kernel (8 warps)
+constexpr int kWarps = kThreads / 32;
+
+void set_error(const char *fmt, ...);
+qtt_status_t cuda_status(cudaError_t e, const char *what);
+
+#define QTT_CUDA_TRY(expr)                                           \
+  do {                                                               \
+    cudaError_t _e = (expr);                                         \
+    if (_e != cudaSuccess) return ::qtt::cuda_status(_e, #expr);     \
+  } while (0)
+
+// ------------------------------------------------------------------ device helpers
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum over kThreads threads; `red` is >= kWarps doubles of shared memory.
+// All threads must call it; returns the total to every thread.
+__device__ __forceinline__ double block_sum(double v, double *red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) t += red[w];   // fixed order: deterministic
+  return t;
+}
+
+// CTA-wide C = A * B (+ C if accumulate) with element accessors.  64x64 output tiles,
+// 16-deep K chunks staged in shared memory `sm` (>= 2*16*64 doubles); 256 threads,
+// each owning a 4x4 register tile (rows ty+16i, cols tx+16j: conflict-free smem reads).
+// A(m,k), B(k,n) are callables returning double; store(m,n,v) writes the result.
+template <typename FA, typename FB, typename FS>
+__device__ void cta_gemm(int M, int N, int K, FA A, FB B, FS store, double *sm) {
+  double *As = sm;            // [16][64]
+  double *Bs = sm + 16 * 64;  // [16][64]
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  for (int m0 = 0; m0 < M; m0 += 64) {
+    for (int n0 = 0; n0 < N; n0 += 64) {
+      double acc[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+      for (int k0 = 0; k0 < K; k0 += 16) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int idx = tid + e * kThreads;      // 0..1023
+          const int kk = idx >> 6, mm = idx & 63;
+          const int gm = m0 + mm, gk = k0 + kk, gn = n0 + mm;
+          As[kk * 64 + mm] = (gm < M && gk < K) ? A(gm, gk) : 0.0;
+          Bs[kk * 64 + mm] = (gn < N && gk < K) ? B(gk, gn) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+          double a[4], b[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a[i] = As[kk * 64 + ty + 16 * i];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) b[j] = Bs[kk * 64 + tx + 16 * j];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int gm = m0 + ty + 16 * i, gn = n0 + tx + 16 * j;
+          if (gm < M && gn < N) store(gm, gn, acc[i][j]);
+        }
+    }
+  }
+}
+
+// LAPACK dlarfg convention: x = [alpha; x2], ||x2||^2 = xnorm2.  Returns tau and beta and
+// the scale 1/(alpha - beta) for v2 = x2 * scale (v0 = 1 implicit).  H x = [beta; 0].
+__device__ __forceinline__ void householder(double alpha, double xnorm2, double &tau, double &beta,
+                                            double &scale) {
+  if (xnorm2 == 0.0) {
+    tau = 0.0; beta = alpha; scale = 0.0;
+    return;
+  }
+  const double nrm = sqrt(alpha * alpha + xnorm2);
+  beta = (alpha >= 0.0) ? -nrm : nrm;
+  tau = (beta - alpha) / beta;
+  scale = 1.0 / (alpha - beta);
+}
+
+}  // namespace qtt

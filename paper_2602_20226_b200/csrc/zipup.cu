@@ -1,0 +1,751 @@
+// zipup.cu -- the zip-up hot path (§3.2).
+//
+// Small-member path: one CTA (256 threads, 1 per SM) owns one batch member at a time.
+//   k_orth : a1 right-orthonormalisation of one operand, all sites right-to-left (Householder
+//            QR with explicit Q, R absorbed into the left neighbour).
+//   k_site : one site step q for every member: a2 contraction -> T (L2-resident scratch),
+//            a3 incremental Householder QR of T^H (R in shared memory), a4 one-sided Jacobi
+//            SVD on R^H in shared memory (warp-shuffle reductions, round-robin ordering),
+//            a5 tail-sum truncation, a6 emit U_k and carry G = U_k^T T, a7 last site.
+// All ranks live on the device (int arrays); no host synchronisation anywhere.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <string.h>
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace qtt {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+qtt_status_t cuda_status(cudaError_t e, const char *what) {
+  set_error("CUDA error %s in %s", cudaGetErrorString(e), what);
+  return QTT_ECUDA;
+}
+
+enum Kind { MATVEC = 0, HADAMARD = 1, TRUNCATE = 2 };
+
+constexpr int kMaxSites = 64;
+constexpr int kSmall = 128;            // max rows m (and p) of a site matrix on this path
+constexpr int kLdA = kSmall + 1;       // leading dim of the shared R / Jacobi matrix (odd: no bank conflicts)
+constexpr int kBS = 32;                // rows of T^H per incremental-QR block
+constexpr int kLdB = kSmall + 1;
+constexpr int kBkDoubles = 4352;       // >= kBS*kLdB, >= 2*16*64 GEMM staging, >= staged MPO core
+constexpr int kSiteSmemDoubles = kSmall * kLdA + kBkDoubles + kSmall + 8 + 8;
+constexpr size_t kSiteSmemBytes = kSiteSmemDoubles * sizeof(double) + (kSmall + 8) * sizeof(int);
+constexpr int kOrthSmemDoubles = 26000;  // a1 staging budget (~203 KB)
+constexpr int kJacobiMaxSweeps = 60;
+
+enum StatusBits { ST_NONFINITE = 1, ST_NOCONV = 2 };
+
+// ======================================================================= a1: pre-pass
+
+struct OrthArgs {
+  int L, orth, shared;
+  int legs[kMaxSites];
+  int r0[kMaxSites + 1];
+  long long off[kMaxSites + 1];       // per-member offsets (elements) of each core in dst
+  const double *src[kMaxSites];       // batch-strided input cores
+  double *dst; long long dst_bs;
+  int *rk;                            // [B][L+1] ranks after a1
+};
+
+// Householder QR of the c x r column-major matrix Ms (ld = c) in shared memory:
+// reflectors below the diagonal, R on and above it, tau[j].  LAPACK dgeqr2 order.
+__device__ void smem_geqr2(double *Ms, int c, int r, double *tau, double *red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int k = min(c, r);
+  for (int j = 0; j < k; ++j) {
+    double *cj = Ms + (size_t)j * c;
+    if (warp == 0) {
+      double s = 0.0;
+      for (int i = j + 1 + lane; i < c; i += 32) s += cj[i] * cj[i];
+      s = warp_sum(s);
+      double t, beta, scale;
+      householder(cj[j], s, t, beta, scale);
+      for (int i = j + 1 + lane; i < c; i += 32) cj[i] *= scale;
+      __syncwarp();
+      if (lane == 0) { tau[j] = t; cj[j] = beta; }
+    }
+    __syncthreads();
+    const double t = tau[j];
+    if (t != 0.0) {
+      for (int col = j + 1 + warp; col < r; col += kWarps) {
+        double *cc = Ms + (size_t)col * c;
+        double s = (lane == 0) ? cc[j] : 0.0;
+        for (int i = j + 1 + lane; i < c; i += 32) s += cj[i] * cc[i];
+        s = warp_sum(s) * t;
+        if (lane == 0) cc[j] -= s;
+        for (int i = j + 1 + lane; i < c; i += 32) cc[i] -= s * cj[i];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Form the first k columns of Q in place from the reflectors (LAPACK dorg2r).
+__device__ void smem_org2r(double *Ms, int c, int k, const double *tau) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = k - 1; j >= 0; --j) {
+    double *cj = Ms + (size_t)j * c;
+    const double t = tau[j];
+    if (j < k - 1 && t != 0.0) {
+      for (int col = j + 1 + warp; col < k; col += kWarps) {
+        double *cc = Ms + (size_t)col * c;
+        double s = (lane == 0) ? cc[j] : 0.0;   // v_j = 1
+        for (int i = j + 1 + lane; i < c; i += 32) s += cj[i] * cc[i];
+        s = warp_sum(s) * t;
+        if (lane == 0) cc[j] -= s;
+        for (int i = j + 1 + lane; i < c; i += 32) cc[i] -= s * cj[i];
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < c; i += kThreads) {
+      if (i > j) cj[i] *= -t;
+      else if (i == j) cj[i] = 1.0 - t;
+      else cj[i] = 0.0;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_orth(OrthArgs a) {
+  extern __shared__ double smem[];
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int L = a.L;
+  double *base = a.dst + (size_t)b * a.dst_bs;
+  // copy every core of member b into the workspace (inputs are never modified)
+  for (int q = 0; q < L; ++q) {
+    const long long n = (long long)a.r0[q] * a.legs[q] * a.r0[q + 1];
+    const double *src = a.src[q] + (a.shared ? 0 : (size_t)b * n);
+    double *dst = base + a.off[q];
+    for (long long i = tid; i < n; i += kThreads) dst[i] = src[i];
+  }
+  int *rk = a.rk + (size_t)b * (L + 1);
+  for (int q = tid; q <= L; q += kThreads) rk[q] = a.r0[q];
+  __syncthreads();
+  if (!a.orth) return;
+  double *tau = smem;                  // [kSmall*2]
+  double *red = tau + 2 * kSmall;      // [16]
+  double *Ms = red + 16;
+  int rr = 1;                          // current right rank of core q
+  for (int q = L - 1; q >= 1; --q) {
+    const int r = a.r0[q];
+    const int legs = a.legs[q];
+    const int c = legs * rr;
+    const int k = min(c, r);
+    double *core = base + a.off[q];
+    double *Rsm = Ms + (size_t)c * r;                 // k x r
+    double *Psm = Rsm + (size_t)k * r;                // rows_prev x r
+    // M^T (c x r, column-major): column aa = row aa of the core (contiguous)
+    for (int i = tid; i < c * r; i += kThreads) Ms[i] = core[i];
+    __syncthreads();
+    smem_geqr2(Ms, c, r, tau, red);
+    for (int i = tid; i < k * r; i += kThreads) {
+      const int kk = i / r, aa = i % r;
+      Rsm[i] = (aa >= kk) ? Ms[(size_t)aa * c + kk] : 0.0;
+    }
+    __syncthreads();
+    smem_org2r(Ms, c, k, tau);
+    // core q <- Q^T (k x c): row kk = column kk of Q
+    for (int i = tid; i < k * c; i += kThreads) core[i] = Ms[i];
+    // core q-1 <- core q-1 x_last R^T
+    const int rows = a.r0[q - 1] * a.legs[q - 1];
+    double *prev = base + a.off[q - 1];
+    for (int i = tid; i < rows * r; i += kThreads) Psm[i] = prev[i];
+    __syncthreads();
+    for (int i = tid; i < rows * k; i += kThreads) {
+      const int row = i / k, kk = i % k;
+      double s = 0.0;
+      for (int aa = kk; aa < r; ++aa) s = fma(Psm[row * r + aa], Rsm[kk * r + aa], s);
+      prev[i] = s;
+    }
+    if (tid == 0) rk[q] = k;
+    rr = k;
+    __syncthreads();
+  }
+}
+
+// ======================================================================= a2..a7: site step
+
+struct SiteArgs {
+  int q, L, kind, d, dj, shared_op;
+  const double *Xq; long long Xq_bs;     // orthonormalised x core q (workspace)
+  const double *Oq; long long Oq_bs;     // orthonormalised operator core q (workspace)
+  const int *xr; const int *orr;         // [B][L+1] operand ranks after a1
+  int *yr;                               // [B][L+1] output ranks
+  double *G; long long G_bs;             // carry (chi, w, r)
+  double *T; long long T_bs;             // site matrix (m x n), row-major
+  double *X; long long X_bs;             // state-contraction intermediate
+  double *Cq; long long Cq_bs;           // output core q slot
+  double *delta2, *norm2, *sigma;
+  int sigma_stride;
+  int *sweeps;
+  int *status;
+  double eps;
+  int max_rank;
+};
+
+// a3: R (m x m, upper, row-major in Rs with ld kLdA) of T^H, T row-major m x n, m <= n.
+// Incremental Householder over row blocks of T^H: QR([R; block]) for each block of kBS
+// columns of T; the reflector of column j touches R[j][j] and the block column only.
+__device__ void qr_of_TH(const double *T, int m, int n, double *Rs, double *Bk, double *scal) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < m * kLdA; i += kThreads) Rs[i] = 0.0;
+  for (int c0 = 0; c0 < n; c0 += kBS) {
+    const int nb = min(kBS, n - c0);
+    __syncthreads();
+    for (int idx = tid; idx < kBS * m; idx += kThreads) {
+      const int j = idx / kBS, i = idx % kBS;          // coalesced along i (columns of T)
+      Bk[i * kLdB + j] = (i < nb) ? T[(size_t)j * n + c0 + i] : 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < m; ++j) {
+      if (warp == 0) {
+        const double v = Bk[lane * kLdB + j];          // kBS == 32: one row per lane
+        const double xn2 = warp_sum(v * v);
+        double t, beta, scale;
+        householder(Rs[j * kLdA + j], xn2, t, beta, scale);
+        Bk[lane * kLdB + j] = v * scale;
+        __syncwarp();
+        if (lane == 0) { scal[0] = t; Rs[j * kLdA + j] = beta; }
+      }
+      __syncthreads();
+      const double t = scal[0];
+      if (t != 0.0) {
+        for (int col = j + 1 + tid; col < m; col += kThreads) {
+          double s = Rs[j * kLdA + col];
+#pragma unroll 8
+          for (int i = 0; i < kBS; ++i) s = fma(Bk[i * kLdB + j], Bk[i * kLdB + col], s);
+          s *= t;
+          Rs[j * kLdA + col] -= s;
+#pragma unroll 8
+          for (int i = 0; i < kBS; ++i) Bk[i * kLdB + col] = fma(-s, Bk[i * kLdB + j], Bk[i * kLdB + col]);
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// a4: one-sided (Hestenes) Jacobi on the columns of A (m rows, p columns, column j at
+// A + j*kLdA), cyclic round-robin parallel ordering, one warp per column pair, warp-shuffle
+// dot products.  Converged when every pair satisfies |a_i.a_j| <= m*eps*|a_i||a_j|.
+// Returns the number of sweeps (>= kJacobiMaxSweeps means not converged).
+__device__ int jacobi_smem(double *A, int m, int p, int *flag) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int P = p + (p & 1);
+  const double tol = (double)max(m, 1) * DBL_EPSILON;
+  int sweep = 0;
+  for (; sweep < kJacobiMaxSweeps; ++sweep) {
+    if (threadIdx.x == 0) *flag = 0;
+    __syncthreads();
+    for (int rd = 0; rd < P - 1; ++rd) {
+      for (int t = warp; t < P / 2; t += kWarps) {
+        const int i = (t == 0) ? 0 : 1 + (t - 1 + rd) % (P - 1);
+        const int j = 1 + (P - 2 - t + rd) % (P - 1);
+        if (i >= p || j >= p) continue;
+        double *ai = A + (size_t)i * kLdA, *aj = A + (size_t)j * kLdA;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int row = lane; row < m; row += 32) {
+          const double x = ai[row], y = aj[row];
+          al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
+        }
+        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+        if (ga != 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double tt = (fabs(zeta) > 1e150) ? 0.5 / zeta
+                                                 : copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          const double cs = 1.0 / sqrt(fma(tt, tt, 1.0)), sn = cs * tt;
+          for (int row = lane; row < m; row += 32) {
+            const double x = ai[row], y = aj[row];
+            ai[row] = fma(cs, x, -sn * y);
+            aj[row] = fma(sn, x, cs * y);
+          }
+          if (lane == 0) *flag = 1;
+        }
+      }
+      __syncthreads();
+    }
+    const int rot = *flag;
+    __syncthreads();
+    if (!rot) break;
+  }
+  return sweep;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_site(SiteArgs a) {
+  extern __shared__ double smem[];
+  double *Rs = smem;                         // kSmall x kLdA: R (row-major) == A = R^T (col-major)
+  double *Bk = Rs + kSmall * kLdA;           // QR block / GEMM staging / staged MPO core
+  double *sg = Bk + kBkDoubles;              // sigma^2 per column
+  double *red = sg + kSmall;                 // block-reduction scratch
+  double *scal = red + 8;                    // scalars
+  int *perm = reinterpret_cast<int *>(scal + 8);
+  int *iflag = perm + kSmall;
+
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int L = a.L, L1 = L + 1, q = a.q;
+  const int chi = (q == 0) ? 1 : a.yr[(size_t)b * L1 + q];
+  const int r = a.xr[(size_t)b * L1 + q], r2 = a.xr[(size_t)b * L1 + q + 1];
+  int w = 1, w2 = 1;
+  if (a.kind != TRUNCATE) { w = a.orr[(size_t)b * L1 + q]; w2 = a.orr[(size_t)b * L1 + q + 1]; }
+  const int d = a.d, dj = a.dj;
+  const int m = chi * d, n = w2 * r2;
+  double *G = a.G + (size_t)b * a.G_bs;
+  double *T = a.T + (size_t)b * a.T_bs;
+  double *X = a.X + (size_t)b * a.X_bs;
+  const double *Xq = a.Xq + (size_t)b * a.Xq_bs;
+  const double *Oq = a.Oq ? a.Oq + (a.shared_op ? 0 : (size_t)b * a.Oq_bs) : nullptr;
+  double *Cq = a.Cq + (size_t)b * a.Cq_bs;
+
+  if (q == 0) {
+    if (tid == 0) G[0] = 1.0;                // G_0 = [[[1]]]
+    __syncthreads();
+  }
+  // ---------------------------------------------------------------- a2: contraction
+  if (a.kind == MATVEC) {
+    const int M = chi * w, K = r, N = dj * r2;     // X[(c,w),(j,r')] = G[(c,w),r] x_q[r,(j,r')]
+    cta_gemm(M, N, K, [&](int i, int k) { return G[(size_t)i * K + k]; },
+             [&](int k, int j) { return Xq[(size_t)k * N + j]; },
+             [&](int i, int j, double v) { X[(size_t)i * N + j] = v; }, Bk);
+    __syncthreads();
+    const int wsz = w * d * dj * w2;
+    for (int i = tid; i < wsz; i += kThreads) Bk[i] = Oq[i];
+    __syncthreads();
+    // T[c,i,w',r'] = sum_{w,j} X[c,w,j,r'] W[w,i,j,w']
+    for (int idx = tid; idx < m * n; idx += kThreads) {
+      const int rr2 = idx % r2;
+      int t1 = idx / r2;
+      const int ww2 = t1 % w2; t1 /= w2;
+      const int ii = t1 % d, c = t1 / d;
+      double s = 0.0;
+      for (int ww = 0; ww < w; ++ww)
+        for (int jj = 0; jj < dj; ++jj)
+          s = fma(X[((size_t)(c * w + ww) * dj + jj) * r2 + rr2], Bk[((ww * d + ii) * dj + jj) * w2 + ww2], s);
+      T[idx] = s;
+    }
+  } else if (a.kind == HADAMARD) {
+    const int M = chi * w, K = r, N = d * r2;      // X[(c,a),(i,b')] = G[(c,a),b] x_q[b,(i,b')]
+    cta_gemm(M, N, K, [&](int i, int k) { return G[(size_t)i * K + k]; },
+             [&](int k, int j) { return Xq[(size_t)k * N + j]; },
+             [&](int i, int j, double v) { X[(size_t)i * N + j] = v; }, Bk);
+    __syncthreads();
+    for (int ci = 0; ci < chi * d; ++ci) {         // T[c,i,a',b'] = sum_a A[a,i,a'] X[c,a,i,b']
+      const int c = ci / d, ii = ci % d;
+      cta_gemm(w2, r2, w, [&](int a2, int aa) { return Oq[((size_t)aa * d + ii) * w2 + a2]; },
+               [&](int aa, int bb) { return X[((size_t)(c * w + aa) * d + ii) * r2 + bb]; },
+               [&](int a2, int bb, double v) { T[((size_t)(c * d + ii) * w2 + a2) * r2 + bb] = v; }, Bk);
+    }
+  } else {
+    const int M = chi, K = r, N = d * r2;          // T[c,(i,r')] = G[c,r] x_q[r,(i,r')]
+    cta_gemm(M, N, K, [&](int i, int k) { return G[(size_t)i * K + k]; },
+             [&](int k, int j) { return Xq[(size_t)k * N + j]; },
+             [&](int i, int j, double v) { T[(size_t)i * N + j] = v; }, Bk);
+  }
+  __syncthreads();
+
+  // ---------------------------------------------------------------- a7: last site
+  if (q == L - 1) {
+    double s = 0.0;
+    for (int i = tid; i < m; i += kThreads) { const double v = T[i]; Cq[i] = v; s = fma(v, v, s); }
+    s = block_sum(s, red);
+    if (tid == 0) {
+      if (a.sweeps) a.sweeps[(size_t)b * L + q] = 0;
+      a.norm2[b] = s;
+      a.delta2[(size_t)b * L + q] = 0.0;
+      a.yr[(size_t)b * L1 + L] = 1;
+      if (L == 1) a.yr[(size_t)b * L1] = 1;
+      if (!isfinite(s)) atomicOr(a.status, ST_NONFINITE);
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------------- a3: QR
+  int p;
+  if (m <= n) {
+    p = m;
+    qr_of_TH(T, m, n, Rs, Bk, scal);               // A = R^T: column j of A = row j of R
+  } else {
+    p = n;                                         // A = T (m x n): column j = T[:, j]
+    for (int idx = tid; idx < m * n; idx += kThreads) {
+      const int row = idx / n, j = idx % n;
+      Rs[(size_t)j * kLdA + row] = T[idx];
+    }
+  }
+  __syncthreads();
+
+  // ---------------------------------------------------------------- a4: Jacobi SVD
+  const int sweeps = jacobi_smem(Rs, m, p, iflag);
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int j = warp; j < p; j += kWarps) {
+    double s = 0.0;
+    for (int row = lane; row < m; row += 32) { const double v = Rs[(size_t)j * kLdA + row]; s = fma(v, v, s); }
+    s = warp_sum(s);
+    if (lane == 0) {
+      if (!isfinite(s)) { atomicOr(a.status, ST_NONFINITE); s = 0.0; }   // keep the sort well-defined
+      sg[j] = s;
+    }
+  }
+  __syncthreads();
+  for (int j = tid; j < p; j += kThreads) {         // descending order, ties by index
+    const double sj = sg[j];
+    int rank = 0;
+    for (int l = 0; l < p; ++l) rank += (sg[l] > sj) || (sg[l] == sj && l < j);
+    perm[rank] = j;
+  }
+  __syncthreads();
+
+  // ---------------------------------------------------------------- a5: truncation rule
+  if (tid == 0) {
+    double *tail = Bk;                             // tail[k] = sum_{j>=k} s_j^2, smallest first
+    double acc = 0.0;
+    tail[p] = 0.0;
+    for (int jj = p - 1; jj >= 0; --jj) { acc += sg[perm[jj]]; tail[jj] = acc; }
+    const double tot = acc;
+    int k = p;
+    const double tau = a.eps * a.eps * tot;
+    for (int kk = 1; kk <= p; ++kk)
+      if (tail[kk] <= tau) { k = kk; break; }
+    if (a.max_rank > 0) k = min(k, a.max_rank);
+    if (tot == 0.0) k = 1;
+    k = max(k, 1);
+    scal[1] = (double)k;
+    scal[2] = tail[k];
+    if (!isfinite(tot)) atomicOr(a.status, ST_NONFINITE);
+    if (sweeps >= kJacobiMaxSweeps) atomicOr(a.status, ST_NOCONV);
+  }
+  __syncthreads();
+  const int k = (int)scal[1];
+
+  // ---------------------------------------------------------------- a6: emit + carry
+  for (int idx = tid; idx < k * m; idx += kThreads) {   // normalise kept columns: U = A V / sigma
+    const int kk = idx / m, row = idx % m;
+    const int j = perm[kk];
+    const double s2 = sg[j];
+    double *col = Rs + (size_t)j * kLdA;
+    col[row] = (s2 > 0.0) ? col[row] / sqrt(s2) : (row == kk ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  for (int idx = tid; idx < m * k; idx += kThreads) {   // C_q = U[:, :k] as (chi, d, k)
+    const int row = idx / k, kk = idx % k;
+    Cq[idx] = Rs[(size_t)perm[kk] * kLdA + row];
+  }
+  if (a.sigma) {
+    double *sgo = a.sigma + ((size_t)b * (L - 1) + q) * a.sigma_stride;
+    for (int jj = tid; jj < a.sigma_stride; jj += kThreads) sgo[jj] = (jj < p) ? sqrt(sg[perm[jj]]) : 0.0;
+  }
+  if (tid == 0) {
+    if (a.sweeps) a.sweeps[(size_t)b * L + q] = sweeps;
+    a.yr[(size_t)b * L1 + q + 1] = k;
+    if (q == 0) a.yr[(size_t)b * L1] = 1;
+    a.delta2[(size_t)b * L + q] = scal[2];
+  }
+  // G_{q+1}[kk][col] = sum_row U[row][kk] T[row][col]   (k x n) = diag(s_k) V_k^H
+  cta_gemm(k, n, m, [&](int kk, int row) { return Rs[(size_t)perm[kk] * kLdA + row]; },
+           [&](int row, int col) { return T[(size_t)row * n + col]; },
+           [&](int kk, int col, double v) { G[(size_t)kk * n + col] = v; }, Bk);
+}
+
+// ======================================================================= host side
+
+struct Shape {
+  int L = 0, B = 0, kind = 0, shared_op = 0;
+  std::vector<int> d, dj, xr, orr, cap;
+  std::vector<long long> xoff, ooff;
+  long long xo_elems = 0, oo_elems = 0, g_elems = 1, t_elems = 1, x_elems = 1;
+};
+
+static int parse_kind(const char *s, const qtt_trains_t *op) {
+  if (s == nullptr || strcmp(s, "i->i") == 0) return op ? -1 : TRUNCATE;
+  if (strcmp(s, "ij,j->i") == 0) return MATVEC;
+  if (strcmp(s, "i,i->i") == 0) return HADAMARD;
+  return -2;
+}
+
+static long long round4(long long v) { return (v + 3) & ~3LL; }
+
+static qtt_status_t analyse(const char *subs, const qtt_trains_t *op, const qtt_trains_t *x,
+                           int32_t max_rank, Shape &S) {
+  if (!x) { set_error("x is NULL"); return QTT_EINVAL; }
+  const int kind = parse_kind(subs, op);
+  if (kind == -2) { set_error("unsupported subscripts '%s'", subs); return QTT_EUNSUPPORTED; }
+  if (kind == -1) { set_error("subscripts 'i->i' take no operator"); return QTT_EINVAL; }
+  if (kind != TRUNCATE && !op) { set_error("operator is NULL"); return QTT_EINVAL; }
+  const int L = x->n_sites;
+  if (L < 1 || L > kMaxSites) { set_error("n_sites %d outside [1,%d]", L, kMaxSites); return QTT_EUNSUPPORTED; }
+  if (x->n_legs != 1) { set_error("x must be an MPS (n_legs 1)"); return QTT_ESHAPE; }
+  if (x->batch < 1) { set_error("batch < 1"); return QTT_EINVAL; }
+  if (!x->d_out || !x->ranks || !x->cores) { set_error("x has NULL arrays"); return QTT_EINVAL; }
+  if (x->ranks[0] != 1 || x->ranks[L] != 1) { set_error("x boundary ranks must be 1"); return QTT_ESHAPE; }
+  S.L = L; S.B = x->batch; S.kind = kind;
+  S.d.assign(L, 0); S.dj.assign(L, 0);
+  S.xr.assign(x->ranks, x->ranks + L + 1);
+  S.orr.assign(L + 1, 1);
+  for (int q = 0; q < L; ++q) {
+    if (x->d_out[q] < 1 || x->ranks[q + 1] < 1) { set_error("x site %d: bad extent", q); return QTT_ESHAPE; }
+  }
+  if (kind != TRUNCATE) {
+    if (op->n_sites != L) { set_error("operator has %d sites, x has %d", op->n_sites, L); return QTT_ECONFORM; }
+    if (op->batch != 1 && op->batch != x->batch) { set_error("operator batch must be 1 or x batch"); return QTT_EINVAL; }
+    if (!op->d_out || !op->ranks || !op->cores) { set_error("operator has NULL arrays"); return QTT_EINVAL; }
+    if (op->ranks[0] != 1 || op->ranks[L] != 1) { set_error("operator boundary ranks must be 1"); return QTT_ESHAPE; }
+    S.shared_op = (op->batch == 1 && x->batch > 1);
+    S.orr.assign(op->ranks, op->ranks + L + 1);
+    if (kind == MATVEC) {
+      if (op->n_legs != 2 || !op->d_in) { set_error("'ij,j->i' needs an MPO operator"); return QTT_ESHAPE; }
+      for (int q = 0; q < L; ++q) {
+        if (op->d_in[q] != x->d_out[q]) {
+          set_error("conformance: letter 'j' misaligned at core %d (%d vs %d)", q, op->d_in[q], x->d_out[q]);
+          return QTT_ECONFORM;
+        }
+        S.d[q] = op->d_out[q]; S.dj[q] = op->d_in[q];
+      }
+    } else {
+      if (op->n_legs != 1) { set_error("'i,i->i' needs two MPS operands"); return QTT_ESHAPE; }
+      for (int q = 0; q < L; ++q) {
+        if (op->d_out[q] != x->d_out[q]) {
+          set_error("conformance: letter 'i' misaligned at core %d (%d vs %d)", q, op->d_out[q], x->d_out[q]);
+          return QTT_ECONFORM;
+        }
+        S.d[q] = S.dj[q] = x->d_out[q];
+      }
+    }
+  } else {
+    for (int q = 0; q < L; ++q) S.d[q] = S.dj[q] = x->d_out[q];
+  }
+  // capacities
+  S.cap.assign(L + 1, 1);
+  for (int q = 0; q < L; ++q) {
+    long long c = (long long)S.cap[q] * S.d[q];
+    c = std::min<long long>(c, (long long)S.orr[q + 1] * S.xr[q + 1]);
+    if (max_rank > 0) c = std::min<long long>(c, max_rank);
+    S.cap[q + 1] = (q == L - 1) ? 1 : (int)c;
+  }
+  // workspace geometry (per member, elements)
+  S.xoff.assign(L + 1, 0); S.ooff.assign(L + 1, 0);
+  for (int q = 0; q < L; ++q) {
+    S.xoff[q + 1] = S.xoff[q] + (long long)S.xr[q] * S.dj[q] * S.xr[q + 1];
+    long long oe = 0;
+    if (kind == MATVEC) oe = (long long)S.orr[q] * S.d[q] * S.dj[q] * S.orr[q + 1];
+    else if (kind == HADAMARD) oe = (long long)S.orr[q] * S.d[q] * S.orr[q + 1];
+    S.ooff[q + 1] = S.ooff[q] + oe;
+  }
+  S.xo_elems = round4(S.xoff[L]);
+  S.oo_elems = round4(S.ooff[L]);
+  for (int q = 0; q < L; ++q) {
+    const long long m = (long long)S.cap[q] * S.d[q];
+    const long long n = (long long)S.orr[q + 1] * S.xr[q + 1];
+    S.g_elems = std::max(S.g_elems, (long long)S.cap[q] * S.orr[q] * S.xr[q]);
+    S.g_elems = std::max(S.g_elems, (long long)S.cap[q + 1] * n);
+    S.t_elems = std::max(S.t_elems, m * n);
+    if (kind == MATVEC) S.x_elems = std::max(S.x_elems, (long long)S.cap[q] * S.orr[q] * S.dj[q] * S.xr[q + 1]);
+    if (kind == HADAMARD) S.x_elems = std::max(S.x_elems, (long long)S.cap[q] * S.orr[q] * S.d[q] * S.xr[q + 1]);
+  }
+  S.g_elems = round4(S.g_elems); S.t_elems = round4(S.t_elems); S.x_elems = round4(S.x_elems);
+  return QTT_OK;
+}
+
+static qtt_status_t check_small_path(const Shape &S) {
+  for (int q = 0; q < S.L; ++q) {
+    const long long m = (long long)S.cap[q] * S.d[q];
+    if (m > kSmall) {
+      set_error("site %d: site matrix has %lld rows > %d (large-member path not in this build)", q, m, kSmall);
+      return QTT_EUNSUPPORTED;
+    }
+    if (S.kind == MATVEC && (long long)S.orr[q] * S.d[q] * S.dj[q] * S.orr[q + 1] > kBkDoubles) {
+      set_error("site %d: operator core too large to stage", q);
+      return QTT_EUNSUPPORTED;
+    }
+  }
+  // a1 staging budget for both operands
+  for (int pass = 0; pass < 2; ++pass) {
+    const std::vector<int> &rk = pass == 0 ? S.xr : S.orr;
+    if (pass == 1 && S.kind == TRUNCATE) break;
+    int rr = 1;
+    for (int q = S.L - 1; q >= 1; --q) {
+      const int legs = (pass == 0) ? S.dj[q] : (S.kind == MATVEC ? S.d[q] * S.dj[q] : S.d[q]);
+      const int legsp = (pass == 0) ? S.dj[q - 1] : (S.kind == MATVEC ? S.d[q - 1] * S.dj[q - 1] : S.d[q - 1]);
+      const long long c = (long long)legs * rr, r = rk[q], k = std::min<long long>(c, r);
+      const long long need = 2 * kSmall + 16 + c * r + k * r + (long long)rk[q - 1] * legsp * r;
+      if (need > kOrthSmemDoubles || r > 2 * kSmall) {
+        set_error("a1: core %d of operand %d too large for the shared-memory QR (%lld doubles)", q, pass, need);
+        return QTT_EUNSUPPORTED;
+      }
+      rr = (int)k;
+    }
+  }
+  return QTT_OK;
+}
+
+struct WsLayout {
+  size_t xo, oo, g, t, x, xr, orr, total;
+};
+
+static WsLayout layout(const Shape &S) {
+  WsLayout w;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+  w.xo = take(sizeof(double) * S.xo_elems * S.B);
+  w.oo = take(sizeof(double) * S.oo_elems * (S.shared_op ? 1 : S.B));
+  w.g = take(sizeof(double) * S.g_elems * S.B);
+  w.t = take(sizeof(double) * S.t_elems * S.B);
+  w.x = take(sizeof(double) * S.x_elems * S.B);
+  w.xr = take(sizeof(int) * (S.L + 1) * S.B);
+  w.orr = take(sizeof(int) * (S.L + 1) * S.B);
+  w.total = off;
+  return w;
+}
+
+}  // namespace qtt
+
+using namespace qtt;
+
+extern "C" {
+
+const char *qtt_last_error(void) { return qtt::g_err; }
+const char *qtt_version(void) { return "libqtt 0.1 (sm_100a, fp64 zip-up small-member path)"; }
+
+qtt_status_t qtt_zipup_capacity(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                                int32_t max_rank, int32_t *cap) {
+  Shape S;
+  qtt_status_t st = analyse(subscripts, op, x, max_rank, S);
+  if (st != QTT_OK) return st;
+  if (!cap) { set_error("cap is NULL"); return QTT_EINVAL; }
+  for (int q = 0; q <= S.L; ++q) cap[q] = S.cap[q];
+  return QTT_OK;
+}
+
+size_t qtt_zipup_workspace_bytes(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                                 const qtt_trains_t *out) {
+  (void)out;
+  Shape S;
+  if (analyse(subscripts, op, x, 0, S) != QTT_OK) return 0;
+  return layout(S).total;
+}
+
+qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x, double eps,
+                       int32_t max_rank, uint32_t flags, const qtt_trains_t *out, int32_t *out_ranks,
+                       double *delta2, double *norm2, int32_t *status, const qtt_zipup_diag_t *diag,
+                       void *workspace, size_t workspace_bytes, void *stream) {
+  double *sigma = diag ? diag->sigma : nullptr;
+  const int sigma_stride = diag ? diag->sigma_stride : 0;
+  int *sweeps = diag ? diag->sweeps : nullptr;
+  void *const *events = diag ? diag->events : nullptr;
+  g_err[0] = 0;
+  if (!(eps >= 0.0 && eps < 1.0)) { set_error("eps %g outside [0,1)", eps); return QTT_EINVAL; }
+  Shape S;
+  qtt_status_t st = analyse(subscripts, op, x, max_rank, S);
+  if (st != QTT_OK) return st;
+  if (!out || !out->cores || !out->ranks || !out_ranks || !delta2 || !norm2 || !status) {
+    set_error("NULL output argument");
+    return QTT_EINVAL;
+  }
+  if (out->n_sites != S.L || out->batch != S.B || out->n_legs != 1) {
+    set_error("output train shape mismatch");
+    return QTT_ESHAPE;
+  }
+  for (int q = 0; q <= S.L; ++q) {
+    if (out->ranks[q] < S.cap[q]) {
+      set_error("output capacity %d at bond %d below required %d", out->ranks[q], q, S.cap[q]);
+      return QTT_ECAPACITY;
+    }
+  }
+  for (int q = 0; q < S.L; ++q) {
+    if (out->d_out[q] != S.d[q]) { set_error("output digit size mismatch at core %d", q); return QTT_ESHAPE; }
+  }
+  if (sigma && sigma_stride < 1) { set_error("sigma_stride < 1"); return QTT_EINVAL; }
+  st = check_small_path(S);
+  if (st != QTT_OK) return st;
+  const WsLayout W = layout(S);
+  if (workspace_bytes < W.total || !workspace) {
+    set_error("workspace %zu bytes < required %zu", workspace_bytes, W.total);
+    return QTT_ECAPACITY;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  char *ws = (char *)workspace;
+  double *Xo = (double *)(ws + W.xo), *Oo = (double *)(ws + W.oo), *G = (double *)(ws + W.g);
+  double *T = (double *)(ws + W.t), *Xb = (double *)(ws + W.x);
+  int *xr = (int *)(ws + W.xr), *orr = (int *)(ws + W.orr);
+
+  static bool attr_done = false;
+  if (!attr_done) {
+    QTT_CUDA_TRY(cudaFuncSetAttribute(k_site, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSiteSmemBytes));
+    QTT_CUDA_TRY(cudaFuncSetAttribute(k_orth, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(kOrthSmemDoubles * sizeof(double))));
+    attr_done = true;
+  }
+  QTT_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), s));
+
+  auto record = [&](int i) -> cudaError_t {
+    return events ? cudaEventRecord((cudaEvent_t)events[i], s) : cudaSuccess;
+  };
+  QTT_CUDA_TRY(record(0));
+  // a1: right-orthonormalise the operands
+  {
+    OrthArgs oa;
+    memset(&oa, 0, sizeof(oa));
+    oa.L = S.L; oa.orth = 1; oa.shared = 0;
+    for (int q = 0; q < S.L; ++q) { oa.legs[q] = S.dj[q]; oa.src[q] = (const double *)x->cores[q]; oa.off[q] = S.xoff[q]; }
+    for (int q = 0; q <= S.L; ++q) oa.r0[q] = S.xr[q];
+    oa.dst = Xo; oa.dst_bs = S.xo_elems; oa.rk = xr;
+    k_orth<<<S.B, kThreads, kOrthSmemDoubles * sizeof(double), s>>>(oa);
+    QTT_CUDA_TRY(cudaGetLastError());
+  }
+  if (S.kind != TRUNCATE) {
+    OrthArgs oa;
+    memset(&oa, 0, sizeof(oa));
+    oa.L = S.L; oa.orth = (flags & QTT_NO_OPERATOR_ORTH) ? 0 : 1; oa.shared = S.shared_op;
+    for (int q = 0; q < S.L; ++q) {
+      oa.legs[q] = (S.kind == MATVEC) ? S.d[q] * S.dj[q] : S.d[q];
+      oa.src[q] = (const double *)op->cores[q];
+      oa.off[q] = S.ooff[q];
+    }
+    for (int q = 0; q <= S.L; ++q) oa.r0[q] = S.orr[q];
+    oa.dst = Oo; oa.dst_bs = S.oo_elems; oa.rk = orr;
+    // a shared operator is orthonormalised once; its ranks are then broadcast per member
+    const int nb = S.shared_op ? 1 : S.B;
+    k_orth<<<nb, kThreads, kOrthSmemDoubles * sizeof(double), s>>>(oa);
+    QTT_CUDA_TRY(cudaGetLastError());
+    if (S.shared_op) {
+      for (int b = 1; b < S.B; ++b)
+        QTT_CUDA_TRY(cudaMemcpyAsync(orr + (size_t)b * (S.L + 1), orr, sizeof(int) * (S.L + 1),
+                                     cudaMemcpyDeviceToDevice, s));
+    }
+  } else {
+    QTT_CUDA_TRY(cudaMemsetAsync(orr, 0, sizeof(int) * (S.L + 1) * S.B, s));
+  }
+
+  QTT_CUDA_TRY(record(1));
+  // a2..a7: the sweep over sites
+  for (int q = 0; q < S.L; ++q) {
+    SiteArgs a;
+    memset(&a, 0, sizeof(a));
+    a.q = q; a.L = S.L; a.kind = S.kind; a.d = S.d[q]; a.dj = S.dj[q]; a.shared_op = S.shared_op;
+    a.Xq = Xo + S.xoff[q]; a.Xq_bs = S.xo_elems;
+    a.Oq = (S.kind == TRUNCATE) ? nullptr : Oo + S.ooff[q];
+    a.Oq_bs = S.oo_elems;
+    a.xr = xr; a.orr = orr; a.yr = out_ranks;
+    a.G = G; a.G_bs = S.g_elems; a.T = T; a.T_bs = S.t_elems; a.X = Xb; a.X_bs = S.x_elems;
+    a.Cq = (double *)out->cores[q];
+    a.Cq_bs = (long long)out->ranks[q] * S.d[q] * out->ranks[q + 1];
+    a.delta2 = delta2; a.norm2 = norm2; a.sigma = sigma; a.sigma_stride = sigma_stride; a.sweeps = sweeps;
+    a.status = status; a.eps = eps; a.max_rank = max_rank;
+    QTT_CUDA_TRY(record(2 + 2 * q));
+    k_site<<<S.B, kThreads, kSiteSmemBytes, s>>>(a);
+    QTT_CUDA_TRY(cudaGetLastError());
+    QTT_CUDA_TRY(record(3 + 2 * q));
+  }
+  return QTT_OK;
+}
+
+}  // extern "C"
