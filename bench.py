@@ -242,6 +242,9 @@ def main():
 
     # ---------------- timed region (device time, max over ranks)
     ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * (L + 1))] for _ in range(args.steps)]
+    for ev in ev_sets:          # torch creates the CUDA event lazily: force it before handing the handle over
+        for e in ev:
+            e.record(stream)
     clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
