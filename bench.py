@@ -221,7 +221,7 @@ def main():
     xd = qtt.to_device(xs)
     od = None if ops is None else qtt.to_device(ops, mpo=mpo)
     p0 = probs[0]
-    plan = qtt.ZipupPlan(subs, od, xd, p0.eps, p0.max_rank, sweeps=True)
+    plan = qtt.ZipupPlan(subs, od, xd, p0.eps, p0.max_rank, sweeps=True, cycles=True)
     L = xd.n_sites
     B = xd.batch
     summary = torch.zeros(4, dtype=torch.float64, device="cuda")
@@ -272,6 +272,9 @@ def main():
     orth_ms = sum(ev[0].elapsed_time(ev[1]) for ev in ev_sets)
     ranks = res.ranks.cpu().numpy()
     sweeps = res.sweeps.cpu().numpy()
+    cyc = res.cycles.cpu().numpy().astype(np.float64).sum(axis=(0, 1))
+    phase_share = {k: round(float(v / cyc.sum()), 4) for k, v in
+                   zip(("a2_contract", "a3_qr", "a4_jacobi", "a5_a6_trunc_emit_carry"), cyc)}
     d = xd.d_out if kind != "matvec" else od.d_out
     dj = xd.d_out
     tot = np.zeros(4)
@@ -362,7 +365,7 @@ def main():
                          "share_of_step": round(site_ms / args.steps / ms, 4),
                          "flop_split": {"contract": tot[0], "qr": tot[1], "carry": tot[2], "jacobi": tot[3]},
                          "prepass_ms_per_step": round(orth_ms / args.steps, 3)},
-            "fp64_peaks": peaks,
+            "fp64_peaks": peaks, "site_kernel_phase_share": phase_share,
             "jacobi_sweeps": {"mean": float(sweeps[:, :-1].mean()), "max": int(sweeps.max())},
             "cpu_baseline": cpu, "parity_sample": parity, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "clocks": clk,

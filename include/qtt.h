@@ -114,6 +114,9 @@ typedef struct {
   void *const *events;    /* host [2*(L+1)] cudaEvent_t recorded on `stream`: events[0]/[1]
                              bracket the a1 pre-pass, events[2+2q]/[3+2q] the site-q kernel;
                              NULL to skip (used by bench.py to time the dominant kernel)     */
+  int64_t *phase_cycles;  /* device int64 [B*L*4]: SM clock cycles of the site kernel phases
+                             (a2 contraction, a3 QR, a4 Jacobi, a5+a6 truncation/emit/carry)
+                             for every member and site; NULL to skip                          */
 } qtt_zipup_diag_t;
 
 qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,

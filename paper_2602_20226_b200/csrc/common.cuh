@@ -12,6 +12,7 @@ namespace qtt {
 
 constexpr int kThreads = 256;     // CTA size of every per-member kernel (8 warps)
 constexpr int kWarps = kThreads / 32;
+constexpr int kLdA = 129;         // leading dim of the shared R / Jacobi matrix (odd: no bank conflicts)
 
 void set_error(const char *fmt, ...);
 qtt_status_t cuda_status(cudaError_t e, const char *what);

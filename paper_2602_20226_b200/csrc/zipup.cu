@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "jacobi.cuh"
 
 namespace qtt {
 
@@ -36,14 +37,12 @@ enum Kind { MATVEC = 0, HADAMARD = 1, TRUNCATE = 2 };
 
 constexpr int kMaxSites = 64;
 constexpr int kSmall = 128;            // max rows m (and p) of a site matrix on this path
-constexpr int kLdA = kSmall + 1;       // leading dim of the shared R / Jacobi matrix (odd: no bank conflicts)
-constexpr int kBS = 32;                // rows of T^H per incremental-QR block
-constexpr int kLdB = kSmall + 1;
-constexpr int kBkDoubles = 4352;       // >= kBS*kLdB, >= 2*16*64 GEMM staging, >= staged MPO core
-constexpr int kSiteSmemDoubles = kSmall * kLdA + kBkDoubles + kSmall + 8 + 8;
+constexpr int kBS = 64;                // rows of T^H per incremental-QR block
+constexpr int kLdB = kSmall + 1;       // leading dim of the QR block (odd: no bank conflicts)
+constexpr int kBkDoubles = kBS * kLdB; // QR block / GEMM staging (>= 2*16*64) / staged MPO core
+constexpr int kSiteSmemDoubles = kSmall * kLdA + kBkDoubles + kSmall + 8 + 8 + kSmall;
 constexpr size_t kSiteSmemBytes = kSiteSmemDoubles * sizeof(double) + (kSmall + 8) * sizeof(int);
 constexpr int kOrthSmemDoubles = 26000;  // a1 staging budget (~203 KB)
-constexpr int kJacobiMaxSweeps = 60;
 
 enum StatusBits { ST_NONFINITE = 1, ST_NOCONV = 2 };
 
@@ -190,6 +189,7 @@ struct SiteArgs {
   double *delta2, *norm2, *sigma;
   int sigma_stride;
   int *sweeps;
+  long long *cycles;                     // optional [B][L][4] clock64 per phase
   int *status;
   double eps;
   int max_rank;
@@ -198,9 +198,25 @@ struct SiteArgs {
 // a3: R (m x m, upper, row-major in Rs with ld kLdA) of T^H, T row-major m x n, m <= n.
 // Incremental Householder over row blocks of T^H: QR([R; block]) for each block of kBS
 // columns of T; the reflector of column j touches R[j][j] and the block column only.
-__device__ void qr_of_TH(const double *T, int m, int n, double *Rs, double *Bk, double *scal) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// Two threads own one column (32 block rows each); the owner of column j+1 builds the next
+// reflector right after applying reflector j, so each column costs one barrier.
+__device__ void qr_of_TH(const double *T, int m, int n, double *Rs, double *Bk, double *tau) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int col = tid >> 1, half = tid & 1, r0 = half * (kBS / 2);
+  const unsigned pair_mask = 3u << (lane & ~1);
   for (int i = tid; i < m * kLdA; i += kThreads) Rs[i] = 0.0;
+  auto make_reflector = [&](int j) {            // owners of column j; block part already updated
+    double *bj = Bk + j;
+    double s = 0.0;
+#pragma unroll 8
+    for (int i = r0; i < r0 + kBS / 2; ++i) s = fma(bj[i * kLdB], bj[i * kLdB], s);
+    s += __shfl_xor_sync(pair_mask, s, 1);
+    double t, beta, scale;
+    householder(Rs[j * kLdA + j], s, t, beta, scale);
+#pragma unroll 8
+    for (int i = r0; i < r0 + kBS / 2; ++i) bj[i * kLdB] *= scale;
+    if (half == 0) { tau[j] = t; Rs[j * kLdA + j] = beta; }
+  };
   for (int c0 = 0; c0 < n; c0 += kBS) {
     const int nb = min(kBS, n - c0);
     __syncthreads();
@@ -209,78 +225,34 @@ __device__ void qr_of_TH(const double *T, int m, int n, double *Rs, double *Bk, 
       Bk[i * kLdB + j] = (i < nb) ? T[(size_t)j * n + c0 + i] : 0.0;
     }
     __syncthreads();
+    if (col == 0) make_reflector(0);
+    __syncthreads();
     for (int j = 0; j < m; ++j) {
-      if (warp == 0) {
-        const double v = Bk[lane * kLdB + j];          // kBS == 32: one row per lane
-        const double xn2 = warp_sum(v * v);
-        double t, beta, scale;
-        householder(Rs[j * kLdA + j], xn2, t, beta, scale);
-        Bk[lane * kLdB + j] = v * scale;
-        __syncwarp();
-        if (lane == 0) { scal[0] = t; Rs[j * kLdA + j] = beta; }
-      }
-      __syncthreads();
-      const double t = scal[0];
-      if (t != 0.0) {
-        for (int col = j + 1 + tid; col < m; col += kThreads) {
-          double s = Rs[j * kLdA + col];
-#pragma unroll 8
-          for (int i = 0; i < kBS; ++i) s = fma(Bk[i * kLdB + j], Bk[i * kLdB + col], s);
-          s *= t;
-          Rs[j * kLdA + col] -= s;
-#pragma unroll 8
-          for (int i = 0; i < kBS; ++i) Bk[i * kLdB + col] = fma(-s, Bk[i * kLdB + j], Bk[i * kLdB + col]);
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
-// a4: one-sided (Hestenes) Jacobi on the columns of A (m rows, p columns, column j at
-// A + j*kLdA), cyclic round-robin parallel ordering, one warp per column pair, warp-shuffle
-// dot products.  Converged when every pair satisfies |a_i.a_j| <= m*eps*|a_i||a_j|.
-// Returns the number of sweeps (>= kJacobiMaxSweeps means not converged).
-__device__ int jacobi_smem(double *A, int m, int p, int *flag) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int P = p + (p & 1);
-  const double tol = (double)max(m, 1) * DBL_EPSILON;
-  int sweep = 0;
-  for (; sweep < kJacobiMaxSweeps; ++sweep) {
-    if (threadIdx.x == 0) *flag = 0;
-    __syncthreads();
-    for (int rd = 0; rd < P - 1; ++rd) {
-      for (int t = warp; t < P / 2; t += kWarps) {
-        const int i = (t == 0) ? 0 : 1 + (t - 1 + rd) % (P - 1);
-        const int j = 1 + (P - 2 - t + rd) % (P - 1);
-        if (i >= p || j >= p) continue;
-        double *ai = A + (size_t)i * kLdA, *aj = A + (size_t)j * kLdA;
-        double al = 0.0, be = 0.0, ga = 0.0;
-        for (int row = lane; row < m; row += 32) {
-          const double x = ai[row], y = aj[row];
-          al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
-        }
-        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
-        if (ga != 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double tt = (fabs(zeta) > 1e150) ? 0.5 / zeta
-                                                 : copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-          const double cs = 1.0 / sqrt(fma(tt, tt, 1.0)), sn = cs * tt;
-          for (int row = lane; row < m; row += 32) {
-            const double x = ai[row], y = aj[row];
-            ai[row] = fma(cs, x, -sn * y);
-            aj[row] = fma(sn, x, cs * y);
+      if (col > j && col < m) {
+        const double t = tau[j];
+        if (t != 0.0) {
+          const double *vj = Bk + j;
+          double *bc = Bk + col;
+          double s0 = (half == 0) ? Rs[j * kLdA + col] : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+          for (int i = r0; i < r0 + kBS / 2; i += 4) {
+            s0 = fma(vj[i * kLdB], bc[i * kLdB], s0);
+            s1 = fma(vj[(i + 1) * kLdB], bc[(i + 1) * kLdB], s1);
+            s2 = fma(vj[(i + 2) * kLdB], bc[(i + 2) * kLdB], s2);
+            s3 = fma(vj[(i + 3) * kLdB], bc[(i + 3) * kLdB], s3);
           }
-          if (lane == 0) *flag = 1;
+          double w = (s0 + s1) + (s2 + s3);
+          w += __shfl_xor_sync(pair_mask, w, 1);
+          w *= t;
+          if (half == 0) Rs[j * kLdA + col] -= w;
+#pragma unroll
+          for (int i = r0; i < r0 + kBS / 2; ++i) bc[i * kLdB] = fma(-w, vj[i * kLdB], bc[i * kLdB]);
         }
+        if (col == j + 1) make_reflector(col);
       }
       __syncthreads();
     }
-    const int rot = *flag;
-    __syncthreads();
-    if (!rot) break;
   }
-  return sweep;
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_site(SiteArgs a) {
@@ -290,7 +262,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_site(SiteArgs a) {
   double *sg = Bk + kBkDoubles;              // sigma^2 per column
   double *red = sg + kSmall;                 // block-reduction scratch
   double *scal = red + 8;                    // scalars
-  int *perm = reinterpret_cast<int *>(scal + 8);
+  double *tau = scal + 8;                    // Householder tau per column
+  int *perm = reinterpret_cast<int *>(tau + kSmall);
   int *iflag = perm + kSmall;
 
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -308,6 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_site(SiteArgs a) {
   const double *Oq = a.Oq ? a.Oq + (a.shared_op ? 0 : (size_t)b * a.Oq_bs) : nullptr;
   double *Cq = a.Cq + (size_t)b * a.Cq_bs;
 
+  long long t_phase = clock64();
   if (q == 0) {
     if (tid == 0) G[0] = 1.0;                // G_0 = [[[1]]]
     __syncthreads();
@@ -353,6 +327,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_site(SiteArgs a) {
              [&](int i, int j, double v) { T[(size_t)i * N + j] = v; }, Bk);
   }
   __syncthreads();
+  if (tid == 0 && a.cycles) a.cycles[((size_t)b * L + q) * 4 + 0] = clock64() - t_phase;
+  t_phase = clock64();
 
   // ---------------------------------------------------------------- a7: last site
   if (q == L - 1) {
@@ -374,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_site(SiteArgs a) {
   int p;
   if (m <= n) {
     p = m;
-    qr_of_TH(T, m, n, Rs, Bk, scal);               // A = R^T: column j of A = row j of R
+    qr_of_TH(T, m, n, Rs, Bk, tau);                // A = R^T: column j of A = row j of R
   } else {
     p = n;                                         // A = T (m x n): column j = T[:, j]
     for (int idx = tid; idx < m * n; idx += kThreads) {
@@ -383,9 +359,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_site(SiteArgs a) {
     }
   }
   __syncthreads();
+  if (tid == 0 && a.cycles) a.cycles[((size_t)b * L + q) * 4 + 1] = clock64() - t_phase;
+  t_phase = clock64();
 
   // ---------------------------------------------------------------- a4: Jacobi SVD
-  const int sweeps = jacobi_smem(Rs, m, p, iflag);
+  {  // zero padding required by the register-blocked Jacobi: rows [m, 32*RPL), columns [p, 16*WB)
+    const int mp = (m <= 32) ? 32 : (m <= 64) ? 64 : 128;
+    const int pp = (p <= 16) ? 16 : (p <= 32) ? 32 : (p <= 64) ? 64 : 128;
+    for (int idx = tid; idx < pp * mp; idx += kThreads) {
+      const int j = idx / mp, row = idx % mp;
+      if (row >= m || j >= p) Rs[(size_t)j * kLdA + row] = 0.0;
+    }
+    __syncthreads();
+  }
+  const int sweeps = jacobi_dispatch(Rs, m, p, iflag);
+  if (tid == 0 && a.cycles) a.cycles[((size_t)b * L + q) * 4 + 2] = clock64() - t_phase;
+  t_phase = clock64();
   const int lane = tid & 31, warp = tid >> 5;
   for (int j = warp; j < p; j += kWarps) {
     double s = 0.0;
@@ -454,6 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_site(SiteArgs a) {
   cta_gemm(k, n, m, [&](int kk, int row) { return Rs[(size_t)perm[kk] * kLdA + row]; },
            [&](int row, int col) { return T[(size_t)row * n + col]; },
            [&](int kk, int col, double v) { G[(size_t)kk * n + col] = v; }, Bk);
+  if (tid == 0 && a.cycles) a.cycles[((size_t)b * L + q) * 4 + 3] = clock64() - t_phase;
 }
 
 // ======================================================================= host side
@@ -641,6 +631,7 @@ qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt
   const int sigma_stride = diag ? diag->sigma_stride : 0;
   int *sweeps = diag ? diag->sweeps : nullptr;
   void *const *events = diag ? diag->events : nullptr;
+  long long *cycles = diag ? (long long *)diag->phase_cycles : nullptr;
   g_err[0] = 0;
   if (!(eps >= 0.0 && eps < 1.0)) { set_error("eps %g outside [0,1)", eps); return QTT_EINVAL; }
   Shape S;
@@ -738,7 +729,7 @@ qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt
     a.G = G; a.G_bs = S.g_elems; a.T = T; a.T_bs = S.t_elems; a.X = Xb; a.X_bs = S.x_elems;
     a.Cq = (double *)out->cores[q];
     a.Cq_bs = (long long)out->ranks[q] * S.d[q] * out->ranks[q + 1];
-    a.delta2 = delta2; a.norm2 = norm2; a.sigma = sigma; a.sigma_stride = sigma_stride; a.sweeps = sweeps;
+    a.delta2 = delta2; a.norm2 = norm2; a.sigma = sigma; a.sigma_stride = sigma_stride; a.sweeps = sweeps; a.cycles = cycles;
     a.status = status; a.eps = eps; a.max_rank = max_rank;
     QTT_CUDA_TRY(record(2 + 2 * q));
     k_site<<<S.B, kThreads, kSiteSmemBytes, s>>>(a);

@@ -32,7 +32,7 @@ class QttError(RuntimeError):
 
 class _Diag(ctypes.Structure):
     _fields_ = [("sigma", ctypes.c_void_p), ("sigma_stride", ctypes.c_int32), ("sweeps", ctypes.c_void_p),
-                ("events", ctypes.POINTER(ctypes.c_void_p))]
+                ("events", ctypes.POINTER(ctypes.c_void_p)), ("phase_cycles", ctypes.c_void_p)]
 
 
 class _Trains(ctypes.Structure):
@@ -177,6 +177,7 @@ class ZipupResult:
     sigma: Optional[torch.Tensor]  # float64 (B, L-1, sigma_stride) or None
     sweeps: Optional[torch.Tensor]  # int32 (B, L) Jacobi sweeps per site or None
     workspace: torch.Tensor
+    cycles: Optional[torch.Tensor] = None  # int64 (B, L, 4) clock64 per site-kernel phase
 
 
 def capacity(subscripts: str, op: Optional[DeviceTrains], x: DeviceTrains, max_rank: int) -> List[int]:
@@ -196,7 +197,8 @@ class ZipupPlan:
     (the bench loop and CUDA-graph capture use this; no allocation per call)."""
 
     def __init__(self, subscripts: str, op: Optional[DeviceTrains], x: DeviceTrains, eps: float,
-                 max_rank: int, flags: int = 0, sigma_stride: int = 0, sweeps: bool = False, device="cuda"):
+                 max_rank: int, flags: int = 0, sigma_stride: int = 0, sweeps: bool = False, cycles: bool = False,
+                 device="cuda"):
         self.lib = load_library()
         self.subscripts, self.eps, self.max_rank, self.flags = subscripts, float(eps), int(max_rank), int(flags)
         d_out = op.d_out if (op is not None and subscripts == "ij,j->i") else x.d_out
@@ -211,6 +213,7 @@ class ZipupPlan:
         self.sigma = (torch.zeros((B, max(L - 1, 1), sigma_stride), dtype=torch.float64, device=device)
                       if sigma_stride > 0 else None)
         self.sweeps = torch.zeros((B, L), dtype=torch.int32, device=device) if sweeps else None
+        self.cycles = torch.zeros((B, L, 4), dtype=torch.int64, device=device) if cycles else None
         xs, kx = x.c_struct()
         os_ = None
         if op is not None:
@@ -230,13 +233,14 @@ class ZipupPlan:
             os_, ko = op.c_struct()
         outs, kout = self.out.c_struct()
         diag = None
-        if self.sigma is not None or self.sweeps is not None or events is not None:
+        if self.sigma is not None or self.sweeps is not None or events is not None or self.cycles is not None:
             ev = None
             if events is not None:
                 ev = (ctypes.c_void_p * len(events))(*[e.cuda_event for e in events])
             diag = _Diag(self.sigma.data_ptr() if self.sigma is not None else None, max(self.sigma_stride, 1),
                          self.sweeps.data_ptr() if self.sweeps is not None else None,
-                         ctypes.cast(ev, ctypes.POINTER(ctypes.c_void_p)) if ev is not None else None)
+                         ctypes.cast(ev, ctypes.POINTER(ctypes.c_void_p)) if ev is not None else None,
+                         self.cycles.data_ptr() if self.cycles is not None else None)
             self._keep = ev
         _check(self.lib.qtt_zipup(self.subscripts.encode(), ctypes.byref(os_) if os_ is not None else None,
                                   ctypes.byref(xs), self.eps, self.max_rank, self.flags, ctypes.byref(outs),
@@ -244,7 +248,7 @@ class ZipupPlan:
                                   self.status.data_ptr(), ctypes.byref(diag) if diag is not None else None,
                                   self.workspace.data_ptr(), self.workspace.numel(), _stream_ptr(stream)))
         return ZipupResult(self.out, self.ranks, self.delta2, self.norm2, self.status, self.sigma, self.sweeps,
-                           self.workspace)
+                           self.workspace, self.cycles)
 
 
 def zipup(subscripts: str, op: Optional[DeviceTrains], x: DeviceTrains, eps: float, max_rank: int,
