@@ -241,7 +241,7 @@ def main():
     assert int(res.status.item()) == 0, f"device status {int(res.status.item())}"
 
     # ---------------- timed region (device time, max over ranks)
-    ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * (L + 1))] for _ in range(args.steps)]
+    ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     for ev in ev_sets:          # torch creates the CUDA event lazily: force it before handing the handle over
         for e in ev:
             e.record(stream)
@@ -268,7 +268,7 @@ def main():
     ms_max = float(ms_t.item())
 
     # per-kernel device time of the dominant kernel (k_site) from the live events
-    site_ms = sum(ev[2 + 2 * q].elapsed_time(ev[3 + 2 * q]) for ev in ev_sets for q in range(L))
+    site_ms = sum(ev[2].elapsed_time(ev[3]) for ev in ev_sets)
     orth_ms = sum(ev[0].elapsed_time(ev[1]) for ev in ev_sets)
     ranks = res.ranks.cpu().numpy()
     sweeps = res.sweeps.cpu().numpy()
@@ -286,7 +286,7 @@ def main():
     site_s = site_ms * 1e-3 / args.steps
     fp64_peak = max(peaks["dfma_tflops"], peaks["dmma_tflops"])
     achieved = flops_all / site_s / 1e12
-    launches_per_step = L + 2 + (1 if kind != "truncate" else 0)   # L site kernels, a1 (x[, op]), summary
+    launches_per_step = 3 + (1 if kind != "truncate" else 0)   # a1 (x[, op]), k_sweep, summary
 
     units = world * B * L
     value = units / (ms_max * 1e-3)
@@ -357,7 +357,7 @@ def main():
                            (sum(c.numel() for c in xd.cores) * 8 / 1e9)),
             "alg_tflops": round(world * flops_alg / (ms_max * 1e-3) / 1e12, 3),
             "alg_tflops_note": "contraction+QR+carry flops (SURVEY.md §8(d)); Jacobi excluded",
-            "roofline": {"kernel": "k_site (a2-a7 fused site step; Jacobi-dominated)", "bound": "fp64",
+            "roofline": {"kernel": "k_sweep (persistent a2-a7 over all sites and members; Jacobi-dominated)", "bound": "fp64",
                          "achieved": round(achieved, 3), "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": round(achieved / fp64_peak, 4), "traffic": None,
                          "peak_source": "measured in this run by csrc/probe/peak.cu (MEASURED_PEAKS.json has no FP64)",

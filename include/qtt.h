@@ -111,9 +111,10 @@ typedef struct {
                              matrix, descending, zero padded; NULL to skip                    */
   int32_t sigma_stride;
   int32_t *sweeps;        /* device int32 [B*L]: Jacobi sweeps run at every site; NULL to skip */
-  void *const *events;    /* host [2*(L+1)] cudaEvent_t recorded on `stream`: events[0]/[1]
-                             bracket the a1 pre-pass, events[2+2q]/[3+2q] the site-q kernel;
-                             NULL to skip (used by bench.py to time the dominant kernel)     */
+  void *const *events;    /* host [4] cudaEvent_t recorded on `stream`: events[0]/[1] bracket
+                             the a1 pre-pass kernels, events[2]/[3] the persistent sweep
+                             kernel (a2..a7 for every site and member); NULL to skip (used by
+                             bench.py to time the dominant kernel)                           */
   int64_t *phase_cycles;  /* device int64 [B*L*4]: SM clock cycles of the site kernel phases
                              (a2 contraction, a3 QR, a4 Jacobi, a5+a6 truncation/emit/carry)
                              for every member and site; NULL to skip                          */

@@ -6,8 +6,9 @@
 // leading dimension kLdA; rows >= m and columns >= p must be zero.  The 16 column blocks of
 // WB columns are paired by a cyclic round-robin over the 8 warps (15 block rounds per
 // sweep).  A warp holds its two blocks in registers (lane l owns rows l, l+32, ...), and
-// processes WB disjoint column pairs per inner round: 3*WB partial dot products per lane,
-// one butterfly reduce-scatter across the warp, rotation parameters computed in parallel
+// processes WB disjoint column pairs per inner round: WB partial dot products per lane,
+// one butterfly reduce-scatter across the warp (column norms are tracked in shared memory
+// by the rotation identities), rotation parameters computed in parallel
 // (one pair per lane), broadcast by shuffles, rotations applied in registers.  Every pair of
 // columns is visited exactly once per sweep (cross pairs for every block pair, intra-block
 // pairs in the first block round).  Converged when no pair needed a rotation, i.e.
@@ -60,43 +61,76 @@ __device__ constexpr int pair_j(int a) {
   return base + ((k == 0) ? 0 : 1 + (k - 1 + S) % (WB > 1 ? WB - 1 : 1));
 }
 
+// Exact squared norms of the warp's 2*WB register columns -> nrm[0..2WB) (shared, per warp).
+template <int RPL, int WB>
+__device__ __forceinline__ void warp_norms(const double (&X)[2 * WB][RPL], double *nrm) {
+  constexpr int NC = 2 * WB;
+  constexpr int NV = (NC <= 4) ? 4 : (NC <= 8) ? 8 : (NC <= 16) ? 16 : 32;
+  const int lane = threadIdx.x & 31;
+  double v[NV];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    double s = 0.0;
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) s = fma(X[c][t], X[c][t], s);
+    v[c] = s;
+  }
+#pragma unroll
+  for (int k = NC; k < NV; ++k) v[k] = 0.0;
+  halve<NV, 16, NV>(v, lane);
+  constexpr int sh = 5 - ilog2<NV>();
+  if ((lane & ((1 << sh) - 1)) == 0 && (lane >> sh) < NC) nrm[lane >> sh] = v[0];
+  __syncwarp();
+}
+
+// One inner round: NP disjoint column pairs.  Column norms come from nrm[] (kept up to date
+// by the exact rotation identities a' = a - t*g, b' = b + t*g, refreshed exactly when a
+// norm collapses by more than sqrt(eps), as in LAPACK dgesvj); only the NP cross dot
+// products g are reduced across the warp.
 template <int RPL, int WB, int MODE, int S>
-__device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double tol, int &rot) {
+__device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm, double tol, int &rot) {
   constexpr int NP = (MODE == 0) ? WB : 2 * (WB / 2);   // pairs in this round
-  constexpr int NV = (3 * NP <= 4) ? 4 : (3 * NP <= 8) ? 8 : (3 * NP <= 16) ? 16 : 32;
+  constexpr int NV = (NP <= 4) ? 4 : (NP <= 8) ? 8 : (NP <= 16) ? 16 : 32;
   const int lane = threadIdx.x & 31;
   double v[NV];
 #pragma unroll
   for (int a = 0; a < NP; ++a) {
     const int i = pair_i<WB, MODE, S>(a), j = pair_j<WB, MODE, S>(a);
-    double al = 0.0, be = 0.0, ga = 0.0;
+    double g0 = 0.0, g1 = 0.0;
 #pragma unroll
-    for (int t = 0; t < RPL; ++t) {
-      al = fma(X[i][t], X[i][t], al);
-      be = fma(X[j][t], X[j][t], be);
-      ga = fma(X[i][t], X[j][t], ga);
+    for (int t = 0; t < RPL; t += 2) {
+      g0 = fma(X[i][t], X[j][t], g0);
+      if (t + 1 < RPL) g1 = fma(X[i][t + 1], X[j][t + 1], g1);
     }
-    v[3 * a] = al; v[3 * a + 1] = be; v[3 * a + 2] = ga;
+    v[a] = g0 + g1;
   }
 #pragma unroll
-  for (int k = 3 * NP; k < NV; ++k) v[k] = 0.0;
+  for (int k = NP; k < NV; ++k) v[k] = 0.0;
   halve<NV, 16, NV>(v, lane);
-  const double tot = v[0];
   constexpr int sh = 5 - ilog2<NV>();
   const int a = lane % NP;
-  const double al = __shfl_sync(0xffffffffu, tot, (3 * a) << sh);
-  const double be = __shfl_sync(0xffffffffu, tot, (3 * a + 1) << sh);
-  const double ga = __shfl_sync(0xffffffffu, tot, (3 * a + 2) << sh);
-  double c = 1.0, s = 0.0;
-  const bool doit = (ga != 0.0) && (fabs(ga) > tol * sqrt(al) * sqrt(be));
-  if (doit) {
-    const double zeta = (be - al) / (2.0 * ga);
-    const double t = (fabs(zeta) > 1e150) ? 0.5 / zeta
-                                          : copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-    c = 1.0 / sqrt(fma(t, t, 1.0));
-    s = c * t;
-  }
+  const double ga = __shfl_sync(0xffffffffu, v[0], a << sh);
+  int ia = 0, ja = 0;
+#pragma unroll
+  for (int k = 0; k < NP; ++k)
+    if (a == k) { ia = pair_i<WB, MODE, S>(k); ja = pair_j<WB, MODE, S>(k); }
+  const double al = nrm[ia], be = nrm[ja];
+  // Rotation angle (Rutishauser): t = sign(d) 2g / (|d| + sqrt(d^2 + 4g^2)), d = b - a;
+  // c = 1/sqrt(1+t^2), s = c t.  Rotate only if |g| > tol sqrt(a b) (squared test).
+  const double d = be - al;
+  const double g2 = ga + ga;
+  const bool doit = (ga * ga > (tol * tol) * (al * be)) && (al > 0.0) && (be > 0.0);
+  const double h = sqrt(fma(d, d, g2 * g2));
+  const double den = fabs(d) + h;
+  const double t = doit ? copysign(1.0, d) * g2 * __drcp_rn(den) : 0.0;
+  const double c = rsqrt(fma(t, t, 1.0));
+  const double s = c * t;
+  const double al2 = doit ? fma(-t, ga, al) : al;
+  const double be2 = doit ? fma(t, ga, be) : be;
+  const bool collapse = doit && (al2 < 1.5e-8 * al || be2 < 1.5e-8 * be);
   if (__any_sync(0xffffffffu, doit)) rot = 1;
+  __syncwarp();
+  if (lane < NP) { nrm[ia] = al2; nrm[ja] = be2; }
 #pragma unroll
   for (int a2 = 0; a2 < NP; ++a2) {
     const int i = pair_i<WB, MODE, S>(a2), j = pair_j<WB, MODE, S>(a2);
@@ -108,23 +142,26 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double tol, 
       X[j][t] = fma(sa, x, ca * y);
     }
   }
+  __syncwarp();
+  if (__any_sync(0xffffffffu, collapse)) warp_norms<RPL, WB>(X, nrm);   // cancellation: refresh exactly
 }
 
 template <int RPL, int WB, int MODE, int S, int SEND>
-__device__ __forceinline__ void jac_rounds(double (&X)[2 * WB][RPL], double tol, int &rot) {
+__device__ __forceinline__ void jac_rounds(double (&X)[2 * WB][RPL], double *nrm, double tol, int &rot) {
   if constexpr (S < SEND) {
-    jac_round<RPL, WB, MODE, S>(X, tol, rot);
-    jac_rounds<RPL, WB, MODE, S + 1, SEND>(X, tol, rot);
+    jac_round<RPL, WB, MODE, S>(X, nrm, tol, rot);
+    jac_rounds<RPL, WB, MODE, S + 1, SEND>(X, nrm, tol, rot);
   }
 }
 
 // Returns the number of sweeps executed (== kJacobiMaxSweeps: not converged).
 template <int RPL, int WB>
-__device__ int jacobi_blocked(double *A, int m, int *flag) {
+__device__ int jacobi_blocked(double *A, int m, int *flag, double *nrm_all) {
   constexpr int NB = 2 * kWarps;      // 16 blocks of WB columns
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double tol = (double)max(m, 1) * DBL_EPSILON;
   double X[2 * WB][RPL];
+  double *nrm = nrm_all + warp * 2 * WB;
   int sweep = 0;
   for (; sweep < kJacobiMaxSweeps; ++sweep) {
     int rot = 0;
@@ -139,10 +176,11 @@ __device__ int jacobi_blocked(double *A, int m, int *flag) {
           X[c][t] = A[(size_t)(I * WB + c) * kLdA + lane + 32 * t];
           X[WB + c][t] = A[(size_t)(J * WB + c) * kLdA + lane + 32 * t];
         }
+      warp_norms<RPL, WB>(X, nrm);
       if constexpr (WB > 1) {
-        if (r == 0) jac_rounds<RPL, WB, 1, 0, WB - 1>(X, tol, rot);
+        if (r == 0) jac_rounds<RPL, WB, 1, 0, WB - 1>(X, nrm, tol, rot);
       }
-      jac_rounds<RPL, WB, 0, 0, WB>(X, tol, rot);
+      jac_rounds<RPL, WB, 0, 0, WB>(X, nrm, tol, rot);
 #pragma unroll
       for (int c = 0; c < WB; ++c)
 #pragma unroll
@@ -164,10 +202,10 @@ __device__ int jacobi_blocked(double *A, int m, int *flag) {
 }
 
 // Dispatch on the padded sizes: RPL = ceil(m/32) in {1,2,4}, WB = ceil(p/16) in {1,2,4,8}.
-__device__ __forceinline__ int jacobi_dispatch(double *A, int m, int p, int *flag) {
+__device__ __forceinline__ int jacobi_dispatch(double *A, int m, int p, int *flag, double *nrm_all) {
   const int rpl = (m <= 32) ? 1 : (m <= 64) ? 2 : 4;
   const int wb = (p <= 16) ? 1 : (p <= 32) ? 2 : (p <= 64) ? 4 : 8;
-#define QTT_JAC(R, W) if (rpl == R && wb == W) return jacobi_blocked<R, W>(A, m, flag);
+#define QTT_JAC(R, W) if (rpl == R && wb == W) return jacobi_blocked<R, W>(A, m, flag, nrm_all);
   QTT_JAC(1, 1) QTT_JAC(1, 2) QTT_JAC(1, 4) QTT_JAC(1, 8)
   QTT_JAC(2, 1) QTT_JAC(2, 2) QTT_JAC(2, 4) QTT_JAC(2, 8)
   QTT_JAC(4, 1) QTT_JAC(4, 2) QTT_JAC(4, 4) QTT_JAC(4, 8)

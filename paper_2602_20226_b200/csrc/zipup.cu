@@ -3,7 +3,7 @@
 // Small-member path: one CTA (256 threads, 1 per SM) owns one batch member at a time.
 //   k_orth : a1 right-orthonormalisation of one operand, all sites right-to-left (Householder
 //            QR with explicit Q, R absorbed into the left neighbour).
-//   k_site : one site step q for every member: a2 contraction -> T (L2-resident scratch),
+//   k_sweep: persistent: every (site, member) step: a2 contraction -> T (L2-resident scratch),
 //            a3 incremental Householder QR of T^H (R in shared memory), a4 one-sided Jacobi
 //            SVD on R^H in shared memory (warp-shuffle reductions, round-robin ordering),
 //            a5 tail-sum truncation, a6 emit U_k and carry G = U_k^T T, a7 last site.
@@ -176,16 +176,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_orth(OrthArgs a) {
 
 // ======================================================================= a2..a7: site step
 
-struct SiteArgs {
-  int q, L, kind, d, dj, shared_op;
-  const double *Xq; long long Xq_bs;     // orthonormalised x core q (workspace)
-  const double *Oq; long long Oq_bs;     // orthonormalised operator core q (workspace)
+struct SweepArgs {
+  int L, B, kind, shared_op;
+  int d[kMaxSites], dj[kMaxSites];       // output / contracted digit size per site
+  long long xoff[kMaxSites], ooff[kMaxSites];
+  double *Cq[kMaxSites];                 // output core slots (batch-strided)
+  long long Cq_bs[kMaxSites];
+  const double *Xo; long long Xo_bs;     // orthonormalised x cores (workspace)
+  const double *Oo; long long Oo_bs;     // orthonormalised operator cores (workspace)
   const int *xr; const int *orr;         // [B][L+1] operand ranks after a1
   int *yr;                               // [B][L+1] output ranks
   double *G; long long G_bs;             // carry (chi, w, r)
   double *T; long long T_bs;             // site matrix (m x n), row-major
   double *X; long long X_bs;             // state-contraction intermediate
-  double *Cq; long long Cq_bs;           // output core q slot
+  int *task_counter;                     // persistent scheduler: next (site, member) task
+  int *done;                             // [B] sites completed per member (acquire/release)
   double *delta2, *norm2, *sigma;
   int sigma_stride;
   int *sweeps;
@@ -198,25 +203,58 @@ struct SiteArgs {
 // a3: R (m x m, upper, row-major in Rs with ld kLdA) of T^H, T row-major m x n, m <= n.
 // Incremental Householder over row blocks of T^H: QR([R; block]) for each block of kBS
 // columns of T; the reflector of column j touches R[j][j] and the block column only.
-// Two threads own one column (32 block rows each); the owner of column j+1 builds the next
-// reflector right after applying reflector j, so each column costs one barrier.
+// Blocked by panels of kPanel columns: warp 0 factors a panel warp-synchronously (two lanes
+// per column), then every thread pair applies the panel's reflectors to one trailing column
+// held in registers -- two CTA barriers per panel.
+constexpr int kPanel = 16;
+
+__device__ __forceinline__ void qr_make_reflector(double *Rs, double *Bk, double *tau, int j, int r0,
+                                                  int half, unsigned pair_mask) {
+  double *bj = Bk + j;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+  for (int i = r0; i < r0 + kBS / 2; i += 4) {
+    s0 = fma(bj[i * kLdB], bj[i * kLdB], s0);
+    s1 = fma(bj[(i + 1) * kLdB], bj[(i + 1) * kLdB], s1);
+    s2 = fma(bj[(i + 2) * kLdB], bj[(i + 2) * kLdB], s2);
+    s3 = fma(bj[(i + 3) * kLdB], bj[(i + 3) * kLdB], s3);
+  }
+  double s = (s0 + s1) + (s2 + s3);
+  s += __shfl_xor_sync(pair_mask, s, 1);
+  double t, beta, scale;
+  householder(Rs[j * kLdA + j], s, t, beta, scale);
+#pragma unroll
+  for (int i = r0; i < r0 + kBS / 2; ++i) bj[i * kLdB] *= scale;
+  if (half == 0) { tau[j] = t; Rs[j * kLdA + j] = beta; }
+}
+
+// Apply reflector j (v = [1 at R row j; Bk[:, j]], tau[j]) to column c whose block rows
+// r0..r0+kBS/2 are x[] (registers); the pair of lanes combines the two half dot products.
+__device__ __forceinline__ void qr_apply(const double *Rs_row_j, double *Rjc, const double *Bk, double t, int j,
+                                         int r0, int half, unsigned pair_mask, double (&x)[kBS / 2]) {
+  const double *vj = Bk + j;
+  double s0 = (half == 0) ? *Rjc : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+  for (int i = 0; i < kBS / 2; i += 4) {
+    s0 = fma(vj[(r0 + i) * kLdB], x[i], s0);
+    s1 = fma(vj[(r0 + i + 1) * kLdB], x[i + 1], s1);
+    s2 = fma(vj[(r0 + i + 2) * kLdB], x[i + 2], s2);
+    s3 = fma(vj[(r0 + i + 3) * kLdB], x[i + 3], s3);
+  }
+  double w = (s0 + s1) + (s2 + s3);
+  w += __shfl_xor_sync(pair_mask, w, 1);
+  w *= t;
+  if (half == 0) *Rjc -= w;
+#pragma unroll
+  for (int i = 0; i < kBS / 2; ++i) x[i] = fma(-w, vj[(r0 + i) * kLdB], x[i]);
+  (void)Rs_row_j;
+}
+
 __device__ void qr_of_TH(const double *T, int m, int n, double *Rs, double *Bk, double *tau) {
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int col = tid >> 1, half = tid & 1, r0 = half * (kBS / 2);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int half = tid & 1, r0 = half * (kBS / 2);
   const unsigned pair_mask = 3u << (lane & ~1);
   for (int i = tid; i < m * kLdA; i += kThreads) Rs[i] = 0.0;
-  auto make_reflector = [&](int j) {            // owners of column j; block part already updated
-    double *bj = Bk + j;
-    double s = 0.0;
-#pragma unroll 8
-    for (int i = r0; i < r0 + kBS / 2; ++i) s = fma(bj[i * kLdB], bj[i * kLdB], s);
-    s += __shfl_xor_sync(pair_mask, s, 1);
-    double t, beta, scale;
-    householder(Rs[j * kLdA + j], s, t, beta, scale);
-#pragma unroll 8
-    for (int i = r0; i < r0 + kBS / 2; ++i) bj[i * kLdB] *= scale;
-    if (half == 0) { tau[j] = t; Rs[j * kLdA + j] = beta; }
-  };
   for (int c0 = 0; c0 < n; c0 += kBS) {
     const int nb = min(kBS, n - c0);
     __syncthreads();
@@ -225,38 +263,47 @@ __device__ void qr_of_TH(const double *T, int m, int n, double *Rs, double *Bk, 
       Bk[i * kLdB + j] = (i < nb) ? T[(size_t)j * n + c0 + i] : 0.0;
     }
     __syncthreads();
-    if (col == 0) make_reflector(0);
-    __syncthreads();
-    for (int j = 0; j < m; ++j) {
-      if (col > j && col < m) {
-        const double t = tau[j];
-        if (t != 0.0) {
-          const double *vj = Bk + j;
-          double *bc = Bk + col;
-          double s0 = (half == 0) ? Rs[j * kLdA + col] : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    for (int j0 = 0; j0 < m; j0 += kPanel) {
+      const int jn = min(j0 + kPanel, m);
+      // (1) panel factorisation by warp 0: lane pair pc owns panel column j0 + pc
+      if (warp == 0) {
+        const int c = j0 + (lane >> 1);
+        for (int j = j0; j < jn; ++j) {
+          if (c == j) qr_make_reflector(Rs, Bk, tau, j, r0, half, pair_mask);
+          __syncwarp();
+          if (c > j && c < jn) {
+            const double t = tau[j];
+            if (t != 0.0) {
+              double x[kBS / 2];
 #pragma unroll
-          for (int i = r0; i < r0 + kBS / 2; i += 4) {
-            s0 = fma(vj[i * kLdB], bc[i * kLdB], s0);
-            s1 = fma(vj[(i + 1) * kLdB], bc[(i + 1) * kLdB], s1);
-            s2 = fma(vj[(i + 2) * kLdB], bc[(i + 2) * kLdB], s2);
-            s3 = fma(vj[(i + 3) * kLdB], bc[(i + 3) * kLdB], s3);
+              for (int i = 0; i < kBS / 2; ++i) x[i] = Bk[(r0 + i) * kLdB + c];
+              qr_apply(nullptr, Rs + j * kLdA + c, Bk, t, j, r0, half, pair_mask, x);
+#pragma unroll
+              for (int i = 0; i < kBS / 2; ++i) Bk[(r0 + i) * kLdB + c] = x[i];
+            }
           }
-          double w = (s0 + s1) + (s2 + s3);
-          w += __shfl_xor_sync(pair_mask, w, 1);
-          w *= t;
-          if (half == 0) Rs[j * kLdA + col] -= w;
-#pragma unroll
-          for (int i = r0; i < r0 + kBS / 2; ++i) bc[i * kLdB] = fma(-w, vj[i * kLdB], bc[i * kLdB]);
+          __syncwarp();
         }
-        if (col == j + 1) make_reflector(col);
+      }
+      __syncthreads();
+      // (2) trailing update: columns jn..m-1, two threads per column, column in registers
+      for (int c = jn + (tid >> 1); c < m; c += kThreads / 2) {
+        double x[kBS / 2];
+#pragma unroll
+        for (int i = 0; i < kBS / 2; ++i) x[i] = Bk[(r0 + i) * kLdB + c];
+        for (int j = j0; j < jn; ++j) {
+          const double t = tau[j];
+          if (t != 0.0) qr_apply(nullptr, Rs + j * kLdA + c, Bk, t, j, r0, half, pair_mask, x);
+        }
+#pragma unroll
+        for (int i = 0; i < kBS / 2; ++i) Bk[(r0 + i) * kLdB + c] = x[i];
       }
       __syncthreads();
     }
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_site(SiteArgs a) {
-  extern __shared__ double smem[];
+__device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, double *smem) {
   double *Rs = smem;                         // kSmall x kLdA: R (row-major) == A = R^T (col-major)
   double *Bk = Rs + kSmall * kLdA;           // QR block / GEMM staging / staged MPO core
   double *sg = Bk + kBkDoubles;              // sigma^2 per column
@@ -266,20 +313,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_site(SiteArgs a) {
   int *perm = reinterpret_cast<int *>(tau + kSmall);
   int *iflag = perm + kSmall;
 
-  const int b = blockIdx.x, tid = threadIdx.x;
-  const int L = a.L, L1 = L + 1, q = a.q;
+  const int tid = threadIdx.x;
+  const int L = a.L, L1 = L + 1;
   const int chi = (q == 0) ? 1 : a.yr[(size_t)b * L1 + q];
   const int r = a.xr[(size_t)b * L1 + q], r2 = a.xr[(size_t)b * L1 + q + 1];
   int w = 1, w2 = 1;
   if (a.kind != TRUNCATE) { w = a.orr[(size_t)b * L1 + q]; w2 = a.orr[(size_t)b * L1 + q + 1]; }
-  const int d = a.d, dj = a.dj;
+  const int d = a.d[q], dj = a.dj[q];
   const int m = chi * d, n = w2 * r2;
   double *G = a.G + (size_t)b * a.G_bs;
   double *T = a.T + (size_t)b * a.T_bs;
   double *X = a.X + (size_t)b * a.X_bs;
-  const double *Xq = a.Xq + (size_t)b * a.Xq_bs;
-  const double *Oq = a.Oq ? a.Oq + (a.shared_op ? 0 : (size_t)b * a.Oq_bs) : nullptr;
-  double *Cq = a.Cq + (size_t)b * a.Cq_bs;
+  const double *Xq = a.Xo + (size_t)b * a.Xo_bs + a.xoff[q];
+  const double *Oq = a.Oo ? a.Oo + (a.shared_op ? 0 : (size_t)b * a.Oo_bs) + a.ooff[q] : nullptr;
+  double *Cq = a.Cq[q] + (size_t)b * a.Cq_bs[q];
 
   long long t_phase = clock64();
   if (q == 0) {
@@ -372,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_site(SiteArgs a) {
     }
     __syncthreads();
   }
-  const int sweeps = jacobi_dispatch(Rs, m, p, iflag);
+  const int sweeps = jacobi_dispatch(Rs, m, p, iflag, Bk);   // Bk: per-warp norm scratch
   if (tid == 0 && a.cycles) a.cycles[((size_t)b * L + q) * 4 + 2] = clock64() - t_phase;
   t_phase = clock64();
   const int lane = tid & 31, warp = tid >> 5;
@@ -444,6 +491,38 @@ __global__ void __launch_bounds__(kThreads, 1) k_site(SiteArgs a) {
            [&](int row, int col) { return T[(size_t)row * n + col]; },
            [&](int kk, int col, double v) { G[(size_t)kk * n + col] = v; }, Bk);
   if (tid == 0 && a.cycles) a.cycles[((size_t)b * L + q) * 4 + 3] = clock64() - t_phase;
+}
+
+// Persistent sweep: one CTA per SM pulls tasks t = q*B + b (site-major, i.e. topological
+// order) from a global counter.  Task (b, q) waits for member b's site q-1 (release/acquire
+// on done[b]); the holder of that task was scheduled earlier and is running or finished, so
+// the wait cannot deadlock.  Balances the B*L site steps over the SMs (no wave tail).
+__global__ void __launch_bounds__(kThreads, 1) k_sweep(SweepArgs a) {
+  extern __shared__ double smem[];
+  __shared__ int s_task;
+  const int total = a.B * a.L;
+  for (;;) {
+    if (threadIdx.x == 0) s_task = atomicAdd(a.task_counter, 1);
+    __syncthreads();
+    const int task = s_task;
+    if (task >= total) break;
+    const int q = task / a.B, b = task % a.B;
+    if (threadIdx.x == 0 && q > 0) {
+      int v;
+      do {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(a.done + b) : "memory");
+        if (v < q) __nanosleep(64);
+      } while (v < q);
+      __threadfence();          // also invalidates this SM's L1: no stale carry / scratch lines
+    }
+    __syncthreads();
+    site_step(a, b, q, smem);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(a.done + b), "r"(q + 1) : "memory");
+    }
+  }
 }
 
 // ======================================================================= host side
@@ -578,7 +657,7 @@ static qtt_status_t check_small_path(const Shape &S) {
 }
 
 struct WsLayout {
-  size_t xo, oo, g, t, x, xr, orr, total;
+  size_t xo, oo, g, t, x, xr, orr, sched, total;
 };
 
 static WsLayout layout(const Shape &S) {
@@ -592,6 +671,7 @@ static WsLayout layout(const Shape &S) {
   w.x = take(sizeof(double) * S.x_elems * S.B);
   w.xr = take(sizeof(int) * (S.L + 1) * S.B);
   w.orr = take(sizeof(int) * (S.L + 1) * S.B);
+  w.sched = take(sizeof(int) * (1 + S.B));
   w.total = off;
   return w;
 }
@@ -670,7 +750,7 @@ qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt
 
   static bool attr_done = false;
   if (!attr_done) {
-    QTT_CUDA_TRY(cudaFuncSetAttribute(k_site, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSiteSmemBytes));
+    QTT_CUDA_TRY(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSiteSmemBytes));
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_orth, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(kOrthSmemDoubles * sizeof(double))));
     attr_done = true;
@@ -717,24 +797,35 @@ qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt
   }
 
   QTT_CUDA_TRY(record(1));
-  // a2..a7: the sweep over sites
-  for (int q = 0; q < S.L; ++q) {
-    SiteArgs a;
+  // a2..a7: the sweep over sites, one persistent launch for all members
+  {
+    SweepArgs a;
     memset(&a, 0, sizeof(a));
-    a.q = q; a.L = S.L; a.kind = S.kind; a.d = S.d[q]; a.dj = S.dj[q]; a.shared_op = S.shared_op;
-    a.Xq = Xo + S.xoff[q]; a.Xq_bs = S.xo_elems;
-    a.Oq = (S.kind == TRUNCATE) ? nullptr : Oo + S.ooff[q];
-    a.Oq_bs = S.oo_elems;
+    a.L = S.L; a.B = S.B; a.kind = S.kind; a.shared_op = S.shared_op;
+    for (int q = 0; q < S.L; ++q) {
+      a.d[q] = S.d[q]; a.dj[q] = S.dj[q];
+      a.xoff[q] = S.xoff[q]; a.ooff[q] = S.ooff[q];
+      a.Cq[q] = (double *)out->cores[q];
+      a.Cq_bs[q] = (long long)out->ranks[q] * S.d[q] * out->ranks[q + 1];
+    }
+    a.Xo = Xo; a.Xo_bs = S.xo_elems;
+    a.Oo = (S.kind == TRUNCATE) ? nullptr : Oo;
+    a.Oo_bs = S.oo_elems;
     a.xr = xr; a.orr = orr; a.yr = out_ranks;
     a.G = G; a.G_bs = S.g_elems; a.T = T; a.T_bs = S.t_elems; a.X = Xb; a.X_bs = S.x_elems;
-    a.Cq = (double *)out->cores[q];
-    a.Cq_bs = (long long)out->ranks[q] * S.d[q] * out->ranks[q + 1];
-    a.delta2 = delta2; a.norm2 = norm2; a.sigma = sigma; a.sigma_stride = sigma_stride; a.sweeps = sweeps; a.cycles = cycles;
-    a.status = status; a.eps = eps; a.max_rank = max_rank;
-    QTT_CUDA_TRY(record(2 + 2 * q));
-    k_site<<<S.B, kThreads, kSiteSmemBytes, s>>>(a);
+    int *sched = (int *)(ws + W.sched);
+    a.task_counter = sched; a.done = sched + 1;
+    a.delta2 = delta2; a.norm2 = norm2; a.sigma = sigma; a.sigma_stride = sigma_stride; a.sweeps = sweeps;
+    a.cycles = cycles; a.status = status; a.eps = eps; a.max_rank = max_rank;
+    QTT_CUDA_TRY(cudaMemsetAsync(sched, 0, sizeof(int) * (1 + S.B), s));
+    int dev = 0, sms = 0;
+    QTT_CUDA_TRY(cudaGetDevice(&dev));
+    QTT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int grid = std::max(1, std::min(sms, S.B * S.L));
+    QTT_CUDA_TRY(record(2));
+    k_sweep<<<grid, kThreads, kSiteSmemBytes, s>>>(a);
     QTT_CUDA_TRY(cudaGetLastError());
-    QTT_CUDA_TRY(record(3 + 2 * q));
+    QTT_CUDA_TRY(record(3));
   }
   return QTT_OK;
 }

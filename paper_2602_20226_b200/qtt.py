@@ -226,7 +226,7 @@ class ZipupPlan:
         self.workspace = torch.empty((nbytes + 255) // 256 * 256, dtype=torch.uint8, device=device)
 
     def run(self, op: Optional[DeviceTrains], x: DeviceTrains, stream=None, events=None) -> ZipupResult:
-        """events: optional list of 2*(L+1) torch.cuda.Event (recorded around each kernel)."""
+        """events: optional list of 4 torch.cuda.Event (a1 pre-pass start/end, sweep start/end)."""
         xs, kx = x.c_struct()
         os_ = None
         if op is not None:
