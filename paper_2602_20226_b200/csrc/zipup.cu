@@ -37,10 +37,9 @@ enum Kind { MATVEC = 0, HADAMARD = 1, TRUNCATE = 2 };
 
 constexpr int kMaxSites = 64;
 constexpr int kSmall = 128;            // max rows m (and p) of a site matrix on this path
-constexpr int kBS = 64;                // rows of T^H per incremental-QR block
-constexpr int kLdB = kSmall + 1;       // leading dim of the QR block (odd: no bank conflicts)
-constexpr int kBkDoubles = kBS * kLdB; // QR block / GEMM staging (>= 2*16*64) / staged MPO core
-constexpr int kSiteSmemDoubles = kSmall * kLdA + kBkDoubles + kSmall + 8 + 8 + kSmall;
+constexpr int kRpDoubles = kSmall * (kSmall + 1) / 2;  // packed R / GEMM staging / scratch (8256)
+constexpr int kBkDoubles = kRpDoubles;                  // staged MPO core limit
+constexpr int kSiteSmemDoubles = kRpDoubles + kSmall * kLdA + kSmall + 8 + 8 + kSmall;
 constexpr size_t kSiteSmemBytes = kSiteSmemDoubles * sizeof(double) + (kSmall + 8) * sizeof(int);
 constexpr int kOrthSmemDoubles = 26000;  // a1 staging budget (~203 KB)
 
@@ -200,103 +199,116 @@ struct SweepArgs {
   int max_rank;
 };
 
-// a3: R (m x m, upper, row-major in Rs with ld kLdA) of T^H, T row-major m x n, m <= n.
-// Incremental Householder over row blocks of T^H: QR([R; block]) for each block of kBS
-// columns of T; the reflector of column j touches R[j][j] and the block column only.
-// Blocked by panels of kPanel columns: warp 0 factors a panel warp-synchronously (two lanes
-// per column), then every thread pair applies the panel's reflectors to one trailing column
-// held in registers -- two CTA barriers per panel.
+// a3: R (m x m upper triangular, packed row-major in Rp) of T^H, T row-major m x n, m <= n.
+// Incremental Householder over row blocks of T^H (kSmall = 128 columns of T per block):
+// QR([R; block]); the reflector of column j touches R[j][j] and the block column only.
+// Blocked by panels of 16 columns: warp 0 factors a panel with the 16 columns x 128 rows in
+// registers (4 rows per lane, warp-wide reductions, no CTA barrier inside the panel); then
+// every thread pair applies the 16 reflectors to one trailing column held in registers.
+// Two CTA barriers per panel; 2 blocks for n = 256.
 constexpr int kPanel = 16;
 
-__device__ __forceinline__ void qr_make_reflector(double *Rs, double *Bk, double *tau, int j, int r0,
-                                                  int half, unsigned pair_mask) {
-  double *bj = Bk + j;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+__device__ __forceinline__ int rp_idx(int j, int c, int m) { return j * m - (j * (j - 1)) / 2 + (c - j); }
+
+__device__ __forceinline__ void qr_panel(double *Rp, double *Bk, double *tau, int m, int j0) {
+  const int lane = threadIdx.x & 31;
+  double P[kPanel][4];
 #pragma unroll
-  for (int i = r0; i < r0 + kBS / 2; i += 4) {
-    s0 = fma(bj[i * kLdB], bj[i * kLdB], s0);
-    s1 = fma(bj[(i + 1) * kLdB], bj[(i + 1) * kLdB], s1);
-    s2 = fma(bj[(i + 2) * kLdB], bj[(i + 2) * kLdB], s2);
-    s3 = fma(bj[(i + 3) * kLdB], bj[(i + 3) * kLdB], s3);
+  for (int cc = 0; cc < kPanel; ++cc)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) P[cc][t] = (j0 + cc < m) ? Bk[(lane + 32 * t) * kLdA + j0 + cc] : 0.0;
+#pragma unroll
+  for (int jj = 0; jj < kPanel; ++jj) {
+    const int j = j0 + jj;
+    if (j < m) {
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) s = fma(P[jj][t], P[jj][t], s);
+      s = warp_sum(s);
+      double tj, beta, scale;
+      householder(Rp[rp_idx(j, j, m)], s, tj, beta, scale);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) P[jj][t] *= scale;
+      __syncwarp();
+      if (lane == 0) { Rp[rp_idx(j, j, m)] = beta; tau[j] = tj; }
+      if (jj + 1 < kPanel && tj != 0.0) {
+        // dots of v_j with the remaining panel columns: reduce-scatter of 16 partials
+        double v[kPanel];
+#pragma unroll
+        for (int cc = 0; cc < kPanel; ++cc) {
+          double d = 0.0;
+          if (cc > jj) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) d = fma(P[jj][t], P[cc][t], d);
+          }
+          v[cc] = d;
+        }
+        halve<kPanel, 16, kPanel>(v, lane);        // lane l holds the total of index l >> 1
+#pragma unroll
+        for (int cc = jj + 1; cc < kPanel; ++cc) {
+          const int c = j0 + cc;
+          const double dot = __shfl_sync(0xffffffffu, v[0], cc << 1);
+          if (c < m) {
+            const double rjc = Rp[rp_idx(j, c, m)];
+            const double w = tj * (rjc + dot);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) P[cc][t] = fma(-w, P[jj][t], P[cc][t]);
+            if (lane == 0) Rp[rp_idx(j, c, m)] = rjc - w;
+          }
+        }
+      }
+      __syncwarp();
+    }
   }
-  double s = (s0 + s1) + (s2 + s3);
-  s += __shfl_xor_sync(pair_mask, s, 1);
-  double t, beta, scale;
-  householder(Rs[j * kLdA + j], s, t, beta, scale);
 #pragma unroll
-  for (int i = r0; i < r0 + kBS / 2; ++i) bj[i * kLdB] *= scale;
-  if (half == 0) { tau[j] = t; Rs[j * kLdA + j] = beta; }
+  for (int cc = 0; cc < kPanel; ++cc)
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (j0 + cc < m) Bk[(lane + 32 * t) * kLdA + j0 + cc] = P[cc][t];
 }
 
-// Apply reflector j (v = [1 at R row j; Bk[:, j]], tau[j]) to column c whose block rows
-// r0..r0+kBS/2 are x[] (registers); the pair of lanes combines the two half dot products.
-__device__ __forceinline__ void qr_apply(const double *Rs_row_j, double *Rjc, const double *Bk, double t, int j,
-                                         int r0, int half, unsigned pair_mask, double (&x)[kBS / 2]) {
-  const double *vj = Bk + j;
-  double s0 = (half == 0) ? *Rjc : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-  for (int i = 0; i < kBS / 2; i += 4) {
-    s0 = fma(vj[(r0 + i) * kLdB], x[i], s0);
-    s1 = fma(vj[(r0 + i + 1) * kLdB], x[i + 1], s1);
-    s2 = fma(vj[(r0 + i + 2) * kLdB], x[i + 2], s2);
-    s3 = fma(vj[(r0 + i + 3) * kLdB], x[i + 3], s3);
-  }
-  double w = (s0 + s1) + (s2 + s3);
-  w += __shfl_xor_sync(pair_mask, w, 1);
-  w *= t;
-  if (half == 0) *Rjc -= w;
-#pragma unroll
-  for (int i = 0; i < kBS / 2; ++i) x[i] = fma(-w, vj[(r0 + i) * kLdB], x[i]);
-  (void)Rs_row_j;
-}
-
-__device__ void qr_of_TH(const double *T, int m, int n, double *Rs, double *Bk, double *tau) {
+__device__ void qr_of_TH(const double *T, int m, int n, double *Rp, double *Bk, double *tau) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int half = tid & 1, r0 = half * (kBS / 2);
+  const int half = tid & 1, r0 = half * (kSmall / 2);
   const unsigned pair_mask = 3u << (lane & ~1);
-  for (int i = tid; i < m * kLdA; i += kThreads) Rs[i] = 0.0;
-  for (int c0 = 0; c0 < n; c0 += kBS) {
-    const int nb = min(kBS, n - c0);
+  for (int i = tid; i < kRpDoubles; i += kThreads) Rp[i] = 0.0;
+  for (int c0 = 0; c0 < n; c0 += kSmall) {
+    const int nb = min(kSmall, n - c0);
     __syncthreads();
-    for (int idx = tid; idx < kBS * m; idx += kThreads) {
-      const int j = idx / kBS, i = idx % kBS;          // coalesced along i (columns of T)
-      Bk[i * kLdB + j] = (i < nb) ? T[(size_t)j * n + c0 + i] : 0.0;
+    for (int idx = tid; idx < kSmall * m; idx += kThreads) {
+      const int j = idx / kSmall, i = idx % kSmall;    // coalesced along i (columns of T)
+      Bk[i * kLdA + j] = (i < nb) ? T[(size_t)j * n + c0 + i] : 0.0;
     }
     __syncthreads();
     for (int j0 = 0; j0 < m; j0 += kPanel) {
       const int jn = min(j0 + kPanel, m);
-      // (1) panel factorisation by warp 0: lane pair pc owns panel column j0 + pc
-      if (warp == 0) {
-        const int c = j0 + (lane >> 1);
-        for (int j = j0; j < jn; ++j) {
-          if (c == j) qr_make_reflector(Rs, Bk, tau, j, r0, half, pair_mask);
-          __syncwarp();
-          if (c > j && c < jn) {
-            const double t = tau[j];
-            if (t != 0.0) {
-              double x[kBS / 2];
-#pragma unroll
-              for (int i = 0; i < kBS / 2; ++i) x[i] = Bk[(r0 + i) * kLdB + c];
-              qr_apply(nullptr, Rs + j * kLdA + c, Bk, t, j, r0, half, pair_mask, x);
-#pragma unroll
-              for (int i = 0; i < kBS / 2; ++i) Bk[(r0 + i) * kLdB + c] = x[i];
-            }
-          }
-          __syncwarp();
-        }
-      }
+      if (warp == 0) qr_panel(Rp, Bk, tau, m, j0);
       __syncthreads();
-      // (2) trailing update: columns jn..m-1, two threads per column, column in registers
       for (int c = jn + (tid >> 1); c < m; c += kThreads / 2) {
-        double x[kBS / 2];
+        double x[kSmall / 2];
 #pragma unroll
-        for (int i = 0; i < kBS / 2; ++i) x[i] = Bk[(r0 + i) * kLdB + c];
+        for (int i = 0; i < kSmall / 2; ++i) x[i] = Bk[(r0 + i) * kLdA + c];
         for (int j = j0; j < jn; ++j) {
           const double t = tau[j];
-          if (t != 0.0) qr_apply(nullptr, Rs + j * kLdA + c, Bk, t, j, r0, half, pair_mask, x);
+          if (t == 0.0) continue;
+          const double *vj = Bk + j;
+          double s0 = (half == 0) ? Rp[rp_idx(j, c, m)] : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+          for (int i = 0; i < kSmall / 2; i += 4) {
+            s0 = fma(vj[(r0 + i) * kLdA], x[i], s0);
+            s1 = fma(vj[(r0 + i + 1) * kLdA], x[i + 1], s1);
+            s2 = fma(vj[(r0 + i + 2) * kLdA], x[i + 2], s2);
+            s3 = fma(vj[(r0 + i + 3) * kLdA], x[i + 3], s3);
+          }
+          double w = (s0 + s1) + (s2 + s3);
+          w += __shfl_xor_sync(pair_mask, w, 1);
+          w *= t;
+          if (half == 0) Rp[rp_idx(j, c, m)] -= w;
+#pragma unroll
+          for (int i = 0; i < kSmall / 2; ++i) x[i] = fma(-w, vj[(r0 + i) * kLdA], x[i]);
         }
 #pragma unroll
-        for (int i = 0; i < kBS / 2; ++i) Bk[(r0 + i) * kLdB + c] = x[i];
+        for (int i = 0; i < kSmall / 2; ++i) Bk[(r0 + i) * kLdA + c] = x[i];
       }
       __syncthreads();
     }
@@ -304,9 +316,10 @@ __device__ void qr_of_TH(const double *T, int m, int n, double *Rs, double *Bk, 
 }
 
 __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, double *smem) {
-  double *Rs = smem;                         // kSmall x kLdA: R (row-major) == A = R^T (col-major)
-  double *Bk = Rs + kSmall * kLdA;           // QR block / GEMM staging / staged MPO core
-  double *sg = Bk + kBkDoubles;              // sigma^2 per column
+  double *Rp = smem;                         // packed R (QR) / GEMM staging / scratch
+  double *Rs = Rp + kRpDoubles;              // kSmall x kLdA: QR block, then A (col-major)
+  double *Bk = Rp;                           // staging alias
+  double *sg = Rs + kSmall * kLdA;           // sigma^2 per column
   double *red = sg + kSmall;                 // block-reduction scratch
   double *scal = red + 8;                    // scalars
   double *tau = scal + 8;                    // Householder tau per column
@@ -397,7 +410,12 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
   int p;
   if (m <= n) {
     p = m;
-    qr_of_TH(T, m, n, Rs, Bk, tau);                // A = R^T: column j of A = row j of R
+    qr_of_TH(T, m, n, Rp, Rs, tau);
+    __syncthreads();
+    for (int idx = tid; idx < m * m; idx += kThreads) {   // A = R^T: column j of A = row j of R
+      const int j = idx / m, row = idx % m;
+      Rs[(size_t)j * kLdA + row] = (row >= j) ? Rp[rp_idx(j, row, m)] : 0.0;
+    }
   } else {
     p = n;                                         // A = T (m x n): column j = T[:, j]
     for (int idx = tid; idx < m * n; idx += kThreads) {
