@@ -44,26 +44,9 @@ __device__ __forceinline__ void halve(double (&v)[NV], int lane) {
 template <int N>
 __device__ constexpr int ilog2() { return N <= 1 ? 0 : 1 + ilog2<N / 2>(); }
 
-// Pair a of an inner round.  MODE 0: cross pairs (a, WB + (a+S)%WB).  MODE 1: intra-block
-// pairs of round S of the circle method on WB players, in block I for a < WB/2, else in J.
-template <int WB, int MODE, int S>
-__device__ constexpr int pair_i(int a) {
-  if (MODE == 0) return a;
-  const int h = WB / 2, t = (a < h) ? a : a - h, base = (a < h) ? 0 : WB;
-  const int k = t;
-  return base + ((k == 0) ? 0 : 1 + (k - 1 + S) % (WB > 1 ? WB - 1 : 1));
-}
-template <int WB, int MODE, int S>
-__device__ constexpr int pair_j(int a) {
-  if (MODE == 0) return WB + (a + S) % WB;
-  const int h = WB / 2, t = (a < h) ? a : a - h, base = (a < h) ? 0 : WB;
-  const int k = WB - 1 - t;
-  return base + ((k == 0) ? 0 : 1 + (k - 1 + S) % (WB > 1 ? WB - 1 : 1));
-}
-
 // Exact squared norms of the warp's 2*WB register columns -> nrm[0..2WB) (shared, per warp).
 template <int RPL, int WB>
-__device__ __forceinline__ void warp_norms(const double (&X)[2 * WB][RPL], double *nrm) {
+__device__ __forceinline__ void warp_norms(const double (&X)[2 * WB][RPL], double *nrm, const int *slot_col) {
   constexpr int NC = 2 * WB;
   constexpr int NV = (NC <= 4) ? 4 : (NC <= 8) ? 8 : (NC <= 16) ? 16 : 32;
   const int lane = threadIdx.x & 31;
@@ -79,23 +62,34 @@ __device__ __forceinline__ void warp_norms(const double (&X)[2 * WB][RPL], doubl
   for (int k = NC; k < NV; ++k) v[k] = 0.0;
   halve<NV, 16, NV>(v, lane);
   constexpr int sh = 5 - ilog2<NV>();
-  if ((lane & ((1 << sh) - 1)) == 0 && (lane >> sh) < NC) nrm[lane >> sh] = v[0];
+  if ((lane & ((1 << sh) - 1)) == 0 && (lane >> sh) < NC) nrm[slot_col[lane >> sh]] = v[0];
   __syncwarp();
 }
 
-// One inner round: NP disjoint column pairs.  Column norms come from nrm[] (kept up to date
-// by the exact rotation identities a' = a - t*g, b' = b + t*g, refreshed exactly when a
-// norm collapses by more than sqrt(eps), as in LAPACK dgesvj); only the NP cross dot
-// products g are reduced across the warp.
-template <int RPL, int WB, int MODE, int S>
-__device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm, double tol, int &rot) {
+// One inner round on NP fixed register pairs (P0 + a, P1 + a*D1 ... see pair_slots):
+//   MODE 0 (cross):  pairs (a, WB + a),              a < WB
+//   MODE 1 (intra):  pairs (t, WB-1-t), (WB+t, 2WB-1-t), t < WB/2
+// The caller rotates registers between rounds so that these fixed slots walk through the
+// round-robin orderings.  slot_col[k] maps register slot k to its column's norm index.
+template <int WB, int MODE>
+__device__ __forceinline__ constexpr int slot_i(int a) {
+  return MODE == 0 ? a : (a < WB / 2 ? a : WB + (a - WB / 2));
+}
+template <int WB, int MODE>
+__device__ __forceinline__ constexpr int slot_j(int a) {
+  return MODE == 0 ? WB + a : (a < WB / 2 ? WB - 1 - a : 2 * WB - 1 - (a - WB / 2));
+}
+
+template <int RPL, int WB, int MODE>
+__device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm, const int *slot_col,
+                                          double tol, int &rot) {
   constexpr int NP = (MODE == 0) ? WB : 2 * (WB / 2);   // pairs in this round
   constexpr int NV = (NP <= 4) ? 4 : (NP <= 8) ? 8 : (NP <= 16) ? 16 : 32;
   const int lane = threadIdx.x & 31;
   double v[NV];
 #pragma unroll
   for (int a = 0; a < NP; ++a) {
-    const int i = pair_i<WB, MODE, S>(a), j = pair_j<WB, MODE, S>(a);
+    const int i = slot_i<WB, MODE>(a), j = slot_j<WB, MODE>(a);
     double g0 = 0.0, g1 = 0.0;
 #pragma unroll
     for (int t = 0; t < RPL; t += 2) {
@@ -110,11 +104,12 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm,
   constexpr int sh = 5 - ilog2<NV>();
   const int a = lane % NP;
   const double ga = __shfl_sync(0xffffffffu, v[0], a << sh);
-  int ia = 0, ja = 0;
+  int si = 0, sj = 0;
 #pragma unroll
   for (int k = 0; k < NP; ++k)
-    if (a == k) { ia = pair_i<WB, MODE, S>(k); ja = pair_j<WB, MODE, S>(k); }
-  const double al = nrm[ia], be = nrm[ja];
+    if (a == k) { si = slot_i<WB, MODE>(k); sj = slot_j<WB, MODE>(k); }
+  const int ci = slot_col[si], cj = slot_col[sj];
+  const double al = nrm[ci], be = nrm[cj];
   // Rotation angle (Rutishauser): t = sign(d) 2g / (|d| + sqrt(d^2 + 4g^2)), d = b - a;
   // c = 1/sqrt(1+t^2), s = c t.  Rotate only if |g| > tol sqrt(a b) (squared test).
   const double d = be - al;
@@ -130,41 +125,78 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm,
   const bool collapse = doit && (al2 < 1.5e-8 * al || be2 < 1.5e-8 * be);
   if (__any_sync(0xffffffffu, doit)) rot = 1;
   __syncwarp();
-  if (lane < NP) { nrm[ia] = al2; nrm[ja] = be2; }
+  if (lane < NP) { nrm[ci] = al2; nrm[cj] = be2; }
 #pragma unroll
   for (int a2 = 0; a2 < NP; ++a2) {
-    const int i = pair_i<WB, MODE, S>(a2), j = pair_j<WB, MODE, S>(a2);
+    const int i = slot_i<WB, MODE>(a2), j = slot_j<WB, MODE>(a2);
     const double ca = __shfl_sync(0xffffffffu, c, a2), sa = __shfl_sync(0xffffffffu, s, a2);
 #pragma unroll
-    for (int t = 0; t < RPL; ++t) {
-      const double x = X[i][t], y = X[j][t];
-      X[i][t] = fma(ca, x, -sa * y);
-      X[j][t] = fma(sa, x, ca * y);
+    for (int tt = 0; tt < RPL; ++tt) {
+      const double x = X[i][tt], y = X[j][tt];
+      X[i][tt] = fma(ca, x, -sa * y);
+      X[j][tt] = fma(sa, x, ca * y);
     }
   }
   __syncwarp();
-  if (__any_sync(0xffffffffu, collapse)) warp_norms<RPL, WB>(X, nrm);   // cancellation: refresh exactly
+  if (__any_sync(0xffffffffu, collapse)) warp_norms<RPL, WB>(X, nrm, slot_col);   // refresh exactly
 }
 
-template <int RPL, int WB, int MODE, int S, int SEND>
-__device__ __forceinline__ void jac_rounds(double (&X)[2 * WB][RPL], double *nrm, double tol, int &rot) {
-  if constexpr (S < SEND) {
-    jac_round<RPL, WB, MODE, S>(X, nrm, tol, rot);
-    jac_rounds<RPL, WB, MODE, S + 1, SEND>(X, nrm, tol, rot);
+// Register rotations that advance the fixed-slot pairings to the next round-robin round.
+template <int RPL, int WB>
+__device__ __forceinline__ void rotate_J(double (&X)[2 * WB][RPL], int *slot_col) {
+  // slot WB+a <- slot WB+(a+1)%WB  (cross rounds: J walks past I)
+#pragma unroll
+  for (int t = 0; t < RPL; ++t) {
+    const double first = X[WB][t];
+#pragma unroll
+    for (int a = 0; a < WB - 1; ++a) X[WB + a][t] = X[WB + a + 1][t];
+    X[2 * WB - 1][t] = first;
   }
+  if ((threadIdx.x & 31) == 0) {
+    const int f = slot_col[WB];
+    for (int a = 0; a < WB - 1; ++a) slot_col[WB + a] = slot_col[WB + a + 1];
+    slot_col[2 * WB - 1] = f;
+  }
+  __syncwarp();
+}
+template <int RPL, int WB>
+__device__ __forceinline__ void rotate_circle(double (&X)[2 * WB][RPL], int *slot_col) {
+  // circle method inside each block: position 0 fixed, positions 1..WB-1 rotate by one
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int o = h * WB;
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) {
+      const double first = X[o + 1][t];
+#pragma unroll
+      for (int k = 1; k < WB - 1; ++k) X[o + k][t] = X[o + k + 1][t];
+      X[o + WB - 1][t] = first;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    for (int h = 0; h < 2; ++h) {
+      const int o = h * WB;
+      const int f = slot_col[o + 1];
+      for (int k = 1; k < WB - 1; ++k) slot_col[o + k] = slot_col[o + k + 1];
+      slot_col[o + WB - 1] = f;
+    }
+  }
+  __syncwarp();
 }
 
 // Returns the number of sweeps executed (== kJacobiMaxSweeps: not converged).
 template <int RPL, int WB>
-__device__ int jacobi_blocked(double *A, int m, int *flag, double *nrm_all) {
+__device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
   constexpr int NB = 2 * kWarps;      // 16 blocks of WB columns
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double tol = (double)max(m, 1) * DBL_EPSILON;
   double X[2 * WB][RPL];
-  double *nrm = nrm_all + warp * 2 * WB;
+  double *nrm = scratch + warp * 2 * WB;                                   // norms by local column
+  int *slot_col = reinterpret_cast<int *>(scratch + kWarps * 2 * WB) + warp * 2 * WB;
   int sweep = 0;
   for (; sweep < kJacobiMaxSweeps; ++sweep) {
     int rot = 0;
+#pragma unroll 1
     for (int r = 0; r < NB - 1; ++r) {
       const int kI = warp, kJ = NB - 1 - warp;                      // circle method positions
       const int I = (kI == 0) ? 0 : 1 + (kI - 1 + r) % (NB - 1);
@@ -176,11 +208,24 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *nrm_all) {
           X[c][t] = A[(size_t)(I * WB + c) * kLdA + lane + 32 * t];
           X[WB + c][t] = A[(size_t)(J * WB + c) * kLdA + lane + 32 * t];
         }
-      warp_norms<RPL, WB>(X, nrm);
+      if (lane < 2 * WB) slot_col[lane] = lane;
+      __syncwarp();
+      warp_norms<RPL, WB>(X, nrm, slot_col);
       if constexpr (WB > 1) {
-        if (r == 0) jac_rounds<RPL, WB, 1, 0, WB - 1>(X, nrm, tol, rot);
+        if (r == 0) {
+#pragma unroll 1
+          for (int u = 0; u < WB - 1; ++u) {
+            jac_round<RPL, WB, 1>(X, nrm, slot_col, tol, rot);
+            rotate_circle<RPL, WB>(X, slot_col);
+          }
+        }
       }
-      jac_rounds<RPL, WB, 0, 0, WB>(X, nrm, tol, rot);
+#pragma unroll 1
+      for (int u = 0; u < WB; ++u) {
+        jac_round<RPL, WB, 0>(X, nrm, slot_col, tol, rot);
+        if (WB > 1) rotate_J<RPL, WB>(X, slot_col);
+      }
+      // slots are back in natural order (WB-1 circle rotations and WB J rotations = identity)
 #pragma unroll
       for (int c = 0; c < WB; ++c)
 #pragma unroll
