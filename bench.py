@@ -27,6 +27,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_2602_20226_b200 import dist as qdist  # noqa: E402
 from paper_2602_20226_b200 import gen  # noqa: E402
 
 METRIC = "zip-up site-contractions/sec"
@@ -53,7 +54,8 @@ def build_workload(args, rank):
     """Returns (subscripts, kind, problems (list of gen.Problem for this rank), x_stack, op_stack, cfg dict)."""
     if args.workload == "cfg5":
         M = args.members_per_gpu
-        members = list(range(rank * M, (rank + 1) * M))
+        lo, hi = qdist.member_range(rank, args.gpus, M)
+        members = list(range(lo, hi))
         probs, xs, ops = gen.cfg5_batch_arrays(members)
         p0 = probs[0]
         cfg = {"workload": "configs[4] cfg5: batch of independent zip-ups, L=40 d=2, state rank 64 N(0,1/64), "
@@ -201,6 +203,8 @@ def oracle_sample(kind, probs, n_members):
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        args.gpus = world
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
@@ -229,8 +233,7 @@ def main():
     def step(events=None):
         res = plan.run(od, xd, events=events)
         s = qtt.summary(res)
-        if world > 1:
-            dist.all_reduce(s)
+        qdist.allreduce_summary(s, dist)          # the one cross-GPU exchange (a8)
         summary.copy_(s)
         return res
 
@@ -262,10 +265,7 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     ms = t0.elapsed_time(t1) / args.steps
-    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+    ms_max = qdist.max_over_ranks(ms, "cuda", dist)
 
     # per-kernel device time of the dominant kernel (k_site) from the live events
     site_ms = sum(ev[2].elapsed_time(ev[3]) for ev in ev_sets)
@@ -325,11 +325,9 @@ def main():
             e2e_step()
         a1.record(stream)
         torch.cuda.synchronize()
-        ems = torch.tensor([a0.elapsed_time(a1) / args.steps], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-        e2e = {"value": units / (float(ems.item()) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(float(ems.item()), 3)}
+        ems = qdist.max_over_ranks(a0.elapsed_time(a1) / args.steps, "cuda", dist)
+        e2e = {"value": units / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ems, 3)}
 
     # ---------------- CPU oracle baseline + sampled parity (rank 0, N=1 only)
     cpu = None
@@ -369,8 +367,7 @@ def main():
             "jacobi_sweeps": {"mean": float(sweeps[:, :-1].mean()), "max": int(sweeps.max())},
             "cpu_baseline": cpu, "parity_sample": parity, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "clocks": clk,
-            "summary": {"sum_delta2": float(summary[0]), "sum_norm2": float(summary[1]),
-                        "rel_trunc_est": math.sqrt(float(summary[0]) / max(float(summary[1]), 1e-300))},
+            "summary": qdist.summary_dict(summary.cpu().tolist()),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
