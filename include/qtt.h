@@ -126,6 +126,25 @@ qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt
                        const qtt_zipup_diag_t *diag, void *workspace, size_t workspace_bytes,
                        void *stream);
 
+/* ---------------------------------------------------------------------------------------
+ * qtt_round -- rounding / truncation of a train (PAPER.md:710 ``TensorTrain.truncate``;
+ * SURVEY.md §8(f) f1): a right-to-left truncated-SVD sweep with the SPEC.md:299 rule, run
+ * as the truncate-mode zip-up ("i->i") of the mirrored train (site order reversed, bond
+ * axes swapped), then mirrored back.  Applied to a zip-up output (left-canonical) it is the
+ * classical TT rounding and reaches the minimal ranks.
+ *   x          : input trains (n_legs 1); x->ranks are capacities; x_ranks (device int32
+ *                [B*(L+1)]) gives each member's actual ranks (cores packed inside the
+ *                capacity slots, as qtt_zipup writes them); NULL = packed at x->ranks.
+ *   out        : output trains; out->ranks are capacities >= qtt_round_capacity.
+ *   out_ranks, delta2 (per split, right-to-left order reversed back to site order: delta2[b*L+q]
+ *                is the mass discarded at bond q+1), norm2, status: as for qtt_zipup.
+ */
+qtt_status_t qtt_round_capacity(const qtt_trains_t *x, int32_t max_rank, int32_t *cap);
+size_t qtt_round_workspace_bytes(const qtt_trains_t *x, int32_t max_rank);
+qtt_status_t qtt_round(const qtt_trains_t *x, const int32_t *x_ranks, double eps, int32_t max_rank,
+                       const qtt_trains_t *out, int32_t *out_ranks, double *delta2, double *norm2,
+                       int32_t *status, void *workspace, size_t workspace_bytes, void *stream);
+
 /* qtt_zipup_summary -- the per-batch scalars that are all-reduced across GPUs
  * (SURVEY.md §8(a) a8): summary4 (device f64 [4]) = [sum_b sum_q delta2, sum_b norm2,
  * sum_b sum_q out_ranks[b][q+1] (q < L-1), B].  Deterministic fixed-order sums. */

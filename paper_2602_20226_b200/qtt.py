@@ -44,6 +44,7 @@ class _Trains(ctypes.Structure):
 _lib = None
 
 SYMBOLS = ["qtt_zipup_capacity", "qtt_zipup_workspace_bytes", "qtt_zipup", "qtt_zipup_summary",
+           "qtt_round_capacity", "qtt_round_workspace_bytes", "qtt_round",
            "qtt_einsum_exact", "qtt_inner_workspace_bytes", "qtt_inner", "qtt_to_dense_workspace_bytes",
            "qtt_to_dense", "qtt_last_error", "qtt_version"]
 
@@ -67,6 +68,12 @@ def load_library(path: str = LIB_PATH):
     L.qtt_zipup.restype = i32
     L.qtt_zipup_summary.argtypes = [i32, i32, vp, vp, vp, vp, vp]
     L.qtt_zipup_summary.restype = i32
+    L.qtt_round_capacity.argtypes = [P, i32, ctypes.POINTER(i32)]
+    L.qtt_round_capacity.restype = i32
+    L.qtt_round_workspace_bytes.argtypes = [P, i32]
+    L.qtt_round_workspace_bytes.restype = sz
+    L.qtt_round.argtypes = [P, vp, f64, i32, P, vp, vp, vp, vp, vp, sz, vp]
+    L.qtt_round.restype = i32
     L.qtt_einsum_exact.argtypes = [ctypes.c_char_p, P, P, P, vp]
     L.qtt_einsum_exact.restype = i32
     L.qtt_inner_workspace_bytes.argtypes = [P, P]
@@ -254,6 +261,30 @@ class ZipupPlan:
 def zipup(subscripts: str, op: Optional[DeviceTrains], x: DeviceTrains, eps: float, max_rank: int,
           flags: int = 0, sigma_stride: int = 0, stream=None) -> ZipupResult:
     return ZipupPlan(subscripts, op, x, eps, max_rank, flags, sigma_stride, sweeps=True).run(op, x, stream)
+
+
+def round_train(x: DeviceTrains, x_ranks: Optional[torch.Tensor], eps: float, max_rank: int,
+                stream=None) -> ZipupResult:
+    """qtt_round: right-to-left truncated-SVD sweep.  x_ranks: device int32
+    (B, L+1) actual ranks of x's members (as qtt_zipup writes them), or None."""
+    L = load_library()
+    xs, kx = x.c_struct()
+    cap = (ctypes.c_int32 * (x.n_sites + 1))()
+    _check(L.qtt_round_capacity(ctypes.byref(xs), int(max_rank), cap))
+    dev = x.cores[0].device
+    out = empty_like_capacity(x.batch, x.d_out, list(cap), dev)
+    os_, ko = out.c_struct()
+    B, n = x.batch, x.n_sites
+    ranks = torch.zeros((B, n + 1), dtype=torch.int32, device=dev)
+    delta2 = torch.zeros((B, n), dtype=torch.float64, device=dev)
+    norm2 = torch.zeros((B,), dtype=torch.float64, device=dev)
+    status = torch.zeros((1,), dtype=torch.int32, device=dev)
+    nbytes = L.qtt_round_workspace_bytes(ctypes.byref(xs), int(max_rank))
+    ws = torch.empty(max(nbytes, 8), dtype=torch.uint8, device=dev)
+    _check(L.qtt_round(ctypes.byref(xs), x_ranks.data_ptr() if x_ranks is not None else None, float(eps),
+                       int(max_rank), ctypes.byref(os_), ranks.data_ptr(), delta2.data_ptr(), norm2.data_ptr(),
+                       status.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+    return ZipupResult(out, ranks, delta2, norm2, status, None, None, ws)
 
 
 def summary(res: ZipupResult, stream=None) -> torch.Tensor:

@@ -156,3 +156,45 @@ def test_nonfinite_input_flagged(lib):
     res = lib.ZipupPlan("i->i", None, xd, 1e-8, 4).run(None, xd)
     torch.cuda.synchronize()
     assert int(res.status.item()) & 1
+
+
+def test_round_after_zipup_reaches_minimal_ranks(lib):
+    """f1: qtt_round on the cfg1 zip-up output == oracle round_train, and the ranks equal the
+    numerical ranks of the dense result's unfoldings."""
+    import torch
+    from oracle import tt
+    from oracle.zipup import zipup as ozip
+    p = gen.cfg1(10)
+    res = run_gpu(lib, "matvec", p.op.cores, p.x.cores, p.eps, p.max_rank)
+    rr = lib.round_train(res.out, res.ranks, 1e-12, 0)
+    torch.cuda.synchronize()
+    assert int(rr.status.item()) == 0
+    ranks = rr.ranks[0].cpu().tolist()
+    y = lib.member_cores(rr.out, ranks, 0)
+    ref_zip = ozip("matvec", p.op.cores, p.x.cores, p.eps, p.max_rank)
+    ref = tt.round_train(ref_zip["cores"], 1e-12, 0)
+    assert ranks == tt.ranks_of(ref)
+    yd = tt.to_dense_vector(ref_zip["cores"])
+    dense_ranks = [tt.truncation_rank(np.linalg.svd(yd.reshape(2 ** k, -1), compute_uv=False), 1e-12, 0)
+                   for k in range(1, 10)]
+    assert ranks[1:-1] == dense_ranks
+    yv, rv = tt.to_dense_vector(y), tt.to_dense_vector(ref)
+    assert np.linalg.norm(yv - rv) <= 1e-10 * np.linalg.norm(rv)
+
+
+def test_round_redundant_and_max_rank(lib):
+    """Rounding a redundant representation (x + x, formal rank 2r) to max_rank: equals the
+    oracle's rounding of the same train."""
+    import torch
+    from oracle import tt
+    x = gen.random_mps([2, 3, 2, 2, 3, 2], 4, np.random.default_rng(21)).cores
+    xx = tt.add(x, x)
+    xd = lib.to_device(xx)
+    for mr, eps in ((0, 1e-12), (3, 0.0)):
+        rr = lib.round_train(xd, None, eps, mr)
+        torch.cuda.synchronize()
+        ranks = rr.ranks[0].cpu().tolist()
+        ref = tt.round_train(xx, eps, mr)
+        assert ranks == tt.ranks_of(ref)
+        yv, rv = tt.to_dense_vector(lib.member_cores(rr.out, ranks, 0)), tt.to_dense_vector(ref)
+        assert np.linalg.norm(yv - rv) <= 1e-10 * np.linalg.norm(rv)
