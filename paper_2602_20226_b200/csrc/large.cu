@@ -1,0 +1,1027 @@
+// large.cu -- large-member path of qtt_zipup: site matrices with m > 128 rows
+// (BASELINE.json configs[1..3] at full size: T up to 512 x 65536 (cfg3) or 2560 x 1000 (cfg4)).
+//
+// One member at a time (these configs are single zip-ups); every kernel reads the site's
+// dimensions from a device SiteDims record written by k_plan, so ranks stay on the device
+// and grids are sized by capacity (surplus CTAs exit).  Per site q:
+//   a2  k_gemm_spec (strided batched GEMM) [+ k_mpo_apply]      T = contract(G, x_q, op_q)
+//   a3  m <= n: k_qr_coop  -- cooperative, row-distributed Householder QR of T^H with grid
+//                             barriers (16-column panels, WY trailing update, fixed-order
+//                             reductions); robust to the exact rank deficiency that cfg2/cfg4
+//                             site matrices show (kappa ~ 1e16), unlike Cholesky-QR.
+//       m >  n: k_transpose -- A = T
+//   a4  k_jacobi_coop -- one-sided Jacobi, block round-robin over CTAs, columns in shared
+//                        memory, exact dot products, grid barrier per block round
+//   a5/a6 k_finish (sigma, sort, truncation, emit U_k) + k_gemm_spec carry G = U_k^T T
+//   a7  k_last
+// Operands too large for the shared-memory a1 kernel are right-orthonormalised by the
+// mirrored truncate sweep (an SVD gauge instead of QR: the zip-up result is gauge
+// invariant).
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+#include <algorithm>
+#include <vector>
+
+#include "large.cuh"
+
+namespace qtt {
+
+// ------------------------------------------------------------------ grid barrier
+
+struct GridBar {
+  unsigned count;
+  unsigned gen;
+  unsigned err;
+  unsigned pad;
+};
+
+// All CTAs of a cooperative launch.  Release/acquire at gpu scope; the fence after the
+// acquire also invalidates this SM's L1 so data written by other CTAs is re-read from L2.
+// A barrier that does not complete within ~seconds records an error (reported through the
+// zip-up status word) and lets the kernel finish instead of hanging the GPU.
+__device__ __forceinline__ void grid_sync(GridBar *gb, unsigned nblocks, int tag = 0) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned g;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(&gb->gen) : "memory");
+    __threadfence();
+    const unsigned arrived = atomicAdd(&gb->count, 1u);
+    if (arrived == nblocks - 1) {
+      atomicExch(&gb->count, 0u);
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&gb->gen), "r"(g + 1) : "memory");
+    } else {
+      unsigned v;
+      long long spins = 0;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&gb->gen) : "memory");
+        if (v == g) __nanosleep(32);
+        if (++spins > (1LL << 24)) {
+          if (atomicExch(&gb->err, 1u) == 0u)
+            printf("qtt grid barrier timeout: tag %d cta %d/%u gen %u count %u\n", tag, (int)blockIdx.x, nblocks, g,
+                   *((volatile unsigned *)&gb->count));
+          break;
+        }
+      } while (v == g);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ site plan
+
+struct SiteDims {
+  int chi, r, r2, w, w2, d, dj, m, n, p, direct, k;
+};
+
+struct GemmSpec {
+  int M, N, K, nz1, nz2;
+  const double *A;
+  const double *B;
+  double *C;
+  long long sam, sak, sbk, sbn, scm, scn;
+  long long sa1, sa2, sb1, sb2, sc1, sc2;
+};
+
+struct PlanArgs {
+  int q, L, kind, d, dj;
+  const int *xr, *orr, *yr;     // member-offset rank rows
+  const double *Xq, *Oq;
+  double *G, *X, *T, *Cq;
+  SiteDims *dims;
+  GemmSpec *spec;               // [0] state GEMM, [1] Hadamard apply, [2] carry (k filled later)
+};
+
+__global__ void k_plan(PlanArgs a) {
+  if (threadIdx.x != 0) return;
+  SiteDims D;
+  D.chi = (a.q == 0) ? 1 : a.yr[a.q];
+  D.r = a.xr[a.q]; D.r2 = a.xr[a.q + 1];
+  D.w = 1; D.w2 = 1;
+  if (a.kind != TRUNCATE) { D.w = a.orr[a.q]; D.w2 = a.orr[a.q + 1]; }
+  D.d = a.d; D.dj = a.dj;
+  D.m = D.chi * D.d; D.n = D.w2 * D.r2;
+  D.direct = (D.m > D.n);
+  D.p = D.direct ? D.n : D.m;
+  D.k = 0;
+  *a.dims = D;
+  GemmSpec g0{};   // X = G (chi*w x r) * x_q (r x dj*r2)   [truncate: T = G (chi x r) * x_q]
+  g0.M = D.chi * D.w; g0.K = D.r; g0.N = ((a.kind == HADAMARD || a.kind == TRUNCATE) ? D.d : D.dj) * D.r2;
+  g0.nz1 = 1; g0.nz2 = 1;
+  g0.A = a.G; g0.sam = g0.K; g0.sak = 1;
+  g0.B = a.Xq; g0.sbk = g0.N; g0.sbn = 1;
+  g0.C = (a.kind == TRUNCATE) ? a.T : a.X; g0.scm = g0.N; g0.scn = 1;
+  a.spec[0] = g0;
+  GemmSpec g1{};   // Hadamard: T[c,i,a2,b2] = sum_a A[a,i,a2] X[c,a,i,b2], batched over (c, i)
+  g1.M = D.w2; g1.N = D.r2; g1.K = D.w; g1.nz1 = D.chi; g1.nz2 = D.d;
+  g1.A = a.Oq; g1.sam = 1; g1.sak = (long long)D.d * D.w2; g1.sa1 = 0; g1.sa2 = D.w2;
+  g1.B = a.X; g1.sbk = (long long)D.d * D.r2; g1.sbn = 1;
+  g1.sb1 = (long long)D.w * D.d * D.r2; g1.sb2 = D.r2;
+  g1.C = a.T; g1.scm = D.r2; g1.scn = 1; g1.sc1 = (long long)D.d * D.w2 * D.r2; g1.sc2 = (long long)D.w2 * D.r2;
+  a.spec[1] = g1;
+}
+
+// C = A * B per spec; grid x = tiles (tiles_n per row of tiles), z = nz1*nz2 (capacity).
+__global__ void __launch_bounds__(kThreads) k_gemm_spec(const GemmSpec *spec, int tiles_n, int nz2_cap) {
+  __shared__ double sm[2 * 16 * 64];
+  const GemmSpec g = *spec;
+  const int z1 = blockIdx.z / nz2_cap, z2 = blockIdx.z % nz2_cap;
+  if (z1 >= g.nz1 || z2 >= g.nz2) return;
+  const int m0 = (blockIdx.x / tiles_n) * 64, n0 = (blockIdx.x % tiles_n) * 64;
+  if (m0 >= g.M || n0 >= g.N) return;
+  const double *A = g.A + z1 * g.sa1 + z2 * g.sa2 + m0 * g.sam;
+  const double *B = g.B + z1 * g.sb1 + z2 * g.sb2 + n0 * g.sbn;
+  double *C = g.C + z1 * g.sc1 + z2 * g.sc2 + m0 * g.scm + n0 * g.scn;
+  cta_gemm(min(64, g.M - m0), min(64, g.N - n0), g.K,
+           [&](int i, int k) { return A[i * g.sam + k * g.sak]; },
+           [&](int k, int j) { return B[k * g.sbk + j * g.sbn]; },
+           [&](int i, int j, double v) { C[i * g.scm + j * g.scn] = v; }, sm);
+}
+
+static void launch_gemm_spec(const GemmSpec *spec, long long Mcap, long long Ncap, long long nz1cap, long long nz2cap,
+                             cudaStream_t s) {
+  const long long tm = (Mcap + 63) / 64, tn = (Ncap + 63) / 64;
+  dim3 grid((unsigned)(tm * tn), 1, (unsigned)(nz1cap * nz2cap));
+  k_gemm_spec<<<grid, kThreads, 0, s>>>(spec, (int)tn, (int)nz2cap);
+}
+
+// T[c,i,w2,r2] = sum_{w,j} X[c,w,j,r2] W[w,i,j,w2]
+__global__ void k_mpo_apply(const SiteDims *dims, const double *X, const double *W, double *T) {
+  const SiteDims D = *dims;
+  const long long total = (long long)D.m * D.n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int rr2 = (int)(idx % D.r2);
+    long long t1 = idx / D.r2;
+    const int ww2 = (int)(t1 % D.w2); t1 /= D.w2;
+    const int ii = (int)(t1 % D.d);
+    const long long c = t1 / D.d;
+    double s = 0.0;
+    for (int ww = 0; ww < D.w; ++ww)
+      for (int jj = 0; jj < D.dj; ++jj)
+        s = fma(X[((c * D.w + ww) * D.dj + jj) * D.r2 + rr2], W[(((long long)ww * D.d + ii) * D.dj + jj) * D.w2 + ww2], s);
+    T[idx] = s;
+  }
+}
+
+__global__ void k_copy_T(const SiteDims *dims, const double *T, double *Tw, double *A) {
+  const SiteDims D = *dims;
+  const long long total = (long long)D.m * D.n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const double v = T[idx];
+    if (D.direct) {   // A (m x n) column-major: A[j*m + row] = T[row*n + j]
+      const long long row = idx / D.n, j = idx % D.n;
+      A[j * D.m + row] = v;
+    } else {
+      Tw[idx] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ a3: cooperative QR
+
+constexpr int kNb = 16;              // panel width
+constexpr int kQrRowsMax = 512;      // max T^H rows per CTA held in shared memory (panel)
+
+struct QrArgs {
+  const SiteDims *dims;
+  double *Tw;          // m x n row-major; T^H column c = row c (length n)
+  double *Rout;        // m x m row-major R (zeros below the diagonal) == A column-major
+  double *part;        // [G][kNb * mcap]  partial sums
+  double *wtot;        // [kNb * mcap]     reduced W
+  double *gram;        // [kNb * kNb]      reduced Y^T Y
+  double *bc;          // broadcast scalars: [0] alpha
+  GridBar *bar;
+  int G, RB, mcap;
+};
+
+// Reduce a per-CTA scalar triple of arrays: block sum of v over kThreads.
+__device__ __forceinline__ double block_sum_l(double v, double *red) { return block_sum(v, red); }
+
+__global__ void __launch_bounds__(kThreads, 1) k_qr_coop(QrArgs a) {
+  extern __shared__ double smq[];
+  const SiteDims D = *a.dims;
+  if (D.direct) return;                         // uniform across the grid
+  const int m = D.m, n = D.n, g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r0 = g * a.RB, r1 = min(n, r0 + a.RB), nr = max(0, r1 - r0);
+  double *P = smq;                              // [kNb][RB] panel (my rows)
+  double *Y = P + kNb * a.RB;                   // [kNb][RB] reflectors (unit diagonal explicit)
+  double *red = Y + kNb * a.RB;                 // [kThreads/32]
+  double *tw = red + 32;                        // [kNb*kNb] T_wy ; [kNb] tau ; [kNb] dots
+  double *tau = tw + kNb * kNb;
+  double *dots = tau + kNb;
+  double *Mt = dots + kNb;                      // [kNb * 64] chunk of T_wy^T W
+  const unsigned G = a.G;
+  for (int j0 = 0; j0 < m; j0 += kNb) {
+    const int nb = min(kNb, m - j0);
+    // load the panel (T^H columns j0..j0+nb, my rows)
+    for (int idx = tid; idx < nb * nr; idx += kThreads) {
+      const int cc = idx / nr, i = idx % nr;
+      P[cc * a.RB + i] = a.Tw[(size_t)(j0 + cc) * n + r0 + i];
+    }
+    __syncthreads();
+    // norm partial of column j0
+    for (int jj = 0; jj < nb; ++jj) {
+      const int j = j0 + jj;
+      {
+        double s = 0.0;
+        for (int i = tid; i < nr; i += kThreads)
+          if (r0 + i > j) s = fma(P[jj * a.RB + i], P[jj * a.RB + i], s);
+        s = block_sum_l(s, red);
+        if (tid == 0) {
+          a.part[(size_t)g * kNb * a.mcap] = s;
+          if (j >= r0 && j < r1) a.bc[0] = P[jj * a.RB + (j - r0)];
+        }
+      }
+      grid_sync(a.bar, G, 1);
+      double tj, beta, scale;
+      {
+        double s = 0.0;
+        for (unsigned gg = 0; gg < G; ++gg) s += a.part[(size_t)gg * kNb * a.mcap];
+        householder(a.bc[0], s, tj, beta, scale);
+      }
+      if (tid == 0) tau[jj] = tj;
+      // v: rows > j scaled; row j -> beta (R diagonal), v_j = 1 implicit
+      for (int i = tid; i < nr; i += kThreads) {
+        const int r = r0 + i;
+        if (r > j) P[jj * a.RB + i] *= scale;
+        else if (r == j) P[jj * a.RB + i] = beta;
+      }
+      __syncthreads();
+      // dots with the remaining panel columns: sum_{r >= j} v_r P[cc][r]
+      for (int cc = jj + 1 + warp; cc < nb; cc += kWarps) {
+        double s = 0.0;
+        for (int i = lane; i < nr; i += 32) {
+          const int r = r0 + i;
+          if (r > j) s = fma(P[jj * a.RB + i], P[cc * a.RB + i], s);
+          else if (r == j) s += P[cc * a.RB + i];
+        }
+        s = warp_sum(s);
+        if (lane == 0) a.part[(size_t)g * kNb * a.mcap + 1 + cc] = s;
+      }
+      grid_sync(a.bar, G, 2);
+      if (tid < kNb) {
+        double s = 0.0;
+        if (tid > jj && tid < nb)
+          for (unsigned gg = 0; gg < G; ++gg) s += a.part[(size_t)gg * kNb * a.mcap + 1 + tid];
+        dots[tid] = tj * s;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < (nb - jj - 1) * nr; idx += kThreads) {
+        const int cc = jj + 1 + idx / nr, i = idx % nr, r = r0 + i;
+        if (r > j) P[cc * a.RB + i] = fma(-dots[cc], P[jj * a.RB + i], P[cc * a.RB + i]);
+        else if (r == j) P[cc * a.RB + i] -= dots[cc];
+      }
+      __syncthreads();
+    }
+    // write the factored panel back (R entries and reflectors), build Y
+    for (int idx = tid; idx < nb * nr; idx += kThreads) {
+      const int cc = idx / nr, i = idx % nr, r = r0 + i, j = j0 + cc;
+      a.Tw[(size_t)j * n + r] = P[cc * a.RB + i];
+      Y[cc * a.RB + i] = (r > j) ? P[cc * a.RB + i] : (r == j ? 1.0 : 0.0);
+    }
+    for (int idx = tid; idx < kNb * a.RB; idx += kThreads)
+      if (idx / a.RB >= nb) Y[idx] = 0.0;
+    __syncthreads();
+    const int c0 = j0 + nb;                     // trailing T^H columns c0..m-1
+    if (c0 < m) {
+      // partial W[k][c] = sum_r Y[r][k] C[r][c] (my rows) and partial Y^T Y
+      for (int c = c0 + warp; c < m; c += kWarps) {
+        double acc[kNb];
+#pragma unroll
+        for (int kk = 0; kk < kNb; ++kk) acc[kk] = 0.0;
+        for (int i = lane; i < nr; i += 32) {
+          const double x = a.Tw[(size_t)c * n + r0 + i];
+#pragma unroll
+          for (int kk = 0; kk < kNb; ++kk) acc[kk] = fma(Y[kk * a.RB + i], x, acc[kk]);
+        }
+#pragma unroll
+        for (int kk = 0; kk < kNb; ++kk) {
+          const double t = warp_sum(acc[kk]);
+          if (lane == 0) a.part[(size_t)g * kNb * a.mcap + (size_t)kk * a.mcap + c] = t;
+        }
+      }
+      double *gpart = a.part + (size_t)G * kNb * a.mcap;    // [G][kNb*kNb]
+      for (int e = warp; e < kNb * kNb; e += kWarps) {
+        const int k1 = e / kNb, k2 = e % kNb;
+        double s = 0.0;
+        for (int i = lane; i < nr; i += 32) s = fma(Y[k1 * a.RB + i], Y[k2 * a.RB + i], s);
+        s = warp_sum(s);
+        if (lane == 0) gpart[(size_t)g * kNb * kNb + e] = s;
+      }
+      grid_sync(a.bar, G, 3);
+      // distributed reduction: CTA g sums columns c = c0 + g, c0 + g + G, ...
+      for (int idx = tid; idx < kNb * ((m - c0 + (int)G - 1 - g) / (int)G); idx += kThreads) {
+        const int kk = idx % kNb, t = idx / kNb, c = c0 + g + t * (int)G;
+        if (c >= m) continue;
+        double s = 0.0;
+        for (unsigned gg = 0; gg < G; ++gg) s += a.part[(size_t)gg * kNb * a.mcap + (size_t)kk * a.mcap + c];
+        a.wtot[(size_t)kk * a.mcap + c] = s;
+      }
+      if (g == 0)
+        for (int e = tid; e < kNb * kNb; e += kThreads) {
+          double s = 0.0;
+          for (unsigned gg = 0; gg < G; ++gg) s += gpart[(size_t)gg * kNb * kNb + e];
+          a.gram[e] = s;
+        }
+      grid_sync(a.bar, G, 4);
+      // T_wy (upper triangular): T_jj = tau_j, T[0:j, j] = -tau_j * T[0:j,0:j] * (Y^T y_j)[0:j]
+      if (tid == 0) {
+        for (int e = 0; e < kNb * kNb; ++e) tw[e] = 0.0;
+        for (int j = 0; j < nb; ++j) {
+          tw[j * kNb + j] = tau[j];
+          for (int i = 0; i < j; ++i) {
+            double s = 0.0;
+            for (int l = i; l < j; ++l) s += tw[i * kNb + l] * a.gram[l * kNb + j];
+            tw[i * kNb + j] = -tau[j] * s;
+          }
+        }
+      }
+      __syncthreads();
+      // C -= Y (T^T W): process trailing columns in chunks of 64
+      for (int cb = c0; cb < m; cb += 64) {
+        const int ncb = min(64, m - cb);
+        for (int idx = tid; idx < kNb * ncb; idx += kThreads) {   // Mt[k][c] = sum_l T[l][k] W[l][c]
+          const int kk = idx / ncb, c = idx % ncb;
+          double s = 0.0;
+          for (int l = 0; l <= kk; ++l) s = fma(tw[l * kNb + kk], a.wtot[(size_t)l * a.mcap + cb + c], s);
+          Mt[kk * 64 + c] = s;
+        }
+        __syncthreads();
+        for (int c = warp; c < ncb; c += kWarps) {
+          double *col = a.Tw + (size_t)(cb + c) * n + r0;
+          for (int i = lane; i < nr; i += 32) {
+            double s = col[i];
+#pragma unroll
+            for (int kk = 0; kk < kNb; ++kk) s = fma(-Y[kk * a.RB + i], Mt[kk * 64 + c], s);
+            col[i] = s;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    grid_sync(a.bar, G, 5);
+  }
+  // R (m x m, row-major, lower part zero) from rows 0..m-1 of the factored T^H
+  for (long long idx = (long long)g * kThreads + tid; idx < (long long)m * m; idx += (long long)G * kThreads) {
+    const int j = (int)(idx / m), c = (int)(idx % m);
+    a.Rout[idx] = (c >= j) ? a.Tw[(size_t)c * n + j] : 0.0;
+  }
+}
+
+// ------------------------------------------------------------------ a4: cooperative Jacobi
+
+struct JacArgs {
+  const SiteDims *dims;
+  double *A;               // m x p column-major, ld m
+  GridBar *bar;
+  int *flags;              // [3] rotating 'rotated in sweep s' flags
+  int G, WB;               // CTAs, block width (columns)
+  int *sweeps_out;
+  int *status;
+};
+
+__device__ __forceinline__ void rot_pair(double *ci, double *cj, int m, double tol, int &rot) {
+  const int lane = threadIdx.x & 31;
+  double al = 0.0, be = 0.0, ga = 0.0;
+  for (int r = lane; r < m; r += 32) {
+    const double x = ci[r], y = cj[r];
+    al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
+  }
+  al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+  if (ga != 0.0 && al > 0.0 && be > 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+    const double d = be - al, g2 = ga + ga;
+    const double t = copysign(1.0, d) * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
+    const double c = 1.0 / sqrt(fma(t, t, 1.0)), s = c * t;
+    for (int r = lane; r < m; r += 32) {
+      const double x = ci[r], y = cj[r];
+      ci[r] = fma(c, x, -s * y);
+      cj[r] = fma(s, x, c * y);
+    }
+    rot = 1;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
+  extern __shared__ double smj[];
+  const SiteDims D = *a.dims;
+  const int m = D.m, p = D.p, WB = a.WB, g = blockIdx.x, tid = threadIdx.x, warp = tid >> 5;
+  const int NB = 2 * ((p + 2 * WB - 1) / (2 * WB));     // even number of blocks
+  const double tol = (double)max(m, 1) * DBL_EPSILON;
+  double *S = smj;                                      // [2*WB][m]
+  __shared__ int s_rot;
+  int sweep = 0;
+  for (; sweep < 60; ++sweep) {
+    // 3 rotating flags: slot s%3 collects "rotated in sweep s".  Slot (s+1)%3 was last read at
+    // the end of sweep s-2 and every CTA has passed the barriers of sweep s-1 since, so it is
+    // cleared here (for sweep s+1) without racing a reader.
+    if (g == 0 && tid == 0) a.flags[(sweep + 1) % 3] = 0;
+    int rot = 0;
+    for (int r = 0; r < NB - 1; ++r) {
+      for (int t = g; t < NB / 2; t += a.G) {
+        const int I = (t == 0) ? 0 : 1 + (t - 1 + r) % (NB - 1);
+        const int J = 1 + (NB - 2 - t + r) % (NB - 1);
+        // load the two blocks (zero columns beyond p)
+        for (int idx = tid; idx < 2 * WB * m; idx += kThreads) {
+          const int c = idx / m, row = idx % m;
+          const int col = (c < WB) ? I * WB + c : J * WB + (c - WB);
+          S[idx] = (col < p) ? a.A[(size_t)col * m + row] : 0.0;
+        }
+        __syncthreads();
+        if (r == 0 && WB > 1) {           // intra-block pairs (circle method on WB players)
+          for (int u = 0; u < WB - 1; ++u) {
+            for (int pr = warp; pr < WB; pr += kWarps) {
+              const int h = WB / 2, tt = pr % h, base = (pr < h) ? 0 : WB;
+              const int k1 = tt, k2 = WB - 1 - tt;
+              const int i = base + ((k1 == 0) ? 0 : 1 + (k1 - 1 + u) % (WB - 1));
+              const int j = base + ((k2 == 0) ? 0 : 1 + (k2 - 1 + u) % (WB - 1));
+              rot_pair(S + (size_t)i * m, S + (size_t)j * m, m, tol, rot);
+            }
+            __syncthreads();
+          }
+        }
+        for (int sft = 0; sft < WB; ++sft) {     // cross pairs (a, WB + (a+sft)%WB)
+          for (int pr = warp; pr < WB; pr += kWarps)
+            rot_pair(S + (size_t)pr * m, S + (size_t)(WB + (pr + sft) % WB) * m, m, tol, rot);
+          __syncthreads();
+        }
+        for (int idx = tid; idx < 2 * WB * m; idx += kThreads) {
+          const int c = idx / m, row = idx % m;
+          const int col = (c < WB) ? I * WB + c : J * WB + (c - WB);
+          if (col < p) a.A[(size_t)col * m + row] = S[idx];
+        }
+        __syncthreads();
+      }
+      grid_sync(a.bar, a.G, 11);
+    }
+    if (tid == 0) s_rot = 0;
+    __syncthreads();
+    if (rot) s_rot = 1;
+    __syncthreads();
+    if (tid == 0 && s_rot) atomicOr(a.flags + (sweep % 3), 1);
+    grid_sync(a.bar, a.G, 12);
+    const int any = *((volatile int *)(a.flags + (sweep % 3)));
+    if (!any) { ++sweep; break; }
+  }
+  if (g == 0 && tid == 0) {
+    *a.sweeps_out = sweep;
+    if (sweep >= 60) atomicOr(a.status, ST_NOCONV);
+  }
+}
+
+// ------------------------------------------------------------------ a5/a6: finish
+
+struct FinishArgs {
+  SiteDims *dims;
+  const double *A;        // m x p column-major
+  double *Cq;             // output core slot: (chi, d, k) = m x k row-major
+  int *yr_next;           // out_ranks[b][q+1]
+  double *delta2;         // &delta2[b*L+q]
+  double *sigma;          // &sigma[(b*(L-1)+q)*stride] or NULL
+  int sigma_stride;
+  double *s2;             // scratch [pcap]
+  int *perm;              // scratch [pcap]
+  double eps;
+  int max_rank;
+  int *status;
+  GemmSpec *carry;        // spec[2]: G' = Cq^T T
+  const double *T;
+  double *Gout;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) k_finish(FinishArgs a) {
+  __shared__ double sc[4];
+  SiteDims D = *a.dims;
+  const int m = D.m, p = D.p, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int j = warp; j < p; j += kWarps) {
+    double s = 0.0;
+    for (int r = lane; r < m; r += 32) { const double v = a.A[(size_t)j * m + r]; s = fma(v, v, s); }
+    s = warp_sum(s);
+    if (lane == 0) {
+      if (!isfinite(s)) { atomicOr(a.status, ST_NONFINITE); s = 0.0; }
+      a.s2[j] = s;
+    }
+  }
+  __syncthreads();
+  for (int j = tid; j < p; j += kThreads) {
+    const double sj = a.s2[j];
+    int rank = 0;
+    for (int l = 0; l < p; ++l) rank += (a.s2[l] > sj) || (a.s2[l] == sj && l < j);
+    a.perm[rank] = j;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double acc = 0.0, tot = 0.0;
+    for (int jj = p - 1; jj >= 0; --jj) tot += a.s2[a.perm[jj]];
+    const double tau = a.eps * a.eps * tot;
+    int k = p;
+    for (int kk = p - 1; kk >= 1; --kk) {       // tail[kk] = sum_{j>=kk} s_j^2 (smallest first)
+      acc += a.s2[a.perm[kk]];
+      if (acc <= tau) k = kk; else break;
+    }
+    // recompute tail[k] in the same order as the oracle
+    double tail = 0.0;
+    for (int jj = p - 1; jj >= k; --jj) tail += a.s2[a.perm[jj]];
+    if (a.max_rank > 0 && k > a.max_rank) {
+      k = a.max_rank;
+      tail = 0.0;
+      for (int jj = p - 1; jj >= k; --jj) tail += a.s2[a.perm[jj]];
+    }
+    if (tot == 0.0) { k = 1; tail = 0.0; }
+    k = max(k, 1);
+    sc[0] = (double)k; sc[1] = tail;
+    *a.yr_next = k;
+    *a.delta2 = tail;
+    a.dims->k = k;
+    GemmSpec gc{};
+    gc.M = k; gc.N = D.n; gc.K = m; gc.nz1 = 1; gc.nz2 = 1;
+    gc.A = a.Cq; gc.sam = 1; gc.sak = k;
+    gc.B = a.T; gc.sbk = D.n; gc.sbn = 1;
+    gc.C = a.Gout; gc.scm = D.n; gc.scn = 1;
+    *a.carry = gc;
+  }
+  __syncthreads();
+  const int k = (int)sc[0];
+  for (long long idx = tid; idx < (long long)m * k; idx += kThreads) {
+    const int row = (int)(idx / k), kk = (int)(idx % k);
+    const int j = a.perm[kk];
+    const double s2 = a.s2[j];
+    a.Cq[idx] = (s2 > 0.0) ? a.A[(size_t)j * m + row] / sqrt(s2) : (row == kk ? 1.0 : 0.0);
+  }
+  if (a.sigma)
+    for (int jj = tid; jj < a.sigma_stride; jj += kThreads) a.sigma[jj] = (jj < p) ? sqrt(a.s2[a.perm[jj]]) : 0.0;
+}
+
+__global__ void k_last(const SiteDims *dims, const double *T, double *Cq, double *norm2, double *delta2, int *yr_L,
+                       int *status) {
+  __shared__ double red[kWarps];
+  const SiteDims D = *dims;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < D.m; i += kThreads) { const double v = T[i]; Cq[i] = v; s = fma(v, v, s); }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) {
+    *norm2 = s; *delta2 = 0.0; *yr_L = 1;
+    if (!isfinite(s)) atomicOr(status, ST_NONFINITE);
+  }
+}
+
+// ------------------------------------------------------------------ mirror (large a1)
+
+struct MirrorL {
+  int L, dm[64];
+  int cap_src[65];
+  const double *src[64];
+  long long src_bs;        // unused (single member)
+  const int *src_ranks;    // device [L+1] or NULL
+  double *dst[64];
+  int pad;
+  int *dst_ranks;
+};
+
+__global__ void k_mirror_l(MirrorL a) {
+  const int qd = blockIdx.x, qs = a.L - 1 - qd;
+  const int rl = a.src_ranks ? a.src_ranks[qs] : a.cap_src[qs];
+  const int rr = a.src_ranks ? a.src_ranks[qs + 1] : a.cap_src[qs + 1];
+  const int d = a.dm[qs];
+  const double *s = a.src[qs];
+  double *t = a.dst[qd];
+  if (a.pad) {
+    const int cl = a.cap_src[qs + 1], cr = a.cap_src[qs];
+    const long long n = (long long)cl * d * cr;
+    for (long long idx = threadIdx.x; idx < n; idx += blockDim.x) {
+      const int aa = (int)(idx % cr);
+      const long long t1 = idx / cr;
+      const int i = (int)(t1 % d), ap = (int)(t1 / d);
+      t[idx] = (ap < rr && aa < rl) ? s[((size_t)aa * d + i) * rr + ap] : 0.0;
+    }
+  } else {
+    const long long n = (long long)rr * d * rl;
+    for (long long idx = threadIdx.x; idx < n; idx += blockDim.x) {
+      const int aa = (int)(idx % rl);
+      const long long t1 = idx / rl;
+      const int i = (int)(t1 % d), ap = (int)(t1 / d);
+      t[idx] = s[((size_t)aa * d + i) * rr + ap];
+    }
+    if (threadIdx.x == 0) {
+      a.dst_ranks[qd + 1] = rl;
+      if (qd == 0) a.dst_ranks[0] = rr;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host: one sweep
+
+struct SweepBufs {
+  double *G, *X, *T, *Tw, *A, *part, *wtot, *gram, *bc, *s2;
+  int *perm, *flags, *sweeps_scratch;
+  GridBar *bar;
+  SiteDims *dims;
+  GemmSpec *spec;
+};
+
+static int g_sms = 0;
+
+static qtt_status_t sweep_caps(int L, const std::vector<int> &d, const std::vector<int> &dj, const std::vector<int> &xr,
+                               const std::vector<int> &orr, const std::vector<int> &cap, int kind, long long &mcap,
+                               long long &ncap, long long &gcap, long long &xcap, long long &tcap, long long &acap,
+                               long long &pcap) {
+  mcap = ncap = gcap = xcap = tcap = acap = pcap = 1;
+  for (int q = 0; q < L; ++q) {
+    const long long m = (long long)cap[q] * d[q];
+    const long long n = (long long)orr[q + 1] * xr[q + 1];
+    mcap = std::max(mcap, m); ncap = std::max(ncap, n);
+    gcap = std::max(gcap, (long long)cap[q] * orr[q] * xr[q]);
+    gcap = std::max(gcap, (long long)cap[q + 1] * n);
+    const long long xe = (kind == MATVEC) ? (long long)cap[q] * orr[q] * dj[q] * xr[q + 1]
+                                          : (kind == HADAMARD ? (long long)cap[q] * orr[q] * d[q] * xr[q + 1] : 1);
+    xcap = std::max(xcap, xe);
+    tcap = std::max(tcap, m * n);
+    acap = std::max(acap, m * std::min(m, n));
+    pcap = std::max(pcap, std::min(m, n));
+  }
+  return QTT_OK;
+}
+
+struct SweepPlan {
+  long long mcap, ncap, gcap, xcap, tcap, acap, pcap;
+  int Gqr, RB, Gjac, WB;
+  size_t qr_smem, jac_smem;
+  size_t off_G, off_X, off_T, off_Tw, off_A, off_part, off_wtot, off_gram, off_bc, off_s2, off_perm, off_flags,
+      off_sw, off_bar, off_dims, off_spec, total;
+};
+
+static qtt_status_t plan_sweep(int L, const std::vector<int> &d, const std::vector<int> &dj, const std::vector<int> &xr,
+                               const std::vector<int> &orr, const std::vector<int> &cap, int kind, SweepPlan &P) {
+  sweep_caps(L, d, dj, xr, orr, cap, kind, P.mcap, P.ncap, P.gcap, P.xcap, P.tcap, P.acap, P.pcap);
+  if (g_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  // QR: rows of T^H per CTA <= kQrRowsMax, >= 32
+  P.Gqr = (int)std::min<long long>(g_sms, std::max<long long>(1, (P.ncap + 31) / 32));
+  P.RB = (int)((P.ncap + P.Gqr - 1) / P.Gqr);
+  P.RB = ((P.RB + 31) / 32) * 32;
+  while (P.RB > kQrRowsMax) { set_error("large path: n = %lld too large", P.ncap); return QTT_EUNSUPPORTED; }
+  P.qr_smem = sizeof(double) * ((size_t)2 * kNb * P.RB + 32 + kNb * kNb + 2 * kNb + kNb * 64);
+  // Jacobi: block width so that 2*WB*m*8 <= 200 KB and #pairs <= #SMs
+  int WB = 1;
+  while (WB < 64 && (P.pcap + 2 * WB - 1) / (2 * WB) > g_sms) WB *= 2;
+  while (WB > 1 && 2 * WB * P.mcap * 8 > 200 * 1024) WB /= 2;
+  if (2 * WB * P.mcap * 8 > 200 * 1024) { set_error("large path: m = %lld too large", P.mcap); return QTT_EUNSUPPORTED; }
+  P.WB = WB;
+  P.Gjac = (int)std::min<long long>(g_sms, std::max<long long>(1, (P.pcap + 2 * WB - 1) / (2 * WB)));
+  P.jac_smem = sizeof(double) * 2 * WB * P.mcap;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+  P.off_G = take(8 * P.gcap);
+  P.off_X = take(8 * P.xcap);
+  P.off_T = take(8 * P.tcap);
+  P.off_Tw = take(8 * P.tcap);
+  P.off_A = take(8 * P.acap);
+  P.off_part = take(8 * ((size_t)P.Gqr * kNb * P.mcap + (size_t)P.Gqr * kNb * kNb + 16));
+  P.off_wtot = take(8 * (size_t)kNb * P.mcap);
+  P.off_gram = take(8 * kNb * kNb);
+  P.off_bc = take(8 * 16);
+  P.off_s2 = take(8 * P.pcap);
+  P.off_perm = take(4 * P.pcap);
+  P.off_flags = take(4 * 4);
+  P.off_sw = take(4 * 4);
+  P.off_bar = take(sizeof(GridBar) * 2);
+  P.off_dims = take(sizeof(SiteDims));
+  P.off_spec = take(sizeof(GemmSpec) * 3);
+  P.total = off;
+  return QTT_OK;
+}
+
+static qtt_status_t coop_launch(const void *fn, int grid, size_t smem, void *args, cudaStream_t s) {
+  void *kargs[] = {args};
+  QTT_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), kargs, smem, s));
+  return QTT_OK;
+}
+
+__global__ void k_site0_init(double *G, int *yr) {
+  if (threadIdx.x == 0) { G[0] = 1.0; yr[0] = 1; }
+}
+
+// One member's sweep a2..a7.  Xq/Oq/Wop per site point at this member's workspace operand
+// copies; xr/orr/yr are this member's device rank rows; orig_xr/orig_or are capacities.
+struct SweepIO {
+  int L, kind;
+  std::vector<int> d, dj, cap, xcap_r, ocap_r;     // digit sizes, output caps, operand rank caps
+  std::vector<const double *> Xq, Oq;              // Oq: Hadamard second state / MPO cores
+  const int *xr, *orr;
+  int *yr;
+  std::vector<double *> Cq;
+  double *delta2, *norm2, *sigma;
+  int sigma_stride;
+  int *sweeps, *status;
+  double eps;
+  int max_rank;
+};
+
+static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, cudaStream_t s) {
+  const int L = io.L, kind = io.kind;
+  SweepBufs Bf;
+  Bf.G = (double *)(ws + P.off_G); Bf.X = (double *)(ws + P.off_X); Bf.T = (double *)(ws + P.off_T);
+  Bf.Tw = (double *)(ws + P.off_Tw); Bf.A = (double *)(ws + P.off_A); Bf.part = (double *)(ws + P.off_part);
+  Bf.wtot = (double *)(ws + P.off_wtot); Bf.gram = (double *)(ws + P.off_gram); Bf.bc = (double *)(ws + P.off_bc);
+  Bf.s2 = (double *)(ws + P.off_s2); Bf.perm = (int *)(ws + P.off_perm); Bf.flags = (int *)(ws + P.off_flags);
+  Bf.sweeps_scratch = (int *)(ws + P.off_sw); Bf.bar = (GridBar *)(ws + P.off_bar);
+  Bf.dims = (SiteDims *)(ws + P.off_dims); Bf.spec = (GemmSpec *)(ws + P.off_spec);
+  static bool attr = false;
+  if (!attr) {
+    QTT_CUDA_TRY(cudaFuncSetAttribute(k_qr_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    QTT_CUDA_TRY(cudaFuncSetAttribute(k_jacobi_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    attr = true;
+  }
+  QTT_CUDA_TRY(cudaMemsetAsync(Bf.bar, 0, sizeof(GridBar) * 2, s));
+  k_site0_init<<<1, 32, 0, s>>>(Bf.G, io.yr);
+  QTT_CUDA_TRY(cudaGetLastError());
+  for (int q = 0; q < L; ++q) {
+    const long long w = (kind == TRUNCATE) ? 1 : io.ocap_r[q], w2 = (kind == TRUNCATE) ? 1 : io.ocap_r[q + 1];
+    const long long m_cap = (long long)io.cap[q] * io.d[q];
+    const long long n_cap = w2 * io.xcap_r[q + 1];
+    PlanArgs pa;
+    pa.q = q; pa.L = L; pa.kind = kind; pa.d = io.d[q]; pa.dj = io.dj[q];
+    pa.xr = io.xr; pa.orr = io.orr; pa.yr = io.yr;
+    pa.Xq = io.Xq[q]; pa.Oq = (kind == TRUNCATE) ? nullptr : io.Oq[q];
+    pa.G = Bf.G; pa.X = Bf.X; pa.T = Bf.T; pa.Cq = io.Cq[q];
+    pa.dims = Bf.dims; pa.spec = Bf.spec;
+    k_plan<<<1, 32, 0, s>>>(pa);
+    QTT_CUDA_TRY(cudaGetLastError());
+    // a2: state GEMM (M <= cap*w, N <= (dj|d)*r2)
+    const long long g0M = (long long)io.cap[q] * w;
+    const long long g0N = (long long)((kind == MATVEC) ? io.dj[q] : io.d[q]) * io.xcap_r[q + 1];
+    launch_gemm_spec(Bf.spec + 0, g0M, g0N, 1, 1, s);
+    QTT_CUDA_TRY(cudaGetLastError());
+    const unsigned ew_grid = (unsigned)std::min<long long>((m_cap * n_cap + kThreads - 1) / kThreads, 8192);
+    if (kind == MATVEC) {
+      k_mpo_apply<<<ew_grid, kThreads, 0, s>>>(Bf.dims, Bf.X, io.Oq[q], Bf.T);
+      QTT_CUDA_TRY(cudaGetLastError());
+    } else if (kind == HADAMARD) {
+      launch_gemm_spec(Bf.spec + 1, w2, io.xcap_r[q + 1], io.cap[q], io.d[q], s);
+      QTT_CUDA_TRY(cudaGetLastError());
+    }
+    if (q == L - 1) {                                                  // a7
+      k_last<<<1, kThreads, 0, s>>>(Bf.dims, Bf.T, io.Cq[q], io.norm2, io.delta2 + q, io.yr + L, io.status);
+      QTT_CUDA_TRY(cudaGetLastError());
+      if (io.sweeps) QTT_CUDA_TRY(cudaMemsetAsync(io.sweeps + q, 0, sizeof(int), s));
+      break;
+    }
+    // a3
+    k_copy_T<<<ew_grid, kThreads, 0, s>>>(Bf.dims, Bf.T, Bf.Tw, Bf.A);
+    QTT_CUDA_TRY(cudaGetLastError());
+    {
+      QrArgs qa;
+      qa.dims = Bf.dims; qa.Tw = Bf.Tw; qa.Rout = Bf.A; qa.part = Bf.part; qa.wtot = Bf.wtot; qa.gram = Bf.gram;
+      qa.bc = Bf.bc; qa.bar = Bf.bar; qa.G = P.Gqr; qa.RB = P.RB; qa.mcap = (int)P.mcap;
+      qtt_status_t st = coop_launch((const void *)k_qr_coop, P.Gqr, P.qr_smem, &qa, s);
+      if (st != QTT_OK) return st;
+    }
+    // a4
+    {
+      JacArgs ja;
+      ja.dims = Bf.dims; ja.A = Bf.A; ja.bar = Bf.bar + 1; ja.flags = Bf.flags; ja.G = P.Gjac; ja.WB = P.WB;
+      ja.sweeps_out = io.sweeps ? io.sweeps + q : Bf.sweeps_scratch; ja.status = io.status;
+      QTT_CUDA_TRY(cudaMemsetAsync(Bf.flags, 0, sizeof(int) * 3, s));
+      qtt_status_t st = coop_launch((const void *)k_jacobi_coop, P.Gjac, P.jac_smem, &ja, s);
+      if (st != QTT_OK) return st;
+    }
+    // a5/a6
+    {
+      FinishArgs fa;
+      fa.dims = Bf.dims; fa.A = Bf.A; fa.Cq = io.Cq[q]; fa.yr_next = io.yr + q + 1; fa.delta2 = io.delta2 + q;
+      fa.sigma = io.sigma ? io.sigma + (size_t)q * io.sigma_stride : nullptr; fa.sigma_stride = io.sigma_stride;
+      fa.s2 = Bf.s2; fa.perm = Bf.perm; fa.eps = io.eps; fa.max_rank = io.max_rank; fa.status = io.status;
+      fa.carry = Bf.spec + 2; fa.T = Bf.T; fa.Gout = Bf.G;
+      k_finish<<<1, kThreads, 0, s>>>(fa);
+      QTT_CUDA_TRY(cudaGetLastError());
+    }
+    launch_gemm_spec(Bf.spec + 2, io.cap[q + 1], n_cap, 1, 1, s);
+    QTT_CUDA_TRY(cudaGetLastError());
+  }
+  return QTT_OK;
+}
+
+__global__ void k_copy_member(const double *src, double *dst, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+__global__ void k_fill_ranks(int *r, const int *vals, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) r[i] = vals[i];
+}
+
+// ------------------------------------------------------------------ host entry
+
+struct OperandPre {       // mirrored-truncate a1 plan for one operand
+  int active;
+  int L;
+  std::vector<int> legs, ranks;          // original (site order)
+  std::vector<int> lm, rm, capm;         // mirrored legs, mirrored ranks, truncate-sweep output caps
+  std::vector<long long> mel, zel;
+  SweepPlan plan;
+  size_t off_M, off_Z, off_zr, off_zd, off_zn, off_ws, total;
+};
+
+static qtt_status_t plan_operand(int L, const std::vector<int> &legs, const std::vector<int> &ranks, OperandPre &O) {
+  O.active = 1; O.L = L; O.legs = legs; O.ranks = ranks;
+  O.lm.resize(L); O.rm.resize(L + 1); O.capm.assign(L + 1, 1);
+  for (int q = 0; q < L; ++q) O.lm[q] = legs[L - 1 - q];
+  for (int q = 0; q <= L; ++q) O.rm[q] = ranks[L - q];
+  for (int q = 0; q < L; ++q) {
+    long long c = (long long)O.capm[q] * O.lm[q];
+    c = std::min<long long>(c, O.rm[q + 1]);
+    O.capm[q + 1] = (q == L - 1) ? 1 : (int)c;
+  }
+  std::vector<int> ones(L + 1, 1);
+  qtt_status_t st = plan_sweep(L, O.lm, O.lm, O.rm, ones, O.capm, TRUNCATE, O.plan);
+  if (st != QTT_OK) return st;
+  O.mel.resize(L); O.zel.resize(L);
+  size_t me = 0, ze = 0;
+  for (int q = 0; q < L; ++q) {
+    O.mel[q] = (long long)O.rm[q] * O.lm[q] * O.rm[q + 1];
+    O.zel[q] = (long long)O.capm[q] * O.lm[q] * O.capm[q + 1];
+    me += O.mel[q]; ze += O.zel[q];
+  }
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+  O.off_M = take(8 * me); O.off_Z = take(8 * ze); O.off_zr = take(4 * (L + 1)); O.off_zd = take(8 * (L + 1));
+  O.off_zn = take(8); O.off_ws = take(O.plan.total);
+  O.total = off;
+  return QTT_OK;
+}
+
+struct RankRow {
+  int v[65];
+};
+__global__ void k_set_ranks(int *dst, RankRow row, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = row.v[i];
+}
+
+// Right-orthonormalise one member's operand in place (slot base + off[q], packed at its
+// capacity ranks O.ranks) by the mirrored truncate sweep; writes its device rank row.
+static qtt_status_t orth_operand(const OperandPre &O, double *base, const std::vector<long long> &off, int *rank_row,
+                                 int *status, char *ws, cudaStream_t s) {
+  const int L = O.L;
+  double *M = (double *)(ws + O.off_M), *Z = (double *)(ws + O.off_Z);
+  int *zr = (int *)(ws + O.off_zr);
+  double *zd = (double *)(ws + O.off_zd), *zn = (double *)(ws + O.off_zn);
+  std::vector<double *> Mp(L), Zp(L);
+  size_t om = 0, oz = 0;
+  for (int q = 0; q < L; ++q) { Mp[q] = M + om; om += O.mel[q]; Zp[q] = Z + oz; oz += O.zel[q]; }
+  MirrorL a;
+  memset(&a, 0, sizeof(a));
+  a.L = L; a.pad = 1; a.src_ranks = nullptr;
+  for (int q = 0; q < L; ++q) { a.dm[q] = O.legs[q]; a.src[q] = base + off[q]; a.dst[q] = Mp[q]; }
+  for (int q = 0; q <= L; ++q) a.cap_src[q] = O.ranks[q];
+  k_mirror_l<<<L, kThreads, 0, s>>>(a);
+  QTT_CUDA_TRY(cudaGetLastError());
+  // the mirrored input is packed at its capacity ranks: constant rank row in the rank_row slot
+  RankRow rr;
+  for (int q = 0; q <= L; ++q) rr.v[q] = O.rm[q];
+  k_set_ranks<<<1, 64, 0, s>>>(rank_row, rr, L + 1);
+  QTT_CUDA_TRY(cudaGetLastError());
+  SweepIO io;
+  io.L = L; io.kind = TRUNCATE; io.d = O.lm; io.dj = O.lm; io.cap = O.capm; io.xcap_r = O.rm;
+  io.ocap_r.assign(L + 1, 1);
+  io.Xq.assign(Mp.begin(), Mp.end());
+  io.Oq.assign(L, nullptr);
+  io.xr = rank_row; io.orr = nullptr; io.yr = zr;
+  io.Cq.assign(Zp.begin(), Zp.end());
+  io.delta2 = zd; io.norm2 = zn; io.sigma = nullptr; io.sigma_stride = 1; io.sweeps = nullptr; io.status = status;
+  io.eps = 0.0; io.max_rank = 0;
+  qtt_status_t st = run_sweep(io, O.plan, ws + O.off_ws, s);
+  if (st != QTT_OK) return st;
+  // mirror back (packed at the sweep's ranks) into the operand slot, ranks -> rank_row
+  MirrorL b;
+  memset(&b, 0, sizeof(b));
+  b.L = L; b.pad = 0; b.src_ranks = zr; b.dst_ranks = rank_row;
+  for (int q = 0; q < L; ++q) { b.dm[q] = O.lm[q]; b.src[q] = Zp[q]; b.dst[q] = base + off[q]; }
+  for (int q = 0; q <= L; ++q) b.cap_src[q] = O.capm[q];
+  k_mirror_l<<<L, kThreads, 0, s>>>(b);
+  QTT_CUDA_TRY(cudaGetLastError());
+  return QTT_OK;
+}
+
+struct LargeLayout {
+  OperandPre px, po;
+  SweepPlan main;
+  size_t off_xo, off_xr, off_or, off_oo, off_scratch, total;
+};
+
+static qtt_status_t large_layout(const Shape &S, uint32_t flags, LargeLayout &Ly) {
+  const int L = S.L;
+  std::vector<int> xlegs(L), olegs(L);
+  for (int q = 0; q < L; ++q) {
+    xlegs[q] = S.dj[q];
+    olegs[q] = (S.kind == MATVEC) ? S.d[q] * S.dj[q] : S.d[q];
+  }
+  qtt_status_t st = plan_operand(L, xlegs, S.xr, Ly.px);
+  if (st != QTT_OK) return st;
+  Ly.po.active = 0; Ly.po.total = 0;
+  if (S.kind != TRUNCATE && !(flags & QTT_NO_OPERATOR_ORTH)) {
+    st = plan_operand(L, olegs, S.orr, Ly.po);
+    if (st != QTT_OK) return st;
+  }
+  st = plan_sweep(L, S.d, S.dj, S.xr, S.orr, S.cap, S.kind, Ly.main);
+  if (st != QTT_OK) return st;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+  Ly.off_xo = take(8 * (size_t)S.xo_elems * S.B);
+  Ly.off_oo = take(8 * (size_t)S.oo_elems * (S.shared_op ? 1 : S.B));
+  Ly.off_xr = take(4 * (size_t)(S.L + 1) * S.B);
+  Ly.off_or = take(4 * (size_t)(S.L + 1) * S.B);
+  Ly.off_scratch = take(std::max(std::max(Ly.px.total, Ly.po.total), Ly.main.total));
+  Ly.total = off;
+  return QTT_OK;
+}
+
+size_t large_workspace_bytes(const Shape &S) {
+  LargeLayout Ly;
+  if (large_layout(S, 0, Ly) != QTT_OK) return 0;
+  return Ly.total;
+}
+
+qtt_status_t large_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags,
+                         const LargeIO &io, void *workspace, size_t workspace_bytes, cudaStream_t s) {
+  LargeLayout Ly;
+  qtt_status_t st = large_layout(S, flags, Ly);
+  if (st != QTT_OK) return st;
+  if (workspace_bytes < Ly.total) { set_error("workspace %zu bytes < required %zu", workspace_bytes, Ly.total); return QTT_ECAPACITY; }
+  char *ws = (char *)workspace;
+  double *Xo = (double *)(ws + Ly.off_xo), *Oo = (double *)(ws + Ly.off_oo);
+  int *xr = (int *)(ws + Ly.off_xr), *orr = (int *)(ws + Ly.off_or);
+  char *scratch = ws + Ly.off_scratch;
+  const int L = S.L, B = S.B;
+  const int nop = (S.kind == TRUNCATE) ? 0 : (S.shared_op ? 1 : B);
+  // copy operands into the workspace slots and set the capacity rank rows
+  for (int q = 0; q < L; ++q) {
+    const long long nx = (long long)S.xr[q] * S.dj[q] * S.xr[q + 1];
+    for (int b = 0; b < B; ++b) {
+      k_copy_member<<<(unsigned)std::min<long long>((nx + 255) / 256, 4096), 256, 0, s>>>(
+          (const double *)x->cores[q] + (size_t)b * nx, Xo + (size_t)b * S.xo_elems + S.xoff[q], nx);
+    }
+    if (nop) {
+      const long long no = S.ooff[q + 1] - S.ooff[q];
+      for (int b = 0; b < nop; ++b)
+        k_copy_member<<<(unsigned)std::min<long long>((no + 255) / 256, 4096), 256, 0, s>>>(
+            (const double *)op->cores[q] + (size_t)b * no, Oo + (size_t)b * S.oo_elems + S.ooff[q], no);
+    }
+  }
+  QTT_CUDA_TRY(cudaGetLastError());
+  {
+    RankRow rx, ro;
+    for (int q = 0; q <= L; ++q) { rx.v[q] = S.xr[q]; ro.v[q] = S.orr[q]; }
+    for (int b = 0; b < B; ++b) {
+      k_set_ranks<<<1, 64, 0, s>>>(xr + (size_t)b * (L + 1), rx, L + 1);
+      k_set_ranks<<<1, 64, 0, s>>>(orr + (size_t)b * (L + 1), ro, L + 1);
+    }
+    QTT_CUDA_TRY(cudaGetLastError());
+  }
+  // a1: right-orthonormalise (mirrored truncate sweeps)
+  for (int b = 0; b < B; ++b) {
+    st = orth_operand(Ly.px, Xo + (size_t)b * S.xo_elems, S.xoff, xr + (size_t)b * (L + 1), io.status, scratch, s);
+    if (st != QTT_OK) return st;
+  }
+  if (Ly.po.active) {
+    for (int b = 0; b < nop; ++b) {
+      st = orth_operand(Ly.po, Oo + (size_t)b * S.oo_elems, S.ooff, orr + (size_t)b * (L + 1), io.status, scratch, s);
+      if (st != QTT_OK) return st;
+    }
+    if (S.shared_op)
+      for (int b = 1; b < B; ++b)
+        QTT_CUDA_TRY(cudaMemcpyAsync(orr + (size_t)b * (L + 1), orr, sizeof(int) * (L + 1), cudaMemcpyDeviceToDevice, s));
+  }
+  // a2..a7 per member
+  for (int b = 0; b < B; ++b) {
+    SweepIO sw;
+    sw.L = L; sw.kind = S.kind; sw.d = S.d; sw.dj = S.dj; sw.cap = S.cap; sw.xcap_r = S.xr; sw.ocap_r = S.orr;
+    sw.Xq.resize(L); sw.Oq.resize(L); sw.Cq.resize(L);
+    for (int q = 0; q < L; ++q) {
+      sw.Xq[q] = Xo + (size_t)b * S.xo_elems + S.xoff[q];
+      sw.Oq[q] = nop ? Oo + (size_t)(S.shared_op ? 0 : b) * S.oo_elems + S.ooff[q] : nullptr;
+      sw.Cq[q] = (double *)io.out->cores[q] + (size_t)b * ((long long)io.out->ranks[q] * S.d[q] * io.out->ranks[q + 1]);
+    }
+    sw.xr = xr + (size_t)b * (L + 1);
+    sw.orr = orr + (size_t)b * (L + 1);
+    sw.yr = io.out_ranks + (size_t)b * (L + 1);
+    sw.delta2 = io.delta2 + (size_t)b * L;
+    sw.norm2 = io.norm2 + b;
+    sw.sigma = io.sigma ? io.sigma + (size_t)b * (L - 1) * io.sigma_stride : nullptr;
+    sw.sigma_stride = io.sigma_stride;
+    sw.sweeps = io.sweeps ? io.sweeps + (size_t)b * L : nullptr;
+    sw.status = io.status; sw.eps = io.eps; sw.max_rank = io.max_rank;
+    st = run_sweep(sw, Ly.main, scratch, s);
+    if (st != QTT_OK) return st;
+  }
+  return QTT_OK;
+}
+
+}  // namespace qtt
+

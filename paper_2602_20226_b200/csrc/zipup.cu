@@ -16,6 +16,7 @@
 
 #include "common.cuh"
 #include "jacobi.cuh"
+#include "large.cuh"
 
 namespace qtt {
 
@@ -33,7 +34,6 @@ qtt_status_t cuda_status(cudaError_t e, const char *what) {
   return QTT_ECUDA;
 }
 
-enum Kind { MATVEC = 0, HADAMARD = 1, TRUNCATE = 2 };
 
 constexpr int kMaxSites = 64;
 constexpr int kSmall = 128;            // max rows m (and p) of a site matrix on this path
@@ -43,7 +43,6 @@ constexpr int kSiteSmemDoubles = kRpDoubles + kSmall * kLdA + kSmall + 8 + 8 + k
 constexpr size_t kSiteSmemBytes = kSiteSmemDoubles * sizeof(double) + (kSmall + 8) * sizeof(int);
 constexpr int kOrthSmemDoubles = 26000;  // a1 staging budget (~203 KB)
 
-enum StatusBits { ST_NONFINITE = 1, ST_NOCONV = 2 };
 
 // ======================================================================= a1: pre-pass
 
@@ -527,9 +526,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(SweepArgs a) {
     const int q = task / a.B, b = task % a.B;
     if (threadIdx.x == 0 && q > 0) {
       int v;
+      long long spins = 0;
       do {
         asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(a.done + b) : "memory");
         if (v < q) __nanosleep(64);
+        if (++spins > (1LL << 28)) __trap();   // predecessor never finished: fail loudly
       } while (v < q);
       __threadfence();          // also invalidates this SM's L1: no stale carry / scratch lines
     }
@@ -544,13 +545,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(SweepArgs a) {
 }
 
 // ======================================================================= host side
-
-struct Shape {
-  int L = 0, B = 0, kind = 0, shared_op = 0;
-  std::vector<int> d, dj, xr, orr, cap;
-  std::vector<long long> xoff, ooff;
-  long long xo_elems = 0, oo_elems = 0, g_elems = 1, t_elems = 1, x_elems = 1;
-};
 
 static int parse_kind(const char *s, const qtt_trains_t *op) {
   if (s == nullptr || strcmp(s, "i->i") == 0) return op ? -1 : TRUNCATE;
@@ -715,10 +709,14 @@ qtt_status_t qtt_zipup_capacity(const char *subscripts, const qtt_trains_t *op, 
 
 size_t qtt_zipup_workspace_bytes(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
                                  const qtt_trains_t *out) {
-  (void)out;
+  // the output capacities the caller will pass bound the zip-up ranks (max_rank)
+  int mr = 0;
+  if (out && out->ranks && x)
+    for (int q = 1; q < x->n_sites; ++q) mr = std::max(mr, (int)out->ranks[q]);
   Shape S;
-  if (analyse(subscripts, op, x, 0, S) != QTT_OK) return 0;
-  return layout(S).total;
+  if (analyse(subscripts, op, x, mr, S) != QTT_OK) return 0;
+  if (check_small_path(S) == QTT_OK) return layout(S).total;
+  return large_workspace_bytes(S);
 }
 
 qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x, double eps,
@@ -753,14 +751,25 @@ qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt
     if (out->d_out[q] != S.d[q]) { set_error("output digit size mismatch at core %d", q); return QTT_ESHAPE; }
   }
   if (sigma && sigma_stride < 1) { set_error("sigma_stride < 1"); return QTT_EINVAL; }
-  st = check_small_path(S);
-  if (st != QTT_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (check_small_path(S) != QTT_OK) {
+    // large-member path (site matrices with more than 128 rows): one member at a time
+    g_err[0] = 0;
+    QTT_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), s));
+    if (events) QTT_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[0], s));
+    if (events) QTT_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[1], s));
+    if (events) QTT_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[2], s));
+    LargeIO io{out, out_ranks, delta2, norm2, sigma, sigma_stride, sweeps, status, eps, max_rank};
+    qtt_status_t lst = large_zipup(S, op, x, flags, io, workspace, workspace_bytes, s);
+    if (lst != QTT_OK) return lst;
+    if (events) QTT_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[3], s));
+    return QTT_OK;
+  }
   const WsLayout W = layout(S);
   if (workspace_bytes < W.total || !workspace) {
     set_error("workspace %zu bytes < required %zu", workspace_bytes, W.total);
     return QTT_ECAPACITY;
   }
-  cudaStream_t s = (cudaStream_t)stream;
   char *ws = (char *)workspace;
   double *Xo = (double *)(ws + W.xo), *Oo = (double *)(ws + W.oo), *G = (double *)(ws + W.g);
   double *T = (double *)(ws + W.t), *Xb = (double *)(ws + W.x);
