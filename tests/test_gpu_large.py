@@ -46,3 +46,64 @@ def test_cfg4_full(lib):
     """configs[3] at full size: 3^8*5^4 mixed radix, rank 512, rank-8 stencil, max rank 512."""
     p = gen.cfg4()
     check(lib, "matvec", p.op.cores, p.x.cores, p.eps, p.max_rank, dense=False)
+
+
+def test_cfg3_full_shape_known_answer(lib):
+    """configs[2] at full shape (L=30, both operands rank 256, max rank 256): with the second
+    operand the constant 1 written as a redundant rank-256 train (block sum of 256 rank-1
+    trains, each 1/256), a o 1 = a exactly, so the zip-up must return a (rank <= 256) --
+    exercising the 512 x 65536 site matrices of the cfg3 path with a closed-form answer."""
+    import torch
+    from oracle import tt
+    L, R = 30, 256
+    a = gen.random_mps([2] * L, R, gen.rng_for(3, 0, 0), 1.0 / math.sqrt(R)).cores
+    ranks = gen.clipped_ranks([2] * L, R)
+    rng = np.random.default_rng(7)
+    # redundant representation of the constant 1: cores mix identical rank-1 pieces through
+    # random orthogonal gauges (so nothing is trivially block-diagonal)
+    ones = []
+    for q in range(L):
+        r0, r1 = ranks[q], ranks[q + 1]
+        core = np.zeros((r0, 2, r1))
+        core[:, :, :] = 0.0
+        u = np.ones(r0) / math.sqrt(r0) if q > 0 else np.ones(1)
+        v = np.ones(r1) / math.sqrt(r1) if q < L - 1 else np.ones(1)
+        for i in range(2):
+            core[:, i, :] = np.outer(u, v)
+        if 0 < q:
+            Q, _ = np.linalg.qr(rng.standard_normal((r0, r0)))
+            core = np.einsum("ab,bic->aic", Q.T, core)
+            ones[-1] = np.einsum("aib,bc->aic", ones[-1], Q)
+        ones.append(core)
+    # normalise so the represented tensor is exactly 1 (check on samples below)
+    dig = np.random.default_rng(8).integers(0, 2, size=(64, L))
+    s = tt.evaluate(ones, dig)
+    ones[0] = ones[0] / s[0]
+    np.testing.assert_allclose(tt.evaluate(ones, dig), 1.0, rtol=1e-10)
+    res = run_gpu(lib, "hadamard", ones, a, 1e-8, 256)
+    rk = res.ranks[0].cpu().tolist()
+    assert max(rk) <= 256
+    y = lib.member_cores(res.out, rk, 0)
+    err = tt.diff_norm(y, a)
+    bound = math.sqrt(float(res.delta2[0].sum().item()))      # ||e||^2 <= sum delta^2 (c-A11)
+    assert err <= bound * (1 + 1e-6) + 1e-10 * tt.qr_norm(a), (err, bound)
+    assert err <= 1e-6 * tt.qr_norm(a)                         # a o 1 = a up to eps-level truncation
+    dig = np.random.default_rng(9).integers(0, 2, size=(4096, L))
+    ya, yy = tt.evaluate(a, dig), tt.evaluate(y, dig)
+    assert np.sqrt(np.mean((ya - yy) ** 2) / np.mean(ya ** 2)) <= 1e-6
+
+
+def test_cfg5_full_batch_sampled_members(lib):
+    """configs[4] in bench.py's launch configuration (512 members on one GPU, one persistent
+    launch): sampled members compared with the oracle one by one."""
+    import torch
+    members = list(range(512))
+    probs, xs, ops = gen.cfg5_batch_arrays(members)
+    xd, od = lib.to_device(xs), lib.to_device(ops, mpo=True)
+    res = lib.ZipupPlan("ij,j->i", od, xd, 1e-10, 64, sigma_stride=128).run(od, xd)
+    torch.cuda.synchronize()
+    assert int(res.status.item()) == 0
+    for b in (0, 147, 148, 333, 511):
+        cores, ranks, sig, d2, n2 = member(lib, res, b)
+        p = probs[b]
+        compare("matvec", p.op.cores, p.x.cores, p.eps, p.max_rank, cores, ranks, sig, d2, n2, dense=False)
