@@ -96,6 +96,31 @@ __device__ void cta_gemm(int M, int N, int K, FA A, FB B, FS store, double *sm) 
   }
 }
 
+// Branch-free reciprocal and reciprocal square root: MUFU seed + 2 Newton steps.  The seed's
+// relative error is <= 1e-6 (measured over 2^-40..2^40 by csrc/probe/lat.cu), so two
+// quadratic steps give ~1e-24 << 2^-53: full fp64 accuracy for the normal range used here.
+// (Rotation parameters need c^2+s^2 = 1 to working precision, which s = c*t with
+// c = rsqrt(1+t^2) guarantees.)
+__device__ __forceinline__ double fast_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const double h = x * y;
+    const double e = fma(-h, y, 1.0);      // 1 - x y^2
+    y = fma(0.5 * y, e, y);
+  }
+  return y;
+}
+
 // LAPACK dlarfg convention: x = [alpha; x2], ||x2||^2 = xnorm2.  Returns tau and beta and
 // the scale 1/(alpha - beta) for v2 = x2 * scale (v0 = 1 implicit).  H x = [beta; 0].
 __device__ __forceinline__ void householder(double alpha, double xnorm2, double &tau, double &beta,
@@ -108,6 +133,25 @@ __device__ __forceinline__ void householder(double alpha, double xnorm2, double 
   beta = (alpha >= 0.0) ? -nrm : nrm;
   tau = (beta - alpha) / beta;
   scale = 1.0 / (alpha - beta);
+}
+
+// householder() with MUFU-seeded Newton rcp / rsqrt instead of IEEE sqrt and two divisions
+// (same values to a few ulps; shortens the serial chain of a panel factorisation).
+// tau = (beta - alpha)/beta = 1 + |alpha|/nrm;  scale = 1/(alpha - beta) = sign(alpha)/(|alpha| + nrm).
+__device__ __forceinline__ void householder_fast(double alpha, double xnorm2, double &tau, double &beta,
+                                                 double &scale) {
+  const double a2 = fma(alpha, alpha, xnorm2);
+  if (xnorm2 == 0.0 || !(a2 > 1e-280 && a2 < 1e280)) {   // zero column / outside the ftz-safe range
+    householder(alpha, xnorm2, tau, beta, scale);
+    return;
+  }
+  const double rn = fast_rsqrt(a2);
+  const double nrm = a2 * rn;
+  const double aa = fabs(alpha);
+  beta = (alpha >= 0.0) ? -nrm : nrm;
+  tau = fma(aa, rn, 1.0);
+  const double sc = fast_rcp(aa + nrm);
+  scale = (alpha >= 0.0) ? sc : -sc;
 }
 
 }  // namespace qtt

@@ -20,31 +20,6 @@ namespace qtt {
 
 constexpr int kJacobiMaxSweeps = 60;
 
-// Branch-free reciprocal and reciprocal square root: MUFU seed + Newton steps (full fp64
-// accuracy for the normal range used here; rotation parameters need c^2+s^2 = 1 to working
-// precision, which s = c*t with c = rsqrt(1+t^2) guarantees).
-__device__ __forceinline__ double fast_rcp(double x) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  return fma(y, e, y);
-}
-__device__ __forceinline__ double fast_rsqrt(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-#pragma unroll
-  for (int it = 0; it < 3; ++it) {
-    const double h = x * y;
-    const double e = fma(-h, y, 1.0);      // 1 - x y^2
-    y = fma(0.5 * y, e, y);
-  }
-  return y;
-}
-
 // Butterfly reduce-scatter: NV (power of two <= 32) per-lane partial sums -> lane l holds the
 // warp total of value index (l >> (5 - log2 NV)) in v[0].
 template <int CNT, int OFF, int NV>

@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "jacobi.cuh"
 #include "large.cuh"
+#include "orth.cuh"
 
 namespace qtt {
 
@@ -141,6 +142,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_orth(OrthArgs a) {
     const int c = legs * rr;
     const int k = min(c, r);
     double *core = base + a.off[q];
+    {  // register-resident QR (orth.cuh) when the site fits; else the shared-memory path below
+      const int rows_prev = a.r0[q - 1] * a.legs[q - 1];
+      const int rpl = (c <= 32) ? 1 : (c <= 64) ? 2 : (c <= 128) ? 4 : 0;
+      const int ncw = (r <= 8) ? 1 : (r <= 16) ? 2 : (r <= 32) ? 4 : (r <= 64) ? 8 : 0;
+      if (rpl && ncw && orth_reg_smem(rpl, c, r, rows_prev) <= kOrthSmemDoubles) {
+        double *prev = base + a.off[q - 1];
+#define QTT_ORTH(R_, N_) \
+  else if (rpl == R_ && ncw == N_) orth_site_reg<R_, N_>(core, c, r, prev, rows_prev, smem);
+        if (false) {}
+        QTT_ORTH(1, 1) QTT_ORTH(1, 2) QTT_ORTH(1, 4) QTT_ORTH(1, 8)
+        QTT_ORTH(2, 1) QTT_ORTH(2, 2) QTT_ORTH(2, 4) QTT_ORTH(2, 8)
+        QTT_ORTH(4, 1) QTT_ORTH(4, 2) QTT_ORTH(4, 4) QTT_ORTH(4, 8)
+#undef QTT_ORTH
+        if (tid == 0) rk[q] = k;
+        rr = k;
+        continue;
+      }
+    }
     double *Rsm = Ms + (size_t)c * r;                 // k x r
     double *Psm = Rsm + (size_t)k * r;                // rows_prev x r
     // M^T (c x r, column-major): column aa = row aa of the core (contiguous)
@@ -220,36 +239,34 @@ __device__ __forceinline__ void qr_panel(double *Rp, double *Bk, double *tau, in
   for (int jj = 0; jj < kPanel; ++jj) {
     const int j = j0 + jj;
     if (j < m) {
-      double s = 0.0;
+      // one reduce-scatter gives both ||x_j||^2 (index jj) and x_j . x_c for the remaining panel
+      // columns (v_j = scale * x_j below the unit entry, so v_j . x_c = scale * x_j . x_c):
+      // the norm and the dot products share one latency chain
+      double v[kPanel];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) s = fma(P[jj][t], P[jj][t], s);
-      s = warp_sum(s);
+      for (int cc = 0; cc < kPanel; ++cc) {
+        double d = 0.0;
+        if (cc >= jj) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) d = fma(P[jj][t], P[cc][t], d);
+        }
+        v[cc] = d;
+      }
+      halve<kPanel, 16, kPanel>(v, lane);          // lane l holds the total of index l >> 1
+      const double s = __shfl_sync(0xffffffffu, v[0], jj << 1);
       double tj, beta, scale;
-      householder(Rp[rp_idx(j, j, m)], s, tj, beta, scale);
+      householder_fast(Rp[rp_idx(j, j, m)], s, tj, beta, scale);
 #pragma unroll
       for (int t = 0; t < 4; ++t) P[jj][t] *= scale;
-      __syncwarp();
       if (lane == 0) { Rp[rp_idx(j, j, m)] = beta; tau[j] = tj; }
-      if (jj + 1 < kPanel && tj != 0.0) {
-        // dots of v_j with the remaining panel columns: reduce-scatter of 16 partials
-        double v[kPanel];
-#pragma unroll
-        for (int cc = 0; cc < kPanel; ++cc) {
-          double d = 0.0;
-          if (cc > jj) {
-#pragma unroll
-            for (int t = 0; t < 4; ++t) d = fma(P[jj][t], P[cc][t], d);
-          }
-          v[cc] = d;
-        }
-        halve<kPanel, 16, kPanel>(v, lane);        // lane l holds the total of index l >> 1
+      if (tj != 0.0) {
 #pragma unroll
         for (int cc = jj + 1; cc < kPanel; ++cc) {
           const int c = j0 + cc;
           const double dot = __shfl_sync(0xffffffffu, v[0], cc << 1);
           if (c < m) {
             const double rjc = Rp[rp_idx(j, c, m)];
-            const double w = tj * (rjc + dot);
+            const double w = tj * fma(scale, dot, rjc);
 #pragma unroll
             for (int t = 0; t < 4; ++t) P[cc][t] = fma(-w, P[jj][t], P[cc][t]);
             if (lane == 0) Rp[rp_idx(j, c, m)] = rjc - w;
