@@ -40,7 +40,7 @@ constexpr int kMaxSites = 64;
 constexpr int kSmall = 128;            // max rows m (and p) of a site matrix on this path
 constexpr int kRpDoubles = kSmall * (kSmall + 1) / 2;  // packed R / GEMM staging / scratch (8256)
 constexpr int kBkDoubles = kRpDoubles;                  // staged MPO core limit
-constexpr int kSiteSmemDoubles = kRpDoubles + kSmall * kLdA + kSmall + 8 + 8 + kSmall;
+constexpr int kSiteSmemDoubles = kRpDoubles + kSmall * kLdA + kSmall + 8 + 8 + kSmall + 16 * 136;
 constexpr size_t kSiteSmemBytes = kSiteSmemDoubles * sizeof(double) + (kSmall + 8) * sizeof(int);
 constexpr int kOrthSmemDoubles = 26000;  // a1 staging budget (~203 KB)
 
@@ -283,10 +283,101 @@ __device__ __forceinline__ void qr_panel(double *Rp, double *Bk, double *tau, in
       if (j0 + cc < m) Bk[(lane + 32 * t) * kLdA + j0 + cc] = P[cc][t];
 }
 
-__device__ void qr_of_TH(const double *T, int m, int n, double *Rp, double *Bk, double *tau) {
+// Trailing update of the panel j0..jn-1 (reflectors v_jj = [e_(j0+jj) on R's row; V_B[:, jj]],
+// V_B = Bk columns j0..jn-1) on the columns c in [jn, m) of [R; B], in compact-WY form without
+// forming T (LAPACK dlarft):  Y = V^T C (DMMA, with G = V_B^T V_B in the same GEMM),
+// Z = tau-forward substitution Z_jj = tau_jj (Y_jj - sum_{i<jj} G_{i,jj} Z_i) (the sequential
+// reflector recurrence, exactly), then R_p -= Z, B -= V_B Z (DMMA).  Equivalent to applying
+// H_(j0) ... H_(jn-1) one after another.
+constexpr int kYld = 136;            // Y/Z row stride (== 8 mod 16: conflict-free fragment loads)
+
+__device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+__device__ void qr_trailing_wy(double *Rp, double *Bk, const double *tau, double *Ysm, int m, int j0, int jn) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int half = tid & 1, r0 = half * (kSmall / 2);
-  const unsigned pair_mask = 3u << (lane & ~1);
+  const int np = jn - j0;                         // reflectors in the panel (<= 16)
+  const int gr = lane >> 2, gc = lane & 3;        // mma fragment coordinates
+  // (1) Yfull (16 x (m - j0)) = V_B^T Bk[:, j0:m]   (columns j0..jn-1 give the Gram G)
+  {
+    const int ntile = (m - j0 + 7) >> 3;
+    for (int nt = warp; nt < ntile; nt += kWarps) {
+      double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      const int bcol = j0 + nt * 8 + gr;          // B fragment: column gr, row gc
+      const bool bok = bcol < m;
+#pragma unroll 4
+      for (int k0 = 0; k0 < kSmall; k0 += 4) {
+        const double *rowp = Bk + (size_t)(k0 + gc) * kLdA;
+        const double b = bok ? rowp[bcol] : 0.0;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int ar = mt * 8 + gr;             // A fragment: row gr (reflector), col gc (k)
+          const double av = (ar < np) ? rowp[j0 + ar] : 0.0;
+          dmma884(c[mt][0], c[mt][1], av, b);
+        }
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = j0 + nt * 8 + 2 * gc + e;
+          if (col < m) Ysm[(mt * 8 + gr) * kYld + col] = c[mt][e];
+        }
+    }
+  }
+  __syncthreads();
+  // (2) per trailing column: Z = forward substitution; R rows j0..jn-1 updated
+  for (int c = jn + tid; c < m; c += kThreads) {
+    double z[kPanel];
+#pragma unroll
+    for (int jj = 0; jj < kPanel; ++jj) {
+      z[jj] = 0.0;
+      if (jj < np) {
+        const int j = j0 + jj;
+        double y = Ysm[jj * kYld + c] + Rp[rp_idx(j, c, m)];
+#pragma unroll
+        for (int i = 0; i < jj; ++i) y = fma(-Ysm[i * kYld + j0 + jj], z[i], y);
+        z[jj] = tau[j] * y;
+        Rp[rp_idx(j, c, m)] -= z[jj];
+        Ysm[jj * kYld + c] = z[jj];
+      }
+    }
+  }
+  __syncthreads();
+  // (3) B[:, jn:m] -= V_B Z      (tiles of 8 rows x 8 columns, K = np <= 16)
+  {
+    const int nct = (m - jn + 7) >> 3;
+    for (int rt = warp; rt < kSmall / 8; rt += kWarps) {
+      double af[4];                                 // -V_B fragments for this row tile
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int kk = ks * 4 + gc;
+        af[ks] = (kk < np) ? -Bk[(size_t)(rt * 8 + gr) * kLdA + j0 + kk] : 0.0;
+      }
+      for (int ct = 0; ct < nct; ++ct) {
+        const int cb = jn + ct * 8;
+        double *crow = Bk + (size_t)(rt * 8 + gr) * kLdA;
+        const int cc0 = cb + 2 * gc;
+        double c0 = (cc0 < m) ? crow[cc0] : 0.0, c1 = (cc0 + 1 < m) ? crow[cc0 + 1] : 0.0;
+        const int zc = cb + gr;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const int kk = ks * 4 + gc;
+          const double zb = (kk < np && zc < m) ? Ysm[kk * kYld + zc] : 0.0;
+          dmma884(c0, c1, af[ks], zb);
+        }
+        if (cc0 < m) crow[cc0] = c0;
+        if (cc0 + 1 < m) crow[cc0 + 1] = c1;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ void qr_of_TH(const double *T, int m, int n, double *Rp, double *Bk, double *tau, double *Ysm) {
+  const int tid = threadIdx.x, warp = tid >> 5;
   for (int i = tid; i < kRpDoubles; i += kThreads) Rp[i] = 0.0;
   for (int c0 = 0; c0 < n; c0 += kSmall) {
     const int nb = min(kSmall, n - c0);
@@ -300,33 +391,7 @@ __device__ void qr_of_TH(const double *T, int m, int n, double *Rp, double *Bk, 
       const int jn = min(j0 + kPanel, m);
       if (warp == 0) qr_panel(Rp, Bk, tau, m, j0);
       __syncthreads();
-      for (int c = jn + (tid >> 1); c < m; c += kThreads / 2) {
-        double x[kSmall / 2];
-#pragma unroll
-        for (int i = 0; i < kSmall / 2; ++i) x[i] = Bk[(r0 + i) * kLdA + c];
-        for (int j = j0; j < jn; ++j) {
-          const double t = tau[j];
-          if (t == 0.0) continue;
-          const double *vj = Bk + j;
-          double s0 = (half == 0) ? Rp[rp_idx(j, c, m)] : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-          for (int i = 0; i < kSmall / 2; i += 4) {
-            s0 = fma(vj[(r0 + i) * kLdA], x[i], s0);
-            s1 = fma(vj[(r0 + i + 1) * kLdA], x[i + 1], s1);
-            s2 = fma(vj[(r0 + i + 2) * kLdA], x[i + 2], s2);
-            s3 = fma(vj[(r0 + i + 3) * kLdA], x[i + 3], s3);
-          }
-          double w = (s0 + s1) + (s2 + s3);
-          w += __shfl_xor_sync(pair_mask, w, 1);
-          w *= t;
-          if (half == 0) Rp[rp_idx(j, c, m)] -= w;
-#pragma unroll
-          for (int i = 0; i < kSmall / 2; ++i) x[i] = fma(-w, vj[(r0 + i) * kLdA], x[i]);
-        }
-#pragma unroll
-        for (int i = 0; i < kSmall / 2; ++i) Bk[(r0 + i) * kLdA + c] = x[i];
-      }
-      __syncthreads();
+      if (jn < m) qr_trailing_wy(Rp, Bk, tau, Ysm, m, j0, jn);
     }
   }
 }
@@ -339,7 +404,8 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
   double *red = sg + kSmall;                 // block-reduction scratch
   double *scal = red + 8;                    // scalars
   double *tau = scal + 8;                    // Householder tau per column
-  int *perm = reinterpret_cast<int *>(tau + kSmall);
+  double *Ysm = tau + kSmall;                  // QR trailing update: Y / Z (16 x kYld)
+  int *perm = reinterpret_cast<int *>(Ysm + 16 * kYld);
   int *iflag = perm + kSmall;
 
   const int tid = threadIdx.x;
@@ -373,6 +439,31 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
     for (int i = tid; i < wsz; i += kThreads) Bk[i] = Oq[i];
     __syncthreads();
     // T[c,i,w',r'] = sum_{w,j} X[c,w,j,r'] W[w,i,j,w']
+    const int dw = d * w2;
+    if (dw <= 16) {
+      // one thread per (c, r'): every X value is loaded once (coalesced along r') and feeds all
+      // d*w' outputs of that (c, r'); W is read from shared memory (warp-uniform addresses)
+      int woff[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) woff[e] = (e < dw) ? (e / w2) * dj * w2 + e % w2 : 0;
+      for (int pr = tid; pr < chi * r2; pr += kThreads) {
+        const int c = pr / r2, rr2 = pr - c * r2;
+        double acc[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) acc[e] = 0.0;
+        for (int ww = 0; ww < w; ++ww)
+          for (int jj = 0; jj < dj; ++jj) {
+            const double xv = X[((size_t)(c * w + ww) * dj + jj) * r2 + rr2];
+            const double *wr = Bk + (ww * d * dj + jj) * w2;
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              if (e < dw) acc[e] = fma(xv, wr[woff[e]], acc[e]);
+          }
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          if (e < dw) T[((size_t)c * dw + e) * r2 + rr2] = acc[e];
+      }
+    } else
     for (int idx = tid; idx < m * n; idx += kThreads) {
       const int rr2 = idx % r2;
       int t1 = idx / r2;
@@ -426,7 +517,7 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
   int p;
   if (m <= n) {
     p = m;
-    qr_of_TH(T, m, n, Rp, Rs, tau);
+    qr_of_TH(T, m, n, Rp, Rs, tau, Ysm);
     __syncthreads();
     for (int idx = tid; idx < m * m; idx += kThreads) {   // A = R^T: column j of A = row j of R
       const int j = idx / m, row = idx % m;
