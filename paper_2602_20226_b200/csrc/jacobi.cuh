@@ -42,7 +42,7 @@ __device__ __forceinline__ void halve(double (&v)[NV], int lane) {
 }
 
 template <int N>
-__device__ constexpr int ilog2() { return N <= 1 ? 0 : 1 + ilog2<N / 2>(); }
+__host__ __device__ constexpr int ilog2() { return N <= 1 ? 0 : 1 + ilog2<N / 2>(); }
 
 // Exact squared norms of the warp's 2*WB register columns -> nrm[0..2WB) (shared, per warp).
 template <int RPL, int WB>

@@ -19,6 +19,10 @@
 #include "large.cuh"
 #include "orth.cuh"
 
+#ifndef QTT_QR_PANEL
+#define QTT_QR_PANEL 8
+#endif
+
 namespace qtt {
 
 static thread_local char g_err[512] = "";
@@ -224,7 +228,8 @@ struct SweepArgs {
 // registers (4 rows per lane, warp-wide reductions, no CTA barrier inside the panel); then
 // every thread pair applies the 16 reflectors to one trailing column held in registers.
 // Two CTA barriers per panel; 2 blocks for n = 256.
-constexpr int kPanel = 16;
+constexpr int kPanel = QTT_QR_PANEL;
+constexpr int kPanelSh = 5 - ilog2<kPanel>();   // halve<kPanel>: lane l holds index l >> kPanelSh
 
 __device__ __forceinline__ int rp_idx(int j, int c, int m) { return j * m - (j * (j - 1)) / 2 + (c - j); }
 
@@ -252,8 +257,8 @@ __device__ __forceinline__ void qr_panel(double *Rp, double *Bk, double *tau, in
         }
         v[cc] = d;
       }
-      halve<kPanel, 16, kPanel>(v, lane);          // lane l holds the total of index l >> 1
-      const double s = __shfl_sync(0xffffffffu, v[0], jj << 1);
+      halve<kPanel, 16, kPanel>(v, lane);
+      const double s = __shfl_sync(0xffffffffu, v[0], jj << kPanelSh);
       double tj, beta, scale;
       householder_fast(Rp[rp_idx(j, j, m)], s, tj, beta, scale);
 #pragma unroll
@@ -263,7 +268,7 @@ __device__ __forceinline__ void qr_panel(double *Rp, double *Bk, double *tau, in
 #pragma unroll
         for (int cc = jj + 1; cc < kPanel; ++cc) {
           const int c = j0 + cc;
-          const double dot = __shfl_sync(0xffffffffu, v[0], cc << 1);
+          const double dot = __shfl_sync(0xffffffffu, v[0], cc << kPanelSh);
           if (c < m) {
             const double rjc = Rp[rp_idx(j, c, m)];
             const double w = tj * fma(scale, dot, rjc);
@@ -304,7 +309,9 @@ __device__ void qr_trailing_wy(double *Rp, double *Bk, const double *tau, double
   {
     const int ntile = (m - j0 + 7) >> 3;
     for (int nt = warp; nt < ntile; nt += kWarps) {
-      double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      double c[kPanel / 8][2];
+#pragma unroll
+      for (int mt = 0; mt < kPanel / 8; ++mt) c[mt][0] = c[mt][1] = 0.0;
       const int bcol = j0 + nt * 8 + gr;          // B fragment: column gr, row gc
       const bool bok = bcol < m;
 #pragma unroll 4
@@ -312,14 +319,14 @@ __device__ void qr_trailing_wy(double *Rp, double *Bk, const double *tau, double
         const double *rowp = Bk + (size_t)(k0 + gc) * kLdA;
         const double b = bok ? rowp[bcol] : 0.0;
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
+        for (int mt = 0; mt < kPanel / 8; ++mt) {
           const int ar = mt * 8 + gr;             // A fragment: row gr (reflector), col gc (k)
           const double av = (ar < np) ? rowp[j0 + ar] : 0.0;
           dmma884(c[mt][0], c[mt][1], av, b);
         }
       }
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+      for (int mt = 0; mt < kPanel / 8; ++mt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int col = j0 + nt * 8 + 2 * gc + e;
@@ -350,9 +357,9 @@ __device__ void qr_trailing_wy(double *Rp, double *Bk, const double *tau, double
   {
     const int nct = (m - jn + 7) >> 3;
     for (int rt = warp; rt < kSmall / 8; rt += kWarps) {
-      double af[4];                                 // -V_B fragments for this row tile
+      double af[kPanel / 4];                        // -V_B fragments for this row tile
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
+      for (int ks = 0; ks < kPanel / 4; ++ks) {
         const int kk = ks * 4 + gc;
         af[ks] = (kk < np) ? -Bk[(size_t)(rt * 8 + gr) * kLdA + j0 + kk] : 0.0;
       }
@@ -363,7 +370,7 @@ __device__ void qr_trailing_wy(double *Rp, double *Bk, const double *tau, double
         double c0 = (cc0 < m) ? crow[cc0] : 0.0, c1 = (cc0 + 1 < m) ? crow[cc0 + 1] : 0.0;
         const int zc = cb + gr;
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
+        for (int ks = 0; ks < kPanel / 4; ++ks) {
           const int kk = ks * 4 + gc;
           const double zb = (kk < np && zc < m) ? Ysm[kk * kYld + zc] : 0.0;
           dmma884(c0, c1, af[ks], zb);

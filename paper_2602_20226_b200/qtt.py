@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libqtt.so")
+LIB_PATH = os.environ.get("QTT_LIB", os.path.join(_HERE, "lib", "libqtt.so"))  # QTT_LIB: A/B variants in experiments
 
 QTT_OK = 0
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ESHAPE", 3: "ECONFORM", 4: "ENUMERIC", 5: "ECAPACITY",
