@@ -31,8 +31,9 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Block-wide sum over kThreads threads; `red` is >= kWarps doubles of shared memory.
+// Block-wide sum over NW warps; `red` is >= NW doubles of shared memory.
 // All threads must call it; returns the total to every thread.
+template <int NW = kWarps>
 __device__ __forceinline__ double block_sum(double v, double *red) {
   v = warp_sum(v);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -41,7 +42,7 @@ __device__ __forceinline__ double block_sum(double v, double *red) {
   __syncthreads();
   double t = 0.0;
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) t += red[w];   // fixed order: deterministic
+  for (int w = 0; w < NW; ++w) t += red[w];   // fixed order: deterministic
   return t;
 }
 
@@ -49,13 +50,16 @@ __device__ __forceinline__ double block_sum(double v, double *red) {
 // 16-deep K chunks staged in shared memory `sm` (>= 2*16*64 doubles); 256 threads,
 // each owning a 4x4 register tile (rows ty+16i, cols tx+16j: conflict-free smem reads).
 // A(m,k), B(k,n) are callables returning double; store(m,n,v) writes the result.
-template <typename FA, typename FB, typename FS>
+// NT threads (256: 64x64 tiles; 512: 64x128 tiles), staging >= 16*64 + 16*TN doubles.
+template <int NT = kThreads, typename FA, typename FB, typename FS>
 __device__ void cta_gemm(int M, int N, int K, FA A, FB B, FS store, double *sm) {
+  static_assert(NT == 256 || NT == 512, "cta_gemm: 256 or 512 threads");
+  constexpr int TN = (NT == 512) ? 128 : 64, TX = TN / 4;
   double *As = sm;            // [16][64]
-  double *Bs = sm + 16 * 64;  // [16][64]
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  double *Bs = sm + 16 * 64;  // [16][TN]
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
   for (int m0 = 0; m0 < M; m0 += 64) {
-    for (int n0 = 0; n0 < N; n0 += 64) {
+    for (int n0 = 0; n0 < N; n0 += TN) {
       double acc[4][4];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -63,12 +67,18 @@ __device__ void cta_gemm(int M, int N, int K, FA A, FB B, FS store, double *sm) 
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
       for (int k0 = 0; k0 < K; k0 += 16) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int idx = tid + e * kThreads;      // 0..1023
+        for (int e = 0; e < 1024 / NT; ++e) {
+          const int idx = tid + e * NT;            // 0..1023
           const int kk = idx >> 6, mm = idx & 63;
-          const int gm = m0 + mm, gk = k0 + kk, gn = n0 + mm;
+          const int gm = m0 + mm, gk = k0 + kk;
           As[kk * 64 + mm] = (gm < M && gk < K) ? A(gm, gk) : 0.0;
-          Bs[kk * 64 + mm] = (gn < N && gk < K) ? B(gk, gn) : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < 16 * TN / NT; ++e) {
+          const int idx = tid + e * NT;            // 0..16*TN-1
+          const int kk = idx / TN, nn = idx % TN;
+          const int gn = n0 + nn, gk = k0 + kk;
+          Bs[kk * TN + nn] = (gn < N && gk < K) ? B(gk, gn) : 0.0;
         }
         __syncthreads();
 #pragma unroll
@@ -77,7 +87,7 @@ __device__ void cta_gemm(int M, int N, int K, FA A, FB B, FS store, double *sm) 
 #pragma unroll
           for (int i = 0; i < 4; ++i) a[i] = As[kk * 64 + ty + 16 * i];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) b[j] = Bs[kk * 64 + tx + 16 * j];
+          for (int j = 0; j < 4; ++j) b[j] = Bs[kk * TN + tx + TX * j];
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -89,7 +99,7 @@ __device__ void cta_gemm(int M, int N, int K, FA A, FB B, FS store, double *sm) 
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int gm = m0 + ty + 16 * i, gn = n0 + tx + 16 * j;
+          const int gm = m0 + ty + 16 * i, gn = n0 + tx + TX * j;
           if (gm < M && gn < N) store(gm, gn, acc[i][j]);
         }
     }

@@ -186,14 +186,14 @@ __device__ __forceinline__ void rotate_circle(double (&X)[2 * WB][RPL], int *slo
 }
 
 // Returns the number of sweeps executed (== kJacobiMaxSweeps: not converged).
-template <int RPL, int WB>
+template <int RPL, int WB, int NW>
 __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
-  constexpr int NB = 2 * kWarps;      // 16 blocks of WB columns
+  constexpr int NB = 2 * NW;          // 2*NW blocks of WB columns (one block pair per warp)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double tol = (double)max(m, 1) * DBL_EPSILON;
   double X[2 * WB][RPL];
   double *nrm = scratch + warp * 2 * WB;                                   // norms by local column
-  int *slot_col = reinterpret_cast<int *>(scratch + kWarps * 2 * WB) + warp * 2 * WB;
+  int *slot_col = reinterpret_cast<int *>(scratch + NW * 2 * WB) + warp * 2 * WB;
   int sweep = 0;
   for (; sweep < kJacobiMaxSweeps; ++sweep) {
     int rot = 0;
@@ -247,14 +247,19 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
   return sweep;
 }
 
-// Dispatch on the padded sizes: RPL = ceil(m/32) in {1,2,4}, WB = ceil(p/16) in {1,2,4,8}.
+// Dispatch on the padded sizes: RPL = ceil(m/32) in {1,2,4}, WB = ceil(p/(2 NW)) (powers of 2,
+// 2*NW*WB <= 128 columns).  The caller zero-pads rows to 32*RPL and columns to 2*NW*WB.
+template <int NW>
 __device__ __forceinline__ int jacobi_dispatch(double *A, int m, int p, int *flag, double *nrm_all) {
   const int rpl = (m <= 32) ? 1 : (m <= 64) ? 2 : 4;
-  const int wb = (p <= 16) ? 1 : (p <= 32) ? 2 : (p <= 64) ? 4 : 8;
-#define QTT_JAC(R, W) if (rpl == R && wb == W) return jacobi_blocked<R, W>(A, m, flag, nrm_all);
-  QTT_JAC(1, 1) QTT_JAC(1, 2) QTT_JAC(1, 4) QTT_JAC(1, 8)
-  QTT_JAC(2, 1) QTT_JAC(2, 2) QTT_JAC(2, 4) QTT_JAC(2, 8)
-  QTT_JAC(4, 1) QTT_JAC(4, 2) QTT_JAC(4, 4) QTT_JAC(4, 8)
+  const int wb = (p <= 2 * NW) ? 1 : (p <= 4 * NW) ? 2 : (p <= 8 * NW) ? 4 : 8;
+#define QTT_JAC(R, W) if (rpl == R && wb == W) return jacobi_blocked<R, W, NW>(A, m, flag, nrm_all);
+  QTT_JAC(1, 1) QTT_JAC(1, 2) QTT_JAC(1, 4)
+  QTT_JAC(2, 1) QTT_JAC(2, 2) QTT_JAC(2, 4)
+  QTT_JAC(4, 1) QTT_JAC(4, 2) QTT_JAC(4, 4)
+  if constexpr (NW <= 8) {
+    QTT_JAC(1, 8) QTT_JAC(2, 8) QTT_JAC(4, 8)
+  }
 #undef QTT_JAC
   return kJacobiMaxSweeps;
 }

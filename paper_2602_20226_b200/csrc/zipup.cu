@@ -44,7 +44,7 @@ constexpr int kMaxSites = 64;
 constexpr int kSmall = 128;            // max rows m (and p) of a site matrix on this path
 constexpr int kRpDoubles = kSmall * (kSmall + 1) / 2;  // packed R / GEMM staging / scratch (8256)
 constexpr int kBkDoubles = kRpDoubles;                  // staged MPO core limit
-constexpr int kSiteSmemDoubles = kRpDoubles + kSmall * kLdA + kSmall + 8 + 8 + kSmall + 16 * 136;
+constexpr int kSiteSmemDoubles = kRpDoubles + kSmall * kLdA + kSmall + 16 + 8 + kSmall + 16 * 136;
 constexpr size_t kSiteSmemBytes = kSiteSmemDoubles * sizeof(double) + (kSmall + 8) * sizeof(int);
 constexpr int kOrthSmemDoubles = 26000;  // a1 staging budget (~203 KB)
 
@@ -197,6 +197,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_orth(OrthArgs a) {
 
 // ======================================================================= a2..a7: site step
 
+// Threads per k_sweep CTA (one CTA per SM).  256 (8 warps, <= 255 registers, one block pair
+// of 2 x 8 columns per warp in the Jacobi) measured faster than 512 (16 warps, <= 128
+// registers, 2 x 4 columns): 90.2k vs 102.2k site-steps/s on cfg5 -- the Jacobi round is
+// bound by FP64 and MIO issue, not by latency that more warps could hide.
+#ifndef QTT_SWEEP_THREADS
+#define QTT_SWEEP_THREADS 256
+#endif
+constexpr int kST = QTT_SWEEP_THREADS;
+constexpr int kSW = kST / 32;
+
 struct SweepArgs {
   int L, B, kind, shared_op;
   int d[kMaxSites], dj[kMaxSites];       // output / contracted digit size per site
@@ -308,7 +318,7 @@ __device__ void qr_trailing_wy(double *Rp, double *Bk, const double *tau, double
   // (1) Yfull (16 x (m - j0)) = V_B^T Bk[:, j0:m]   (columns j0..jn-1 give the Gram G)
   {
     const int ntile = (m - j0 + 7) >> 3;
-    for (int nt = warp; nt < ntile; nt += kWarps) {
+    for (int nt = warp; nt < ntile; nt += kSW) {
       double c[kPanel / 8][2];
 #pragma unroll
       for (int mt = 0; mt < kPanel / 8; ++mt) c[mt][0] = c[mt][1] = 0.0;
@@ -336,7 +346,7 @@ __device__ void qr_trailing_wy(double *Rp, double *Bk, const double *tau, double
   }
   __syncthreads();
   // (2) per trailing column: Z = forward substitution; R rows j0..jn-1 updated
-  for (int c = jn + tid; c < m; c += kThreads) {
+  for (int c = jn + tid; c < m; c += kST) {
     double z[kPanel];
 #pragma unroll
     for (int jj = 0; jj < kPanel; ++jj) {
@@ -356,7 +366,7 @@ __device__ void qr_trailing_wy(double *Rp, double *Bk, const double *tau, double
   // (3) B[:, jn:m] -= V_B Z      (tiles of 8 rows x 8 columns, K = np <= 16)
   {
     const int nct = (m - jn + 7) >> 3;
-    for (int rt = warp; rt < kSmall / 8; rt += kWarps) {
+    for (int rt = warp; rt < kSmall / 8; rt += kSW) {
       double af[kPanel / 4];                        // -V_B fragments for this row tile
 #pragma unroll
       for (int ks = 0; ks < kPanel / 4; ++ks) {
@@ -385,11 +395,11 @@ __device__ void qr_trailing_wy(double *Rp, double *Bk, const double *tau, double
 
 __device__ void qr_of_TH(const double *T, int m, int n, double *Rp, double *Bk, double *tau, double *Ysm) {
   const int tid = threadIdx.x, warp = tid >> 5;
-  for (int i = tid; i < kRpDoubles; i += kThreads) Rp[i] = 0.0;
+  for (int i = tid; i < kRpDoubles; i += kST) Rp[i] = 0.0;
   for (int c0 = 0; c0 < n; c0 += kSmall) {
     const int nb = min(kSmall, n - c0);
     __syncthreads();
-    for (int idx = tid; idx < kSmall * m; idx += kThreads) {
+    for (int idx = tid; idx < kSmall * m; idx += kST) {
       const int j = idx / kSmall, i = idx % kSmall;    // coalesced along i (columns of T)
       Bk[i * kLdA + j] = (i < nb) ? T[(size_t)j * n + c0 + i] : 0.0;
     }
@@ -409,7 +419,7 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
   double *Bk = Rp;                           // staging alias
   double *sg = Rs + kSmall * kLdA;           // sigma^2 per column
   double *red = sg + kSmall;                 // block-reduction scratch
-  double *scal = red + 8;                    // scalars
+  double *scal = red + 16;                   // scalars
   double *tau = scal + 8;                    // Householder tau per column
   double *Ysm = tau + kSmall;                  // QR trailing update: Y / Z (16 x kYld)
   int *perm = reinterpret_cast<int *>(Ysm + 16 * kYld);
@@ -438,12 +448,12 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
   // ---------------------------------------------------------------- a2: contraction
   if (a.kind == MATVEC) {
     const int M = chi * w, K = r, N = dj * r2;     // X[(c,w),(j,r')] = G[(c,w),r] x_q[r,(j,r')]
-    cta_gemm(M, N, K, [&](int i, int k) { return G[(size_t)i * K + k]; },
+    cta_gemm<kST>(M, N, K, [&](int i, int k) { return G[(size_t)i * K + k]; },
              [&](int k, int j) { return Xq[(size_t)k * N + j]; },
              [&](int i, int j, double v) { X[(size_t)i * N + j] = v; }, Bk);
     __syncthreads();
     const int wsz = w * d * dj * w2;
-    for (int i = tid; i < wsz; i += kThreads) Bk[i] = Oq[i];
+    for (int i = tid; i < wsz; i += kST) Bk[i] = Oq[i];
     __syncthreads();
     // T[c,i,w',r'] = sum_{w,j} X[c,w,j,r'] W[w,i,j,w']
     const int dw = d * w2;
@@ -453,7 +463,7 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
       int woff[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) woff[e] = (e < dw) ? (e / w2) * dj * w2 + e % w2 : 0;
-      for (int pr = tid; pr < chi * r2; pr += kThreads) {
+      for (int pr = tid; pr < chi * r2; pr += kST) {
         const int c = pr / r2, rr2 = pr - c * r2;
         double acc[16];
 #pragma unroll
@@ -471,7 +481,7 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
           if (e < dw) T[((size_t)c * dw + e) * r2 + rr2] = acc[e];
       }
     } else
-    for (int idx = tid; idx < m * n; idx += kThreads) {
+    for (int idx = tid; idx < m * n; idx += kST) {
       const int rr2 = idx % r2;
       int t1 = idx / r2;
       const int ww2 = t1 % w2; t1 /= w2;
@@ -484,19 +494,19 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
     }
   } else if (a.kind == HADAMARD) {
     const int M = chi * w, K = r, N = d * r2;      // X[(c,a),(i,b')] = G[(c,a),b] x_q[b,(i,b')]
-    cta_gemm(M, N, K, [&](int i, int k) { return G[(size_t)i * K + k]; },
+    cta_gemm<kST>(M, N, K, [&](int i, int k) { return G[(size_t)i * K + k]; },
              [&](int k, int j) { return Xq[(size_t)k * N + j]; },
              [&](int i, int j, double v) { X[(size_t)i * N + j] = v; }, Bk);
     __syncthreads();
     for (int ci = 0; ci < chi * d; ++ci) {         // T[c,i,a',b'] = sum_a A[a,i,a'] X[c,a,i,b']
       const int c = ci / d, ii = ci % d;
-      cta_gemm(w2, r2, w, [&](int a2, int aa) { return Oq[((size_t)aa * d + ii) * w2 + a2]; },
+      cta_gemm<kST>(w2, r2, w, [&](int a2, int aa) { return Oq[((size_t)aa * d + ii) * w2 + a2]; },
                [&](int aa, int bb) { return X[((size_t)(c * w + aa) * d + ii) * r2 + bb]; },
                [&](int a2, int bb, double v) { T[((size_t)(c * d + ii) * w2 + a2) * r2 + bb] = v; }, Bk);
     }
   } else {
     const int M = chi, K = r, N = d * r2;          // T[c,(i,r')] = G[c,r] x_q[r,(i,r')]
-    cta_gemm(M, N, K, [&](int i, int k) { return G[(size_t)i * K + k]; },
+    cta_gemm<kST>(M, N, K, [&](int i, int k) { return G[(size_t)i * K + k]; },
              [&](int k, int j) { return Xq[(size_t)k * N + j]; },
              [&](int i, int j, double v) { T[(size_t)i * N + j] = v; }, Bk);
   }
@@ -507,8 +517,8 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
   // ---------------------------------------------------------------- a7: last site
   if (q == L - 1) {
     double s = 0.0;
-    for (int i = tid; i < m; i += kThreads) { const double v = T[i]; Cq[i] = v; s = fma(v, v, s); }
-    s = block_sum(s, red);
+    for (int i = tid; i < m; i += kST) { const double v = T[i]; Cq[i] = v; s = fma(v, v, s); }
+    s = block_sum<kSW>(s, red);
     if (tid == 0) {
       if (a.sweeps) a.sweeps[(size_t)b * L + q] = 0;
       a.norm2[b] = s;
@@ -526,13 +536,13 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
     p = m;
     qr_of_TH(T, m, n, Rp, Rs, tau, Ysm);
     __syncthreads();
-    for (int idx = tid; idx < m * m; idx += kThreads) {   // A = R^T: column j of A = row j of R
+    for (int idx = tid; idx < m * m; idx += kST) {   // A = R^T: column j of A = row j of R
       const int j = idx / m, row = idx % m;
       Rs[(size_t)j * kLdA + row] = (row >= j) ? Rp[rp_idx(j, row, m)] : 0.0;
     }
   } else {
     p = n;                                         // A = T (m x n): column j = T[:, j]
-    for (int idx = tid; idx < m * n; idx += kThreads) {
+    for (int idx = tid; idx < m * n; idx += kST) {
       const int row = idx / n, j = idx % n;
       Rs[(size_t)j * kLdA + row] = T[idx];
     }
@@ -544,18 +554,19 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
   // ---------------------------------------------------------------- a4: Jacobi SVD
   {  // zero padding required by the register-blocked Jacobi: rows [m, 32*RPL), columns [p, 16*WB)
     const int mp = (m <= 32) ? 32 : (m <= 64) ? 64 : 128;
-    const int pp = (p <= 16) ? 16 : (p <= 32) ? 32 : (p <= 64) ? 64 : 128;
-    for (int idx = tid; idx < pp * mp; idx += kThreads) {
+    const int wbp = (p <= 2 * kSW) ? 1 : (p <= 4 * kSW) ? 2 : (p <= 8 * kSW) ? 4 : 8;
+    const int pp = 2 * kSW * wbp;                   // columns the Jacobi blocks cover
+    for (int idx = tid; idx < pp * mp; idx += kST) {
       const int j = idx / mp, row = idx % mp;
       if (row >= m || j >= p) Rs[(size_t)j * kLdA + row] = 0.0;
     }
     __syncthreads();
   }
-  const int sweeps = jacobi_dispatch(Rs, m, p, iflag, Bk);   // Bk: per-warp norm scratch
+  const int sweeps = jacobi_dispatch<kSW>(Rs, m, p, iflag, Bk);   // Bk: per-warp norm scratch
   if (tid == 0 && a.cycles) a.cycles[((size_t)b * L + q) * 4 + 2] = clock64() - t_phase;
   t_phase = clock64();
   const int lane = tid & 31, warp = tid >> 5;
-  for (int j = warp; j < p; j += kWarps) {
+  for (int j = warp; j < p; j += kSW) {
     double s = 0.0;
     for (int row = lane; row < m; row += 32) { const double v = Rs[(size_t)j * kLdA + row]; s = fma(v, v, s); }
     s = warp_sum(s);
@@ -565,7 +576,7 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
     }
   }
   __syncthreads();
-  for (int j = tid; j < p; j += kThreads) {         // descending order, ties by index
+  for (int j = tid; j < p; j += kST) {         // descending order, ties by index
     const double sj = sg[j];
     int rank = 0;
     for (int l = 0; l < p; ++l) rank += (sg[l] > sj) || (sg[l] == sj && l < j);
@@ -596,7 +607,7 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
   const int k = (int)scal[1];
 
   // ---------------------------------------------------------------- a6: emit + carry
-  for (int idx = tid; idx < k * m; idx += kThreads) {   // normalise kept columns: U = A V / sigma
+  for (int idx = tid; idx < k * m; idx += kST) {   // normalise kept columns: U = A V / sigma
     const int kk = idx / m, row = idx % m;
     const int j = perm[kk];
     const double s2 = sg[j];
@@ -604,13 +615,13 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
     col[row] = (s2 > 0.0) ? col[row] / sqrt(s2) : (row == kk ? 1.0 : 0.0);
   }
   __syncthreads();
-  for (int idx = tid; idx < m * k; idx += kThreads) {   // C_q = U[:, :k] as (chi, d, k)
+  for (int idx = tid; idx < m * k; idx += kST) {   // C_q = U[:, :k] as (chi, d, k)
     const int row = idx / k, kk = idx % k;
     Cq[idx] = Rs[(size_t)perm[kk] * kLdA + row];
   }
   if (a.sigma) {
     double *sgo = a.sigma + ((size_t)b * (L - 1) + q) * a.sigma_stride;
-    for (int jj = tid; jj < a.sigma_stride; jj += kThreads) sgo[jj] = (jj < p) ? sqrt(sg[perm[jj]]) : 0.0;
+    for (int jj = tid; jj < a.sigma_stride; jj += kST) sgo[jj] = (jj < p) ? sqrt(sg[perm[jj]]) : 0.0;
   }
   if (tid == 0) {
     if (a.sweeps) a.sweeps[(size_t)b * L + q] = sweeps;
@@ -619,7 +630,7 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
     a.delta2[(size_t)b * L + q] = scal[2];
   }
   // G_{q+1}[kk][col] = sum_row U[row][kk] T[row][col]   (k x n) = diag(s_k) V_k^H
-  cta_gemm(k, n, m, [&](int kk, int row) { return Rs[(size_t)perm[kk] * kLdA + row]; },
+  cta_gemm<kST>(k, n, m, [&](int kk, int row) { return Rs[(size_t)perm[kk] * kLdA + row]; },
            [&](int row, int col) { return T[(size_t)row * n + col]; },
            [&](int kk, int col, double v) { G[(size_t)kk * n + col] = v; }, Bk);
   if (tid == 0 && a.cycles) a.cycles[((size_t)b * L + q) * 4 + 3] = clock64() - t_phase;
@@ -629,7 +640,7 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
 // order) from a global counter.  Task (b, q) waits for member b's site q-1 (release/acquire
 // on done[b]); the holder of that task was scheduled earlier and is running or finished, so
 // the wait cannot deadlock.  Balances the B*L site steps over the SMs (no wave tail).
-__global__ void __launch_bounds__(kThreads, 1) k_sweep(SweepArgs a) {
+__global__ void __launch_bounds__(kST, 1) k_sweep(SweepArgs a) {
   extern __shared__ double smem[];
   __shared__ int s_task;
   const int total = a.B * a.L;
@@ -965,7 +976,7 @@ qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt
     QTT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int grid = std::max(1, std::min(sms, S.B * S.L));
     QTT_CUDA_TRY(record(2));
-    k_sweep<<<grid, kThreads, kSiteSmemBytes, s>>>(a);
+    k_sweep<<<grid, kST, kSiteSmemBytes, s>>>(a);
     QTT_CUDA_TRY(cudaGetLastError());
     QTT_CUDA_TRY(record(3));
   }
