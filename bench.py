@@ -78,10 +78,11 @@ def site_flops(kind, ranks_y, xr, orr, d, dj, sweeps):
     """Per-site algorithmic flops for one member:
     contract / qr / carry / jacobi (executed sweeps x p(p-1)/2 pairs x 12 m)."""
     L = len(d)
+    d, dj = [int(v) for v in d], [int(v) for v in dj]
     out = []
     for q in range(L):
-        chi, r, r2 = ranks_y[q], xr[q], xr[q + 1]
-        w, w2 = (orr[q], orr[q + 1]) if kind != "truncate" else (1, 1)
+        chi, r, r2 = int(ranks_y[q]), int(xr[q]), int(xr[q + 1])        # Python ints: no int32 overflow
+        w, w2 = (int(orr[q]), int(orr[q + 1])) if kind != "truncate" else (1, 1)
         m, n = chi * d[q], w2 * r2
         if kind == "matvec":
             fc = 2 * chi * w * r * dj[q] * r2 + 2 * chi * d[q] * w2 * r2 * w * dj[q]
@@ -92,7 +93,7 @@ def site_flops(kind, ranks_y, xr, orr, d, dj, sweeps):
         if q == L - 1:
             out.append((fc, 0.0, 0.0, 0.0))
             continue
-        k = ranks_y[q + 1]
+        k = int(ranks_y[q + 1])
         p = min(m, n)
         fq = (2.0 * n * m * m - (2.0 / 3.0) * m ** 3) if m <= n else 0.0
         fk = 2.0 * k * m * n

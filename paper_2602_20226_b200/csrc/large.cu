@@ -4,7 +4,7 @@
 // One member at a time (these configs are single zip-ups); every kernel reads the site's
 // dimensions from a device SiteDims record written by k_plan, so ranks stay on the device
 // and grids are sized by capacity (surplus CTAs exit).  Per site q:
-//   a2  k_gemm_spec (strided batched GEMM) [+ k_mpo_apply]      T = contract(G, x_q, op_q)
+//   a2  k_gemm_dmma (strided batched FP64 DMMA GEMM, gemm.cuh) [+ k_mpo_apply]  T = contract(G, x_q, op_q)
 //   a3  m <= n: k_qr_coop  -- cooperative, row-distributed Householder QR of T^H with grid
 //                             barriers (16-column panels, WY trailing update, fixed-order
 //                             reductions); robust to the exact rank deficiency that cfg2/cfg4
@@ -12,7 +12,7 @@
 //       m >  n: k_transpose -- A = T
 //   a4  k_jacobi_coop -- one-sided Jacobi, block round-robin over CTAs, columns in shared
 //                        memory, exact dot products, grid barrier per block round
-//   a5/a6 k_finish (sigma, sort, truncation, emit U_k) + k_gemm_spec carry G = U_k^T T
+//   a5/a6 k_finish (sigma, sort, truncation, emit U_k) + k_gemm_dmma carry G = U_k^T T
 //   a7  k_last
 // Operands too large for the shared-memory a1 kernel are right-orthonormalised by the
 // mirrored truncate sweep (an SVD gauge instead of QR: the zip-up result is gauge
@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "large.cuh"
+#include "gemm.cuh"
 
 namespace qtt {
 
@@ -76,15 +77,6 @@ struct SiteDims {
   int chi, r, r2, w, w2, d, dj, m, n, p, direct, k;
 };
 
-struct GemmSpec {
-  int M, N, K, nz1, nz2;
-  const double *A;
-  const double *B;
-  double *C;
-  long long sam, sak, sbk, sbn, scm, scn;
-  long long sa1, sa2, sb1, sb2, sc1, sc2;
-};
-
 struct PlanArgs {
   int q, L, kind, d, dj;
   const int *xr, *orr, *yr;     // member-offset rank rows
@@ -123,28 +115,16 @@ __global__ void k_plan(PlanArgs a) {
   a.spec[1] = g1;
 }
 
-// C = A * B per spec; grid x = tiles (tiles_n per row of tiles), z = nz1*nz2 (capacity).
-__global__ void __launch_bounds__(kThreads) k_gemm_spec(const GemmSpec *spec, int tiles_n, int nz2_cap) {
-  __shared__ double sm[2 * 16 * 64];
-  const GemmSpec g = *spec;
-  const int z1 = blockIdx.z / nz2_cap, z2 = blockIdx.z % nz2_cap;
-  if (z1 >= g.nz1 || z2 >= g.nz2) return;
-  const int m0 = (blockIdx.x / tiles_n) * 64, n0 = (blockIdx.x % tiles_n) * 64;
-  if (m0 >= g.M || n0 >= g.N) return;
-  const double *A = g.A + z1 * g.sa1 + z2 * g.sa2 + m0 * g.sam;
-  const double *B = g.B + z1 * g.sb1 + z2 * g.sb2 + n0 * g.sbn;
-  double *C = g.C + z1 * g.sc1 + z2 * g.sc2 + m0 * g.scm + n0 * g.scn;
-  cta_gemm(min(64, g.M - m0), min(64, g.N - n0), g.K,
-           [&](int i, int k) { return A[i * g.sam + k * g.sak]; },
-           [&](int k, int j) { return B[k * g.sbk + j * g.sbn]; },
-           [&](int i, int j, double v) { C[i * g.scm + j * g.scn] = v; }, sm);
-}
-
+// DMMA GEMM (gemm.cuh) over capacity tiles; a_kcontig selects A's layout (row-major A,
+// sak == 1, vs. transposed views with sam == 1).
 static void launch_gemm_spec(const GemmSpec *spec, long long Mcap, long long Ncap, long long nz1cap, long long nz2cap,
-                             cudaStream_t s) {
-  const long long tm = (Mcap + 63) / 64, tn = (Ncap + 63) / 64;
+                             bool a_kcontig, cudaStream_t s) {
+  const long long tm = (Mcap + dgemm::TM - 1) / dgemm::TM, tn = (Ncap + dgemm::TN - 1) / dgemm::TN;
   dim3 grid((unsigned)(tm * tn), 1, (unsigned)(nz1cap * nz2cap));
-  k_gemm_spec<<<grid, kThreads, 0, s>>>(spec, (int)tn, (int)nz2cap);
+  if (a_kcontig)
+    k_gemm_dmma<true><<<grid, 256, dgemm::SMEM_BYTES, s>>>(spec, (int)tn, (int)nz2cap);
+  else
+    k_gemm_dmma<false><<<grid, 256, dgemm::SMEM_BYTES, s>>>(spec, (int)tn, (int)nz2cap);
 }
 
 // T[c,i,w2,r2] = sum_{w,j} X[c,w,j,r2] W[w,i,j,w2]
@@ -737,6 +717,10 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
   if (!attr) {
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_qr_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_jacobi_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)dgemm::SMEM_BYTES));
+    QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_dmma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)dgemm::SMEM_BYTES));
     attr = true;
   }
   QTT_CUDA_TRY(cudaMemsetAsync(Bf.bar, 0, sizeof(GridBar) * 2, s));
@@ -757,14 +741,14 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
     // a2: state GEMM (M <= cap*w, N <= (dj|d)*r2)
     const long long g0M = (long long)io.cap[q] * w;
     const long long g0N = (long long)((kind == MATVEC) ? io.dj[q] : io.d[q]) * io.xcap_r[q + 1];
-    launch_gemm_spec(Bf.spec + 0, g0M, g0N, 1, 1, s);
+    launch_gemm_spec(Bf.spec + 0, g0M, g0N, 1, 1, true, s);
     QTT_CUDA_TRY(cudaGetLastError());
     const unsigned ew_grid = (unsigned)std::min<long long>((m_cap * n_cap + kThreads - 1) / kThreads, 8192);
     if (kind == MATVEC) {
       k_mpo_apply<<<ew_grid, kThreads, 0, s>>>(Bf.dims, Bf.X, io.Oq[q], Bf.T);
       QTT_CUDA_TRY(cudaGetLastError());
     } else if (kind == HADAMARD) {
-      launch_gemm_spec(Bf.spec + 1, w2, io.xcap_r[q + 1], io.cap[q], io.d[q], s);
+      launch_gemm_spec(Bf.spec + 1, w2, io.xcap_r[q + 1], io.cap[q], io.d[q], false, s);
       QTT_CUDA_TRY(cudaGetLastError());
     }
     if (q == L - 1) {                                                  // a7
@@ -802,7 +786,7 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
       k_finish<<<1, kThreads, 0, s>>>(fa);
       QTT_CUDA_TRY(cudaGetLastError());
     }
-    launch_gemm_spec(Bf.spec + 2, io.cap[q + 1], n_cap, 1, 1, s);
+    launch_gemm_spec(Bf.spec + 2, io.cap[q + 1], n_cap, 1, 1, false, s);
     QTT_CUDA_TRY(cudaGetLastError());
   }
   return QTT_OK;
