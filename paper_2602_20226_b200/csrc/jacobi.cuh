@@ -19,6 +19,9 @@
 namespace qtt {
 
 constexpr int kJacobiMaxSweeps = 60;
+#ifndef QTT_JAC_UNROLL
+#define QTT_JAC_UNROLL 4
+#endif
 
 // Butterfly reduce-scatter: NV (power of two <= 32) per-lane partial sums -> lane l holds the
 // warp total of value index (l >> (5 - log2 NV)) in v[0].
@@ -71,25 +74,26 @@ __device__ __forceinline__ void warp_norms(const double (&X)[2 * WB][RPL], doubl
 //   MODE 1 (intra):  pairs (t, WB-1-t), (WB+t, 2WB-1-t), t < WB/2
 // The caller rotates registers between rounds so that these fixed slots walk through the
 // round-robin orderings.  slot_col[k] maps register slot k to its column's norm index.
-template <int WB, int MODE>
+template <int WB, int MODE, int SH = 0>
 __device__ __forceinline__ constexpr int slot_i(int a) {
-  return MODE == 0 ? a : (a < WB / 2 ? a : WB + (a - WB / 2));
+  return MODE != 1 ? a : (a < WB / 2 ? a : WB + (a - WB / 2));
 }
-template <int WB, int MODE>
+template <int WB, int MODE, int SH = 0>
 __device__ __forceinline__ constexpr int slot_j(int a) {
-  return MODE == 0 ? WB + a : (a < WB / 2 ? WB - 1 - a : 2 * WB - 1 - (a - WB / 2));
+  return MODE == 0 ? WB + (a + SH) % WB                 // cross round SH J positions further
+                   : (a < WB / 2 ? WB - 1 - a : 2 * WB - 1 - (a - WB / 2));
 }
 
-template <int RPL, int WB, int MODE>
+template <int RPL, int WB, int MODE, int SH = 0>
 __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm, const int *slot_col,
                                           double tol, int &rot) {
-  constexpr int NP = (MODE == 0) ? WB : 2 * (WB / 2);   // pairs in this round
+  constexpr int NP = (MODE != 1) ? WB : 2 * (WB / 2);   // pairs in this round
   constexpr int NV = (NP <= 4) ? 4 : (NP <= 8) ? 8 : (NP <= 16) ? 16 : 32;
   const int lane = threadIdx.x & 31;
   double v[NV];
 #pragma unroll
   for (int a = 0; a < NP; ++a) {
-    const int i = slot_i<WB, MODE>(a), j = slot_j<WB, MODE>(a);
+    const int i = slot_i<WB, MODE, SH>(a), j = slot_j<WB, MODE, SH>(a);
     double g0 = 0.0, g1 = 0.0;
 #pragma unroll
     for (int t = 0; t < RPL; t += 2) {
@@ -107,7 +111,7 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm,
   int si = 0, sj = 0;
 #pragma unroll
   for (int k = 0; k < NP; ++k)
-    if (a == k) { si = slot_i<WB, MODE>(k); sj = slot_j<WB, MODE>(k); }
+    if (a == k) { si = slot_i<WB, MODE, SH>(k); sj = slot_j<WB, MODE, SH>(k); }
   const int ci = slot_col[si], cj = slot_col[sj];
   const double al = nrm[ci], be = nrm[cj];
   // Rotation angle (Rutishauser): t = sign(d) 2g / (|d| + sqrt(d^2 + 4g^2)), d = b - a;
@@ -129,7 +133,7 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm,
   if (lane < NP) { nrm[ci] = al2; nrm[cj] = be2; }
 #pragma unroll
   for (int a2 = 0; a2 < NP; ++a2) {
-    const int i = slot_i<WB, MODE>(a2), j = slot_j<WB, MODE>(a2);
+    const int i = slot_i<WB, MODE, SH>(a2), j = slot_j<WB, MODE, SH>(a2);
     const double ca = __shfl_sync(0xffffffffu, c, a2), sa = __shfl_sync(0xffffffffu, s, a2);
 #pragma unroll
     for (int tt = 0; tt < RPL; ++tt) {
@@ -142,24 +146,38 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm,
   if (__any_sync(0xffffffffu, collapse)) warp_norms<RPL, WB>(X, nrm, slot_col);   // refresh exactly
 }
 
-// Register rotations that advance the fixed-slot pairings to the next round-robin round.
-template <int RPL, int WB>
-__device__ __forceinline__ void rotate_J(double (&X)[2 * WB][RPL], int *slot_col) {
-  // slot WB+a <- slot WB+(a+1)%WB  (cross rounds: J walks past I)
+// Shift the J block by S positions at once (after S fixed-slot cross rounds with shifts
+// 0..S-1): each register moves once per S rounds.
+template <int RPL, int WB, int S>
+__device__ __forceinline__ void rotate_Jn(double (&X)[2 * WB][RPL], int *slot_col) {
 #pragma unroll
   for (int t = 0; t < RPL; ++t) {
-    const double first = X[WB][t];
+    double f[S];
 #pragma unroll
-    for (int a = 0; a < WB - 1; ++a) X[WB + a][t] = X[WB + a + 1][t];
-    X[2 * WB - 1][t] = first;
+    for (int e = 0; e < S; ++e) f[e] = X[WB + e][t];
+#pragma unroll
+    for (int a = 0; a < WB - S; ++a) X[WB + a][t] = X[WB + a + S][t];
+#pragma unroll
+    for (int e = 0; e < S; ++e) X[2 * WB - S + e][t] = f[e];
   }
   if ((threadIdx.x & 31) == 0) {
-    const int f = slot_col[WB];
-    for (int a = 0; a < WB - 1; ++a) slot_col[WB + a] = slot_col[WB + a + 1];
-    slot_col[2 * WB - 1] = f;
+    int f[S];
+    for (int e = 0; e < S; ++e) f[e] = slot_col[WB + e];
+    for (int a = 0; a < WB - S; ++a) slot_col[WB + a] = slot_col[WB + a + S];
+    for (int e = 0; e < S; ++e) slot_col[2 * WB - S + e] = f[e];
   }
   __syncwarp();
 }
+
+template <int RPL, int WB, int SH, int U>
+__device__ __forceinline__ void cross_rounds(double (&X)[2 * WB][RPL], double *nrm, const int *slot_col, double tol,
+                                             int &rot) {
+  if constexpr (SH < U) {
+    jac_round<RPL, WB, 0, SH>(X, nrm, slot_col, tol, rot);
+    cross_rounds<RPL, WB, SH + 1, U>(X, nrm, slot_col, tol, rot);
+  }
+}
+
 template <int RPL, int WB>
 __device__ __forceinline__ void rotate_circle(double (&X)[2 * WB][RPL], int *slot_col) {
   // circle method inside each block: position 0 fixed, positions 1..WB-1 rotate by one
@@ -221,10 +239,13 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
           }
         }
       }
+      {  // WB cross rounds: QTT_JAC_UNROLL fixed-slot rounds per register rotation
+        constexpr int U = (WB < QTT_JAC_UNROLL) ? WB : QTT_JAC_UNROLL;
 #pragma unroll 1
-      for (int u = 0; u < WB; ++u) {
-        jac_round<RPL, WB, 0>(X, nrm, slot_col, tol, rot);
-        if (WB > 1) rotate_J<RPL, WB>(X, slot_col);
+        for (int u = 0; u < WB; u += U) {
+          cross_rounds<RPL, WB, 0, U>(X, nrm, slot_col, tol, rot);
+          if constexpr (U < WB) rotate_Jn<RPL, WB, U>(X, slot_col);
+        }
       }
       // slots are back in natural order (WB-1 circle rotations and WB J rotations = identity)
 #pragma unroll
