@@ -177,6 +177,19 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def dram_traffic(workload, members):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel per launch, from the
+    committed ncu --set full capture (profiles/traffic.json, bytes per member), scaled to this
+    launch's member count; None when no capture exists for the workload."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f).get(workload)
+    except (OSError, ValueError):
+        return None
+    return None if not t else round(t["bytes_per_member"] * members)
+
+
 # ----------------------------------------------------------------------------- CPU oracle leg
 
 def oracle_sample(kind, probs, n_members):
@@ -274,8 +287,9 @@ def main():
     ranks = res.ranks.cpu().numpy()
     sweeps = res.sweeps.cpu().numpy()
     cyc = res.cycles.cpu().numpy().astype(np.float64).sum(axis=(0, 1))
-    phase_share = {k: round(float(v / cyc.sum()), 4) for k, v in
-                   zip(("a2_contract", "a3_qr", "a4_jacobi", "a5_a6_trunc_emit_carry"), cyc)}
+    phase_share = None if not cyc.sum() > 0 else {      # the large-member path has no phase counters
+        k: round(float(v / cyc.sum()), 4) for k, v in
+        zip(("a2_contract", "a3_qr", "a4_jacobi", "a5_a6_trunc_emit_carry"), cyc)}
     d = xd.d_out if kind != "matvec" else od.d_out
     dj = xd.d_out
     tot = np.zeros(4)
@@ -291,6 +305,7 @@ def main():
 
     units = world * B * L
     value = units / (ms_max * 1e-3)
+    traffic = dram_traffic(args.workload, B)
 
     # ---------------- e2e through the public API with host buffers
     e2e = None
@@ -358,7 +373,7 @@ def main():
             "alg_tflops_note": "contraction+QR+carry flops (SURVEY.md §8(d)); Jacobi excluded",
             "roofline": {"kernel": "k_sweep (persistent a2-a7 over all sites and members; Jacobi-dominated)", "bound": "fp64",
                          "achieved": round(achieved, 3), "peak": fp64_peak, "unit": "TFLOP/s",
-                         "frac": round(achieved / fp64_peak, 4), "traffic": None,
+                         "frac": round(achieved / fp64_peak, 4), "traffic": traffic,
                          "peak_source": "measured in this run by csrc/probe/peak.cu (MEASURED_PEAKS.json has no FP64)",
                          "flops_per_step": flops_all, "kernel_ms_per_step": round(site_ms / args.steps, 3),
                          "share_of_step": round(site_ms / args.steps / ms, 4),

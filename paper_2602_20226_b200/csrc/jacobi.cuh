@@ -19,6 +19,25 @@
 namespace qtt {
 
 constexpr int kJacobiMaxSweeps = 60;
+#ifndef QTT_JAC_PROFILE
+#define QTT_JAC_PROFILE 0
+#endif
+#if QTT_JAC_PROFILE
+// diagnostics build only: cycles per jac_round phase summed over warp 0 of every CTA
+// [0] dots + reduce-scatter, [1] rotation parameters, [2] rotation, [3] rounds
+__device__ unsigned long long g_jprof[4];
+#define QTT_JPROF_T(v) const long long v = clock64()
+#define QTT_JPROF_ADD(i, d) if (threadIdx.x == 0) atomicAdd(&g_jprof[i], (unsigned long long)(d))
+#else
+#define QTT_JPROF_T(v)
+#define QTT_JPROF_ADD(i, d)
+#endif
+#ifndef QTT_JAC_STAGGER
+#define QTT_JAC_STAGGER 0
+#endif
+#ifndef QTT_JAC_SCALED
+#define QTT_JAC_SCALED 0
+#endif
 #ifndef QTT_JAC_UNROLL
 #define QTT_JAC_UNROLL 4
 #endif
@@ -49,7 +68,8 @@ __host__ __device__ constexpr int ilog2() { return N <= 1 ? 0 : 1 + ilog2<N / 2>
 
 // Exact squared norms of the warp's 2*WB register columns -> nrm[0..2WB) (shared, per warp).
 template <int RPL, int WB>
-__device__ __forceinline__ void warp_norms(const double (&X)[2 * WB][RPL], double *nrm, const int *slot_col) {
+__device__ __forceinline__ void warp_norms(const double (&X)[2 * WB][RPL], double *nrm, const double *dsc,
+                                           const int *slot_col) {
   constexpr int NC = 2 * WB;
   constexpr int NV = (NC <= 4) ? 4 : (NC <= 8) ? 8 : (NC <= 16) ? 16 : 32;
   const int lane = threadIdx.x & 31;
@@ -65,7 +85,14 @@ __device__ __forceinline__ void warp_norms(const double (&X)[2 * WB][RPL], doubl
   for (int k = NC; k < NV; ++k) v[k] = 0.0;
   halve<NV, 16, NV>(v, lane);
   constexpr int sh = 5 - ilog2<NV>();
-  if ((lane & ((1 << sh) - 1)) == 0 && (lane >> sh) < NC) nrm[slot_col[lane >> sh]] = v[0];
+  if ((lane & ((1 << sh) - 1)) == 0 && (lane >> sh) < NC) {
+    const int col = slot_col[lane >> sh];
+#if QTT_JAC_SCALED
+    nrm[col] = v[0] * (dsc[col] * dsc[col]);
+#else
+    nrm[col] = v[0];
+#endif
+  }
   __syncwarp();
 }
 
@@ -85,11 +112,12 @@ __device__ __forceinline__ constexpr int slot_j(int a) {
 }
 
 template <int RPL, int WB, int MODE, int SH = 0>
-__device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm, const int *slot_col,
-                                          double tol, int &rot) {
+__device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm, double *dsc, double *esc,
+                                          const int *slot_col, double tol, int &rot) {
   constexpr int NP = (MODE != 1) ? WB : 2 * (WB / 2);   // pairs in this round
   constexpr int NV = (NP <= 4) ? 4 : (NP <= 8) ? 8 : (NP <= 16) ? 16 : 32;
   const int lane = threadIdx.x & 31;
+  QTT_JPROF_T(jt0);
   double v[NV];
 #pragma unroll
   for (int a = 0; a < NP; ++a) {
@@ -107,13 +135,19 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm,
   halve<NV, 16, NV>(v, lane);
   constexpr int sh = 5 - ilog2<NV>();
   const int a = lane % NP;
-  const double ga = __shfl_sync(0xffffffffu, v[0], a << sh);
   int si = 0, sj = 0;
 #pragma unroll
   for (int k = 0; k < NP; ++k)
     if (a == k) { si = slot_i<WB, MODE, SH>(k); sj = slot_j<WB, MODE, SH>(k); }
   const int ci = slot_col[si], cj = slot_col[sj];
   const double al = nrm[ci], be = nrm[cj];
+#if QTT_JAC_SCALED
+  const double di = dsc[ci], dj = dsc[cj], ei = esc[ci], ej = esc[cj];
+  const double ga = __shfl_sync(0xffffffffu, v[0], a << sh) * (di * dj);   // true a_i . a_j
+#else
+  const double ga = __shfl_sync(0xffffffffu, v[0], a << sh);
+#endif
+  QTT_JPROF_T(jt1);
   // Rotation angle (Rutishauser): t = sign(d) 2g / (|d| + sqrt(d^2 + 4g^2)), d = b - a;
   // c = 1/sqrt(1+t^2), s = c t.  Rotate only if |g| > tol sqrt(a b) (squared test).
   const double d = be - al;
@@ -130,6 +164,29 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm,
   const bool collapse = doit && (al2 < 1.5e-8 * al || be2 < 1.5e-8 * be);
   if (__any_sync(0xffffffffu, doit)) rot = 1;
   __syncwarp();
+  QTT_JPROF_T(jt2);
+#if QTT_JAC_SCALED
+  // scaled (Anda-Park) rotation: true column = dsc * register column; the register columns
+  // take X_i -= t (d_j/d_i) X_j, X_j += t (d_i/d_j) X_i and the scales take the cosine
+  const double z = fma(t, t, 1.0) * c;                 // 1/c
+  const double t1 = t * (dj * ei), t2 = t * (di * ej);
+  if (lane < NP) {
+    nrm[ci] = al2; nrm[cj] = be2;
+    dsc[ci] = di * c; dsc[cj] = dj * c; esc[ci] = ei * z; esc[cj] = ej * z;
+  }
+  (void)s;
+#pragma unroll
+  for (int a2 = 0; a2 < NP; ++a2) {
+    const int i = slot_i<WB, MODE, SH>(a2), j = slot_j<WB, MODE, SH>(a2);
+    const double u1 = __shfl_sync(0xffffffffu, t1, a2), u2 = __shfl_sync(0xffffffffu, t2, a2);
+#pragma unroll
+    for (int tt = 0; tt < RPL; ++tt) {
+      const double x = X[i][tt], y = X[j][tt];
+      X[i][tt] = fma(-u1, y, x);
+      X[j][tt] = fma(u2, x, y);
+    }
+  }
+#else
   if (lane < NP) { nrm[ci] = al2; nrm[cj] = be2; }
 #pragma unroll
   for (int a2 = 0; a2 < NP; ++a2) {
@@ -142,8 +199,11 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm,
       X[j][tt] = fma(sa, x, ca * y);
     }
   }
+#endif
   __syncwarp();
-  if (__any_sync(0xffffffffu, collapse)) warp_norms<RPL, WB>(X, nrm, slot_col);   // refresh exactly
+  QTT_JPROF_T(jt3);
+  QTT_JPROF_ADD(0, jt1 - jt0); QTT_JPROF_ADD(1, jt2 - jt1); QTT_JPROF_ADD(2, jt3 - jt2); QTT_JPROF_ADD(3, 1);
+  if (__any_sync(0xffffffffu, collapse)) warp_norms<RPL, WB>(X, nrm, dsc, slot_col);   // refresh exactly
 }
 
 // Shift the J block by S positions at once (after S fixed-slot cross rounds with shifts
@@ -170,11 +230,11 @@ __device__ __forceinline__ void rotate_Jn(double (&X)[2 * WB][RPL], int *slot_co
 }
 
 template <int RPL, int WB, int SH, int U>
-__device__ __forceinline__ void cross_rounds(double (&X)[2 * WB][RPL], double *nrm, const int *slot_col, double tol,
-                                             int &rot) {
+__device__ __forceinline__ void cross_rounds(double (&X)[2 * WB][RPL], double *nrm, double *dsc, double *esc,
+                                             const int *slot_col, double tol, int &rot) {
   if constexpr (SH < U) {
-    jac_round<RPL, WB, 0, SH>(X, nrm, slot_col, tol, rot);
-    cross_rounds<RPL, WB, SH + 1, U>(X, nrm, slot_col, tol, rot);
+    jac_round<RPL, WB, 0, SH>(X, nrm, dsc, esc, slot_col, tol, rot);
+    cross_rounds<RPL, WB, SH + 1, U>(X, nrm, dsc, esc, slot_col, tol, rot);
   }
 }
 
@@ -211,7 +271,9 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
   const double tol = (double)max(m, 1) * DBL_EPSILON;
   double X[2 * WB][RPL];
   double *nrm = scratch + warp * 2 * WB;                                   // norms by local column
-  int *slot_col = reinterpret_cast<int *>(scratch + NW * 2 * WB) + warp * 2 * WB;
+  double *dsc = scratch + NW * 2 * WB + warp * 2 * WB;                     // column scales (scaled rotations)
+  double *esc = scratch + NW * 4 * WB + warp * 2 * WB;                     // 1 / column scales
+  int *slot_col = reinterpret_cast<int *>(scratch + NW * 6 * WB) + warp * 2 * WB;
   int sweep = 0;
   for (; sweep < kJacobiMaxSweeps; ++sweep) {
     int rot = 0;
@@ -227,14 +289,20 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
           X[c][t] = A[(size_t)(I * WB + c) * kLdA + lane + 32 * t];
           X[WB + c][t] = A[(size_t)(J * WB + c) * kLdA + lane + 32 * t];
         }
-      if (lane < 2 * WB) slot_col[lane] = lane;
+      if (lane < 2 * WB) { slot_col[lane] = lane; dsc[lane] = 1.0; esc[lane] = 1.0; }
       __syncwarp();
-      warp_norms<RPL, WB>(X, nrm, slot_col);
+      warp_norms<RPL, WB>(X, nrm, dsc, slot_col);
+#if QTT_JAC_STAGGER
+      if (warp >= NW / 2) {      // experiment: offset the two warps of each SM sub-partition
+        const long long t0 = clock64();
+        while (clock64() - t0 < QTT_JAC_STAGGER) { }
+      }
+#endif
       if constexpr (WB > 1) {
         if (r == 0) {
 #pragma unroll 1
           for (int u = 0; u < WB - 1; ++u) {
-            jac_round<RPL, WB, 1>(X, nrm, slot_col, tol, rot);
+            jac_round<RPL, WB, 1>(X, nrm, dsc, esc, slot_col, tol, rot);
             rotate_circle<RPL, WB>(X, slot_col);
           }
         }
@@ -243,18 +311,24 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
         constexpr int U = (WB < QTT_JAC_UNROLL) ? WB : QTT_JAC_UNROLL;
 #pragma unroll 1
         for (int u = 0; u < WB; u += U) {
-          cross_rounds<RPL, WB, 0, U>(X, nrm, slot_col, tol, rot);
+          cross_rounds<RPL, WB, 0, U>(X, nrm, dsc, esc, slot_col, tol, rot);
           if constexpr (U < WB) rotate_Jn<RPL, WB, U>(X, slot_col);
         }
       }
       // slots are back in natural order (WB-1 circle rotations and WB J rotations = identity)
 #pragma unroll
-      for (int c = 0; c < WB; ++c)
+      for (int c = 0; c < WB; ++c) {
+#if QTT_JAC_SCALED
+        const double dI = dsc[c], dJ = dsc[WB + c];      // fold the column scales in
+#else
+        const double dI = 1.0, dJ = 1.0;
+#endif
 #pragma unroll
         for (int t = 0; t < RPL; ++t) {
-          A[(size_t)(I * WB + c) * kLdA + lane + 32 * t] = X[c][t];
-          A[(size_t)(J * WB + c) * kLdA + lane + 32 * t] = X[WB + c][t];
+          A[(size_t)(I * WB + c) * kLdA + lane + 32 * t] = X[c][t] * dI;
+          A[(size_t)(J * WB + c) * kLdA + lane + 32 * t] = X[WB + c][t] * dJ;
         }
+      }
       __syncthreads();
     }
     if (threadIdx.x == 0) *flag = 0;

@@ -89,3 +89,47 @@ extern "C" int qtt_probe_latency(double *out, int iters, void *stream) {
   k_approx_err<<<64, 256, 0, (cudaStream_t)stream>>>(out + 8, 1 << 22);
   return (int)cudaGetLastError();
 }
+
+// Throughput probes: 8 warps (one CTA per SM, grid = #SMs), each issuing independent
+// 32-bit SHFL (8 chains) or broadcast LDS.64 (8 chains); out[0] = cycles per SHFL per SM,
+// out[1] = cycles per LDS per SM (SM-wide: total instructions issued by the 8 warps).
+__global__ void __launch_bounds__(256, 1) k_tput(double *out, int iters) {
+  __shared__ double sm[256];
+  sm[threadIdx.x] = threadIdx.x;
+  __syncthreads();
+  int r[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r[i] = threadIdx.x + i;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r[i] = __shfl_xor_sync(0xffffffffu, r[i], 1 + (i & 3));
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  double acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+  const int base = (threadIdx.x >> 5) * 8;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] += sm[(base + i + it) & 255];
+  }
+  __syncthreads();
+  long long t2 = clock64();
+  int s = 0;
+  double a = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { s += r[i]; a += acc[i]; }
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    out[0] = (double)(t1 - t0) / (iters * 8.0 * 8.0);
+    out[1] = (double)(t2 - t1) / (iters * 8.0 * 8.0);
+    out[2] = s + a;
+  }
+}
+
+extern "C" int qtt_probe_tput(double *out, int iters, int blocks, void *stream) {
+  k_tput<<<blocks, 256, 0, (cudaStream_t)stream>>>(out, iters);
+  return (int)cudaGetLastError();
+}

@@ -818,6 +818,15 @@ static WsLayout layout(const Shape &S) {
 
 using namespace qtt;
 
+#if QTT_JAC_PROFILE
+extern "C" int qtt_debug_jprof(unsigned long long *host, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host, qtt::g_jprof, sizeof(unsigned long long) * 4);
+  if (reset) { unsigned long long z[4] = {0, 0, 0, 0}; cudaMemcpyToSymbol(qtt::g_jprof, z, sizeof(z)); }
+  return 0;
+}
+#endif
+
 extern "C" {
 
 const char *qtt_last_error(void) { return qtt::g_err; }

@@ -12,3 +12,9 @@ torch.cuda.synchronize()
 v = out.cpu().tolist()
 print({"dfma": v[0], "shfl64": v[1], "rsqrt_approx": v[2], "rcp_approx": v[3], "lds64_chase": v[4], "dadd": v[5],
        "rsqrt_approx_max_rel_err": v[8], "rcp_approx_max_rel_err": v[9]})
+out.zero_()
+for _ in range(2):
+    lib.qtt_probe_tput(ctypes.c_void_p(out.data_ptr()), 20000, 148, ctypes.c_void_p(s.cuda_stream))
+torch.cuda.synchronize()
+v = out.cpu().tolist()
+print({"shfl32_cycles_per_instr_per_SM": v[0], "lds64_bcast_cycles_per_instr_per_SM": v[1]})
