@@ -59,7 +59,11 @@ typedef struct {
   const int32_t *ranks;   /* host [L+1] bond dims (inputs) / bond capacities (outputs);
                              ranks[0] == ranks[L] == 1                                     */
   void *const *cores;     /* host [L] device pointers, batch-strided as described above    */
+  int32_t dtype;          /* element type of the cores: QTT_F64 (0, default) or QTT_F32 (1);
+                             QTT_F32 is accepted by qtt_zipup only (see there)              */
 } qtt_trains_t;
+
+enum { QTT_F64 = 0, QTT_F32 = 1 };
 
 /* Flags for qtt_zipup. */
 enum {
@@ -105,6 +109,14 @@ size_t qtt_zipup_workspace_bytes(const char *subscripts, const qtt_trains_t *op,
  *   status     : device int32 [1]: 0 on success; bit 1 = non-finite value seen,
  *                bit 2 = Jacobi did not converge (the host status cannot know: no sync).
  *   workspace  : device scratch of >= qtt_zipup_workspace_bytes bytes, 256-byte aligned.
+ *   fp32 variant (BASELINE.json configs[2] "fp64 and fp32", c-A27/A28):
+ *                when x, op and out all have dtype QTT_F32 the cores are IEEE binary32.  They
+ *                are widened into the workspace; the site contractions that run as large
+ *                GEMMs (large-member path: state GEMM, Hadamard apply, carry) execute as
+ *                3xTF32 on the 5th-generation tensor cores (tcgen05 kind::tf32, fp32
+ *                accumulation); QR, Jacobi SVD and truncation run in fp64; the output cores
+ *                are rounded to binary32.  Mixed dtypes return QTT_EINVAL.  Accuracy target:
+ *                relative Frobenius error <= 1e-4 + eps against the fp64 oracle (c-A28).
  */
 typedef struct {
   double *sigma;          /* device f64 [B*(L-1)*sigma_stride]: singular values of every site

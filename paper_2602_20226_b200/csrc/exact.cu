@@ -161,6 +161,7 @@ static long long core_elems(const qtt_trains_t *t, int q) {
 }
 
 static qtt_status_t check_train(const qtt_trains_t *t, const char *name) {
+  if (t && t->dtype != QTT_F64) { set_error("%s: dtype must be QTT_F64 for this call", name); return QTT_EUNSUPPORTED; }
   if (!t || !t->cores || !t->ranks || !t->d_out) { set_error("%s: NULL train", name); return QTT_EINVAL; }
   if (t->n_sites < 1 || t->n_sites > 64) { set_error("%s: n_sites outside [1,64]", name); return QTT_EUNSUPPORTED; }
   if (t->n_legs != 1 && t->n_legs != 2) { set_error("%s: n_legs must be 1 or 2", name); return QTT_EINVAL; }

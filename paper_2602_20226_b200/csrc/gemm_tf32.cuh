@@ -5,9 +5,12 @@
 //   C[z1,z2] (M x N, fp64 storage) = A[z1,z2] (M x K) * B[z1,z2] (K x N)
 //
 // Operands are read from fp64 storage, rounded to fp32 and split x = hi + lo with hi, lo
-// TF32 (cvt.rna.tf32.f32); the product is accumulated in fp32 as hi*hi + hi*lo + lo*hi (the
-// lo*lo term is below fp32 resolution), which restores ~fp32 accuracy on the TF32 tensor
-// pipe.  Same GemmSpec / grid conventions as gemm.cuh (strides and shapes in device memory,
+// TF32 (cvt.rna.tf32.f32); the product is hi*hi + hi*lo + lo*hi (the lo*lo term is below
+// fp32 resolution), which restores ~fp32 accuracy on the TF32 tensor pipe.  Four fp32 TMEM
+// accumulators (hi*hi and the two correction terms kept apart, each split by K-chunk
+// parity) are summed in fp64 in the epilogue: the small correction terms are not rounded
+// against the large hi*hi partial sums, and every accumulator sums half the K range.
+// Same GemmSpec / grid conventions as gemm.cuh (strides and shapes in device memory,
 // capacity-sized grid, surplus CTAs exit).
 //
 // CTA: 128 x 128 output tile, one tcgen05.mma.cta_group::1 M=128 N=128 K=8 per (k-step,
@@ -15,7 +18,8 @@
 // layouts (8 rows x 16 B cores; LBO = 128 B between K-adjacent cores, SBO = 1024 B between
 // 8-row groups), double-buffered; one thread issues the MMAs and commits them to the
 // buffer's mbarrier, so staging of chunk c+1 overlaps the MMAs of chunk c.  Epilogue: every
-// warp reads its TMEM lane quadrant (tcgen05.ld 32x32b) and writes fp64 C.
+// warp reads its TMEM lane quadrant of the four accumulators (tcgen05.ld 32x32b), sums them
+// in fp64 and writes fp64 C.
 #pragma once
 #include "gemm.cuh"
 
@@ -85,9 +89,9 @@ __global__ void __launch_bounds__(256, 1) k_gemm_tf32(const GemmSpec *spec, int 
   uint64_t *bars = reinterpret_cast<uint64_t *>(tsm + 2 * BUFB);   // [2]
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tsm + 2 * BUFB + 64);
 
-  if (warp == 0) {
+  if (warp == 0) {   // 4 accumulators x TN columns = all 512 TMEM columns (one CTA per SM)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TN));
+                 "r"(4 * TN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -163,11 +167,13 @@ __global__ void __launch_bounds__(256, 1) k_gemm_tf32(const GemmSpec *spec, int 
         const uint64_t da[3] = {dAh, dAh, dAl}, db[3] = {dBh, dBl, dBh};
 #pragma unroll
         for (int t = 0; t < 3; ++t) {
-          const uint32_t acc = (kc > 0 || s > 0 || t > 0) ? 1u : 0u;
+          // accumulator: (hi*hi | corrections) x (chunk parity); first use of each overwrites
+          const uint32_t slot = (t == 0 ? 0u : 1u) + 2u * (uint32_t)(kc & 1);
+          const uint32_t acc = (kc > 1 || s > 0 || t == 2) ? 1u : 0u;
           asm volatile(
               "{\n\t.reg .pred p;\n\t"
               "setp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + slot * TN),
               "l"(da[t]), "l"(db[t]), "r"(idesc), "r"(acc));
         }
       }
@@ -183,28 +189,37 @@ __global__ void __launch_bounds__(256, 1) k_gemm_tf32(const GemmSpec *spec, int 
   {
     const int q = warp & 3, half = warp >> 2;
     const int row = q * 32 + lane, gm = m0 + row;
-#pragma unroll
+#pragma unroll 1
     for (int cb = 0; cb < 64; cb += 16) {
-      uint32_t r[16];
-      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * 64 + cb);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      double sum[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) sum[e] = 0.0;
+#pragma unroll
+      for (int slot = 0; slot < 4; ++slot) {
+        if (slot >= 2 && nk < 2) break;               // odd-chunk accumulators never written
+        uint32_t r[16];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(slot * TN + half * 64 + cb);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int e = 0; e < 16; ++e) sum[e] += (double)__uint_as_float(r[e]);
+      }
       if (gm < g.M) {
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int gn = n0 + half * 64 + cb + e;
-          if (gn < g.N) C[(long long)gm * g.scm + (long long)gn * g.scn] = (double)__uint_as_float(r[e]);
+          if (gn < g.N) C[(long long)gm * g.scm + (long long)gn * g.scn] = sum[e];
         }
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TN));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(4 * TN));
 }
 
 }  // namespace qtt

@@ -25,6 +25,7 @@
 
 #include "large.cuh"
 #include "gemm.cuh"
+#include "gemm_tf32.cuh"
 
 namespace qtt {
 
@@ -118,7 +119,16 @@ __global__ void k_plan(PlanArgs a) {
 // DMMA GEMM (gemm.cuh) over capacity tiles; a_kcontig selects A's layout (row-major A,
 // sak == 1, vs. transposed views with sam == 1).
 static void launch_gemm_spec(const GemmSpec *spec, long long Mcap, long long Ncap, long long nz1cap, long long nz2cap,
-                             bool a_kcontig, cudaStream_t s) {
+                             bool a_kcontig, bool tf32, cudaStream_t s) {
+  if (tf32) {        // fp32 variant: 3xTF32 on tcgen05 (gemm_tf32.cuh)
+    const long long tm = (Mcap + tf32g::TM - 1) / tf32g::TM, tn = (Ncap + tf32g::TN - 1) / tf32g::TN;
+    dim3 grid((unsigned)(tm * tn), 1, (unsigned)(nz1cap * nz2cap));
+    if (a_kcontig)
+      k_gemm_tf32<true><<<grid, 256, tf32g::SMEM_BYTES, s>>>(spec, (int)tn, (int)nz2cap);
+    else
+      k_gemm_tf32<false><<<grid, 256, tf32g::SMEM_BYTES, s>>>(spec, (int)tn, (int)nz2cap);
+    return;
+  }
   const long long tm = (Mcap + dgemm::TM - 1) / dgemm::TM, tn = (Ncap + dgemm::TN - 1) / dgemm::TN;
   dim3 grid((unsigned)(tm * tn), 1, (unsigned)(nz1cap * nz2cap));
   if (a_kcontig)
@@ -702,6 +712,7 @@ struct SweepIO {
   int *sweeps, *status;
   double eps;
   int max_rank;
+  bool tf32 = false;                               // contraction GEMMs as 3xTF32 (fp32 variant)
 };
 
 static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, cudaStream_t s) {
@@ -721,6 +732,10 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
                                       (int)dgemm::SMEM_BYTES));
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_dmma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)dgemm::SMEM_BYTES));
+    QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_tf32<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)tf32g::SMEM_BYTES));
+    QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_tf32<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)tf32g::SMEM_BYTES));
     attr = true;
   }
   QTT_CUDA_TRY(cudaMemsetAsync(Bf.bar, 0, sizeof(GridBar) * 2, s));
@@ -741,14 +756,14 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
     // a2: state GEMM (M <= cap*w, N <= (dj|d)*r2)
     const long long g0M = (long long)io.cap[q] * w;
     const long long g0N = (long long)((kind == MATVEC) ? io.dj[q] : io.d[q]) * io.xcap_r[q + 1];
-    launch_gemm_spec(Bf.spec + 0, g0M, g0N, 1, 1, true, s);
+    launch_gemm_spec(Bf.spec + 0, g0M, g0N, 1, 1, true, io.tf32, s);
     QTT_CUDA_TRY(cudaGetLastError());
     const unsigned ew_grid = (unsigned)std::min<long long>((m_cap * n_cap + kThreads - 1) / kThreads, 8192);
     if (kind == MATVEC) {
       k_mpo_apply<<<ew_grid, kThreads, 0, s>>>(Bf.dims, Bf.X, io.Oq[q], Bf.T);
       QTT_CUDA_TRY(cudaGetLastError());
     } else if (kind == HADAMARD) {
-      launch_gemm_spec(Bf.spec + 1, w2, io.xcap_r[q + 1], io.cap[q], io.d[q], false, s);
+      launch_gemm_spec(Bf.spec + 1, w2, io.xcap_r[q + 1], io.cap[q], io.d[q], false, io.tf32, s);
       QTT_CUDA_TRY(cudaGetLastError());
     }
     if (q == L - 1) {                                                  // a7
@@ -786,7 +801,7 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
       k_finish<<<1, kThreads, 0, s>>>(fa);
       QTT_CUDA_TRY(cudaGetLastError());
     }
-    launch_gemm_spec(Bf.spec + 2, io.cap[q + 1], n_cap, 1, 1, false, s);
+    launch_gemm_spec(Bf.spec + 2, io.cap[q + 1], n_cap, 1, 1, false, io.tf32, s);
     QTT_CUDA_TRY(cudaGetLastError());
   }
   return QTT_OK;
@@ -986,6 +1001,7 @@ qtt_status_t large_zipup(const Shape &S, const qtt_trains_t *op, const qtt_train
   for (int b = 0; b < B; ++b) {
     SweepIO sw;
     sw.L = L; sw.kind = S.kind; sw.d = S.d; sw.dj = S.dj; sw.cap = S.cap; sw.xcap_r = S.xr; sw.ocap_r = S.orr;
+    sw.tf32 = (flags & (1u << 30)) != 0;        // fp32 variant (zipup.cu kFlagTF32)
     sw.Xq.resize(L); sw.Oq.resize(L); sw.Cq.resize(L);
     for (int q = 0; q < L; ++q) {
       sw.Xq[q] = Xo + (size_t)b * S.xo_elems + S.xoff[q];

@@ -138,6 +138,10 @@ size_t qtt_round_workspace_bytes(const qtt_trains_t *x, int32_t max_rank) {
 qtt_status_t qtt_round(const qtt_trains_t *x, const int32_t *x_ranks, double eps, int32_t max_rank,
                        const qtt_trains_t *out, int32_t *out_ranks, double *delta2, double *norm2,
                        int32_t *status, void *workspace, size_t workspace_bytes, void *stream) {
+  if ((x && x->dtype != QTT_F64) || (out && out->dtype != QTT_F64)) {
+    set_error("qtt_round: dtype must be QTT_F64");
+    return QTT_EUNSUPPORTED;
+  }
   RoundPlan P;
   qtt_status_t st = plan_round(x, max_rank, P);
   if (st != QTT_OK) return st;

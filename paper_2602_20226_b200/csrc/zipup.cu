@@ -814,6 +814,76 @@ static WsLayout layout(const Shape &S) {
   return w;
 }
 
+// ======================================================================= fp32 variant
+
+constexpr uint32_t kFlagTF32 = 1u << 30;     // internal: large-path contraction GEMMs as 3xTF32
+
+struct CvtArgs {
+  int L;
+  const void *src[kMaxSites];
+  void *dst[kMaxSites];
+  long long n[kMaxSites];
+};
+
+// binary32 <-> binary64 copies of every core of one train (blockIdx.y = site)
+template <bool TO64>
+__global__ void k_cvt(CvtArgs a) {
+  const int q = blockIdx.y;
+  if (q >= a.L) return;
+  const long long n = a.n[q];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    if (TO64) static_cast<double *>(a.dst[q])[i] = (double)static_cast<const float *>(a.src[q])[i];
+    else static_cast<float *>(a.dst[q])[i] = (float)static_cast<const double *>(a.src[q])[i];
+  }
+}
+
+static long long train_elems(const qtt_trains_t *t, int q) {
+  return (long long)t->batch * t->ranks[q] * t->d_out[q] * (t->n_legs == 2 ? t->d_in[q] : 1) * t->ranks[q + 1];
+}
+
+// fp64 views of (op, x, out) carved from the front of the workspace
+struct F32Stage {
+  std::vector<void *> xp, op, outp;
+  qtt_trains_t x64{}, op64{}, out64{};
+  size_t bytes = 0;
+};
+
+static void f32_stage(const qtt_trains_t *op, const qtt_trains_t *x, const qtt_trains_t *out, char *ws, F32Stage &F) {
+  size_t off = 0;
+  auto take = [&](long long n) { void *p = ws ? (void *)(ws + off) : nullptr; off += ((size_t)n * 8 + 255) & ~size_t(255); return p; };
+  const int L = x->n_sites;
+  F.xp.resize(L); F.outp.resize(L);
+  for (int q = 0; q < L; ++q) F.xp[q] = take(train_elems(x, q));
+  if (op) { F.op.resize(L); for (int q = 0; q < L; ++q) F.op[q] = take(train_elems(op, q)); }
+  if (out) for (int q = 0; q < L; ++q) F.outp[q] = take(train_elems(out, q));
+  F.x64 = *x; F.x64.cores = F.xp.data(); F.x64.dtype = QTT_F64;
+  if (op) { F.op64 = *op; F.op64.cores = F.op.data(); F.op64.dtype = QTT_F64; }
+  if (out) { F.out64 = *out; F.out64.cores = F.outp.data(); F.out64.dtype = QTT_F64; }
+  F.bytes = off;
+}
+
+static qtt_status_t cvt_train(const qtt_trains_t *t, void *const *src, void *const *dst, bool to64, cudaStream_t s) {
+  CvtArgs a;
+  memset(&a, 0, sizeof(a));
+  a.L = t->n_sites;
+  long long mx = 1;
+  for (int q = 0; q < a.L; ++q) { a.src[q] = src[q]; a.dst[q] = dst[q]; a.n[q] = train_elems(t, q); mx = std::max(mx, a.n[q]); }
+  dim3 grid((unsigned)std::min<long long>((mx + 255) / 256, 1024), (unsigned)a.L);
+  if (to64) k_cvt<true><<<grid, 256, 0, s>>>(a);
+  else k_cvt<false><<<grid, 256, 0, s>>>(a);
+  QTT_CUDA_TRY(cudaGetLastError());
+  return QTT_OK;
+}
+
+// -1: not all fp64 and not all fp32 (error), 0: fp64, 1: fp32
+static int train_dtypes(const qtt_trains_t *op, const qtt_trains_t *x, const qtt_trains_t *out) {
+  const int dx = x ? x->dtype : QTT_F64;
+  const int dop = op ? op->dtype : dx, dout = out ? out->dtype : dx;
+  if (dx == QTT_F64 && dop == QTT_F64 && dout == QTT_F64) return 0;
+  if (dx == QTT_F32 && dop == QTT_F32 && dout == QTT_F32) return 1;
+  return -1;
+}
+
 }  // namespace qtt
 
 using namespace qtt;
@@ -844,6 +914,16 @@ qtt_status_t qtt_zipup_capacity(const char *subscripts, const qtt_trains_t *op, 
 
 size_t qtt_zipup_workspace_bytes(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
                                  const qtt_trains_t *out) {
+  {
+    const int dt = train_dtypes(op, x, out);
+    if (dt < 0) { set_error("mixed dtypes: x, op and out must all be QTT_F64 or all QTT_F32"); return 0; }
+    if (dt == 1) {                 // fp32 variant: fp64 staging of all three trains + the fp64 workspace
+      F32Stage F;
+      f32_stage(op, x, out, nullptr, F);
+      const size_t inner = qtt_zipup_workspace_bytes(subscripts, op ? &F.op64 : nullptr, &F.x64, out ? &F.out64 : nullptr);
+      return inner ? F.bytes + inner : 0;
+    }
+  }
   // the output capacities the caller will pass bound the zip-up ranks (max_rank)
   int mr = 0;
   if (out && out->ranks && x)
@@ -865,6 +945,26 @@ qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt
   long long *cycles = diag ? (long long *)diag->phase_cycles : nullptr;
   g_err[0] = 0;
   if (!(eps >= 0.0 && eps < 1.0)) { set_error("eps %g outside [0,1)", eps); return QTT_EINVAL; }
+  {
+    const int dt = train_dtypes(op, x, out);
+    if (dt < 0) { set_error("mixed dtypes: x, op and out must all be QTT_F64 or all QTT_F32"); return QTT_EINVAL; }
+    if (dt == 1) {                 // fp32 variant (see qtt.h): widen, run with TF32 GEMMs, narrow
+      if (!x || !out || !x->cores || !out->cores) { set_error("NULL train"); return QTT_EINVAL; }
+      if (!workspace) { set_error("workspace is NULL"); return QTT_EINVAL; }
+      F32Stage F;
+      f32_stage(op, x, out, (char *)workspace, F);
+      if (workspace_bytes < F.bytes) { set_error("workspace too small for the fp32 staging"); return QTT_ECAPACITY; }
+      cudaStream_t s = (cudaStream_t)stream;
+      qtt_status_t st = cvt_train(x, x->cores, F.xp.data(), true, s);
+      if (st == QTT_OK && op) st = cvt_train(op, op->cores, F.op.data(), true, s);
+      if (st != QTT_OK) return st;
+      st = qtt_zipup(subscripts, op ? &F.op64 : nullptr, &F.x64, eps, max_rank, flags | kFlagTF32, &F.out64,
+                     out_ranks, delta2, norm2, status, diag, (char *)workspace + F.bytes, workspace_bytes - F.bytes,
+                     stream);
+      if (st != QTT_OK) return st;
+      return cvt_train(out, F.outp.data(), out->cores, false, s);
+    }
+  }
   Shape S;
   qtt_status_t st = analyse(subscripts, op, x, max_rank, S);
   if (st != QTT_OK) return st;

@@ -38,7 +38,10 @@ class _Diag(ctypes.Structure):
 class _Trains(ctypes.Structure):
     _fields_ = [("n_sites", ctypes.c_int32), ("n_legs", ctypes.c_int32), ("batch", ctypes.c_int32),
                 ("d_out", ctypes.POINTER(ctypes.c_int32)), ("d_in", ctypes.POINTER(ctypes.c_int32)),
-                ("ranks", ctypes.POINTER(ctypes.c_int32)), ("cores", ctypes.POINTER(ctypes.c_void_p))]
+                ("ranks", ctypes.POINTER(ctypes.c_int32)), ("cores", ctypes.POINTER(ctypes.c_void_p)),
+                ("dtype", ctypes.c_int32)]
+
+QTT_F64, QTT_F32 = 0, 1
 
 
 _lib = None
@@ -126,6 +129,10 @@ class DeviceTrains:
     def batch(self) -> int:
         return int(self.cores[0].shape[0])
 
+    @property
+    def dtype_code(self) -> int:
+        return QTT_F32 if self.cores[0].dtype == torch.float32 else QTT_F64
+
     def c_struct(self):
         L = self.n_sites
         keep = []
@@ -136,16 +143,18 @@ class DeviceTrains:
         keep += [d_out, d_in, ranks, ptrs]
         s = _Trains(L, self.n_legs, self.batch, d_out,
                     ctypes.cast(d_in, ctypes.POINTER(ctypes.c_int32)) if d_in is not None else None,
-                    ranks, ptrs)
+                    ranks, ptrs, self.dtype_code)
         return s, keep
 
 
-def to_device(cores_per_site: Sequence[np.ndarray], device="cuda", mpo: bool = False) -> DeviceTrains:
+def to_device(cores_per_site: Sequence[np.ndarray], device="cuda", mpo: bool = False,
+              dtype=np.float64) -> DeviceTrains:
     """Upload batch-stacked numpy cores: cores_per_site[q] has shape (B, r, d, r') (MPS)
-    or (B, w, d_out, d_in, w') (MPO).  Single trains may be given without the batch axis."""
+    or (B, w, d_out, d_in, w') (MPO).  Single trains may be given without the batch axis.
+    dtype np.float32 gives QTT_F32 trains (the fp32 variant of qtt_zipup)."""
     cs = []
     for c in cores_per_site:
-        c = np.asarray(c, dtype=np.float64)
+        c = np.asarray(c, dtype=dtype)
         want = 5 if mpo else 4
         if c.ndim == want - 1:
             c = c[None]
@@ -156,8 +165,9 @@ def to_device(cores_per_site: Sequence[np.ndarray], device="cuda", mpo: bool = F
     return DeviceTrains(cs, ranks, d_out, d_in)
 
 
-def empty_like_capacity(batch: int, d_out: Sequence[int], cap: Sequence[int], device="cuda") -> DeviceTrains:
-    cores = [torch.zeros((batch, cap[q], d_out[q], cap[q + 1]), dtype=torch.float64, device=device)
+def empty_like_capacity(batch: int, d_out: Sequence[int], cap: Sequence[int], device="cuda",
+                        dtype=torch.float64) -> DeviceTrains:
+    cores = [torch.zeros((batch, cap[q], d_out[q], cap[q + 1]), dtype=dtype, device=device)
              for q in range(len(d_out))]
     return DeviceTrains(cores, list(cap), list(d_out), None)
 
@@ -168,7 +178,7 @@ def member_cores(t: DeviceTrains, ranks: Sequence[int], b: int) -> List[np.ndarr
     for q, c in enumerate(t.cores):
         n = ranks[q] * t.d_out[q] * ranks[q + 1]
         flat = c[b].reshape(-1)[:n]
-        out.append(flat.cpu().numpy().reshape(ranks[q], t.d_out[q], ranks[q + 1]))
+        out.append(flat.cpu().double().numpy().reshape(ranks[q], t.d_out[q], ranks[q + 1]))
     return out
 
 
@@ -211,7 +221,7 @@ class ZipupPlan:
         d_out = op.d_out if (op is not None and subscripts == "ij,j->i") else x.d_out
         self.cap = capacity(subscripts, op, x, max_rank)
         B, L = x.batch, x.n_sites
-        self.out = empty_like_capacity(B, d_out, self.cap, device)
+        self.out = empty_like_capacity(B, d_out, self.cap, device, dtype=x.cores[0].dtype)
         self.ranks = torch.zeros((B, L + 1), dtype=torch.int32, device=device)
         self.delta2 = torch.zeros((B, L), dtype=torch.float64, device=device)
         self.norm2 = torch.zeros((B,), dtype=torch.float64, device=device)

@@ -36,5 +36,6 @@ def test_gemm_kernels(probe, kind, M, N, K, akc):
     ref = A @ B
     scale = (A.abs() @ B.abs()).max().item()
     err = (C - ref).abs().max().item() / scale
-    tol = 1e-14 * K if kind == 0 else 2e-6           # fp64 rounding / 3xTF32 ~ fp32 accuracy
+    tol = 1e-14 * K if kind == 0 else 5e-7           # fp64 rounding / 3xTF32 (measured <= 1.7e-7)
+    print(f"kind {kind} M{M} N{N} K{K} err {err:.3e}")
     assert err <= tol, (kind, err)

@@ -48,24 +48,16 @@ def test_cfg4_full(lib):
     check(lib, "matvec", p.op.cores, p.x.cores, p.eps, p.max_rank, dense=False)
 
 
-def test_cfg3_full_shape_known_answer(lib):
-    """configs[2] at full shape (L=30, both operands rank 256, max rank 256): with the second
-    operand the constant 1 written as a redundant rank-256 train (block sum of 256 rank-1
-    trains, each 1/256), a o 1 = a exactly, so the zip-up must return a (rank <= 256) --
-    exercising the 512 x 65536 site matrices of the cfg3 path with a closed-form answer."""
-    import torch
+def _redundant_ones(L, R):
+    """The constant 1 written as a redundant rank-R train (block sum of R rank-1 trains, each
+    1/R per bond), mixed through random orthogonal gauges so nothing is block-diagonal."""
     from oracle import tt
-    L, R = 30, 256
-    a = gen.random_mps([2] * L, R, gen.rng_for(3, 0, 0), 1.0 / math.sqrt(R)).cores
     ranks = gen.clipped_ranks([2] * L, R)
     rng = np.random.default_rng(7)
-    # redundant representation of the constant 1: cores mix identical rank-1 pieces through
-    # random orthogonal gauges (so nothing is trivially block-diagonal)
     ones = []
     for q in range(L):
         r0, r1 = ranks[q], ranks[q + 1]
         core = np.zeros((r0, 2, r1))
-        core[:, :, :] = 0.0
         u = np.ones(r0) / math.sqrt(r0) if q > 0 else np.ones(1)
         v = np.ones(r1) / math.sqrt(r1) if q < L - 1 else np.ones(1)
         for i in range(2):
@@ -75,11 +67,24 @@ def test_cfg3_full_shape_known_answer(lib):
             core = np.einsum("ab,bic->aic", Q.T, core)
             ones[-1] = np.einsum("aib,bc->aic", ones[-1], Q)
         ones.append(core)
-    # normalise so the represented tensor is exactly 1 (check on samples below)
+    # normalise so the represented tensor is exactly 1 (checked on samples)
     dig = np.random.default_rng(8).integers(0, 2, size=(64, L))
     s = tt.evaluate(ones, dig)
     ones[0] = ones[0] / s[0]
     np.testing.assert_allclose(tt.evaluate(ones, dig), 1.0, rtol=1e-10)
+    return ones
+
+
+def test_cfg3_full_shape_known_answer(lib):
+    """configs[2] at full shape (L=30, both operands rank 256, max rank 256): with the second
+    operand the constant 1 written as a redundant rank-256 train (block sum of 256 rank-1
+    trains, each 1/256), a o 1 = a exactly, so the zip-up must return a (rank <= 256) --
+    exercising the 512 x 65536 site matrices of the cfg3 path with a closed-form answer."""
+    import torch
+    from oracle import tt
+    L, R = 30, 256
+    a = gen.random_mps([2] * L, R, gen.rng_for(3, 0, 0), 1.0 / math.sqrt(R)).cores
+    ones = _redundant_ones(L, R)
     res = run_gpu(lib, "hadamard", ones, a, 1e-8, 256)
     rk = res.ranks[0].cpu().tolist()
     assert max(rk) <= 256
