@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--workload", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--members-per-gpu", type=int, default=512)
     ap.add_argument("--cpu-members", type=int, default=8, help="oracle sample size (members) for cpu_baseline")
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
+                    help="f32: the fp32 variant (binary32 cores; large-path contractions as 3xTF32 on tcgen05)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -236,8 +238,9 @@ def main():
 
     subs, kind, probs, xs, ops, cfg = build_workload(args, rank)
     mpo = kind == "matvec"
-    xd = qtt.to_device(xs)
-    od = None if ops is None else qtt.to_device(ops, mpo=mpo)
+    npdt = np.float32 if args.dtype == "f32" else np.float64
+    xd = qtt.to_device(xs, dtype=npdt)
+    od = None if ops is None else qtt.to_device(ops, mpo=mpo, dtype=npdt)
     p0 = probs[0]
     plan = qtt.ZipupPlan(subs, od, xd, p0.eps, p0.max_rank, sweeps=True, cycles=True)
     L = xd.n_sites
@@ -316,8 +319,8 @@ def main():
         hr = torch.empty_like(plan.ranks, device="cpu").pin_memory()
         hd = torch.empty_like(plan.delta2, device="cpu").pin_memory()
         hn = torch.empty_like(plan.norm2, device="cpu").pin_memory()
-        h2d = sum(t.numel() * 8 for t in hx + ho)
-        d2h = sum(t.numel() * 8 for t in hout) + hr.numel() * 4 + hd.numel() * 8 + hn.numel() * 8
+        h2d = sum(t.numel() * t.element_size() for t in hx + ho)
+        d2h = sum(t.numel() * t.element_size() for t in hout) + hr.numel() * 4 + hd.numel() * 8 + hn.numel() * 8
 
         def e2e_step():
             for dst, src in zip(xd.cores, hx):
@@ -365,10 +368,12 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": round(ms_max, 3), "higher_is_better": True,
-            "scaling": "weak" if args.workload == "cfg5" else "replicas", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak" if args.workload == "cfg5" else "replicas", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (seeded generators, BASELINE.json configs)",
-            "config": dict(cfg, l2="inputs %.2f GB/GPU > 126 MB L2: no flush needed" %
-                           (sum(c.numel() for c in xd.cores) * 8 / 1e9)),
+            "config": dict(cfg, l2="inputs %.2f GB/GPU%s" % (
+                sum(c.numel() * c.element_size() for c in xd.cores) / 1e9,
+                " > 126 MB L2: no flush needed" if args.workload == "cfg5" else
+                " (single zip-up; its per-site scratch exceeds L2 for cfg3/cfg4)")),
             "alg_tflops": round(world * flops_alg / (ms_max * 1e-3) / 1e12, 3),
             "alg_tflops_note": "contraction+QR+carry flops (SURVEY.md §8(d)); Jacobi excluded",
             "roofline": {"kernel": "k_sweep (persistent a2-a7 over all sites and members; Jacobi-dominated)", "bound": "fp64",

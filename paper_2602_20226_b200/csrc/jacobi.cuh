@@ -38,6 +38,9 @@ __device__ unsigned long long g_jprof[4];
 #ifndef QTT_JAC_SCALED
 #define QTT_JAC_SCALED 0
 #endif
+#ifndef QTT_JAC_SMEMBC
+#define QTT_JAC_SMEMBC 1
+#endif
 #ifndef QTT_JAC_UNROLL
 #define QTT_JAC_UNROLL 4
 #endif
@@ -184,6 +187,24 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm,
       const double x = X[i][tt], y = X[j][tt];
       X[i][tt] = fma(-u1, y, x);
       X[j][tt] = fma(u2, x, y);
+    }
+  }
+#elif QTT_JAC_SMEMBC
+  // (c, s) of every pair through shared memory: one 16-byte store per pair, one broadcast
+  // 16-byte load per pair and lane (instead of two 64-bit shuffles per pair)
+  double2 *csb = reinterpret_cast<double2 *>(esc);   // esc is free without scaled rotations
+  if (lane < NP) { nrm[ci] = al2; nrm[cj] = be2; csb[lane] = make_double2(c, s); }
+  __syncwarp();
+#pragma unroll
+  for (int a2 = 0; a2 < NP; ++a2) {
+    const int i = slot_i<WB, MODE, SH>(a2), j = slot_j<WB, MODE, SH>(a2);
+    const double2 cs2 = csb[a2];
+    const double ca = cs2.x, sa = cs2.y;
+#pragma unroll
+    for (int tt = 0; tt < RPL; ++tt) {
+      const double x = X[i][tt], y = X[j][tt];
+      X[i][tt] = fma(ca, x, -sa * y);
+      X[j][tt] = fma(sa, x, ca * y);
     }
   }
 #else
