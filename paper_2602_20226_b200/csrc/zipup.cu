@@ -311,19 +311,31 @@ __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double
       : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
-__device__ void qr_trailing_wy(double *Rp, double *Bk, const double *tau, double *Ysm, int m, int j0, int jn) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int np = jn - j0;                         // reflectors in the panel (<= 16)
+// Barrier over the warps [wbeg, wbeg + nw) taking part in a trailing update: the whole CTA,
+// or named barrier 1 when warp 0 is busy factoring the next panel (lookahead).
+__device__ __forceinline__ void wy_sync(int nw) {
+  if (nw == kSW) __syncthreads();
+  else asm volatile("bar.sync 1, %0;" ::"r"(nw * 32) : "memory");
+}
+
+// Update columns [cbeg, cend) of [R; B] with the panel j0..jn-1 (see above).  gram: compute
+// the Gram of the panel (Y columns j0..jn-1) in the same GEMM; otherwise it is already in
+// Ysm from an earlier call for this panel.  Run by warps [wbeg, wbeg + nw) only.
+__device__ void qr_trailing_wy(double *Rp, double *Bk, const double *tau, double *Ysm, int m, int j0, int jn,
+                               int cbeg, int cend, bool gram, int wbeg, int nw) {
+  const int tid = threadIdx.x - wbeg * 32, lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) - wbeg;
+  const int np = jn - j0;                         // reflectors in the panel (<= kPanel)
   const int gr = lane >> 2, gc = lane & 3;        // mma fragment coordinates
-  // (1) Yfull (16 x (m - j0)) = V_B^T Bk[:, j0:m]   (columns j0..jn-1 give the Gram G)
+  // (1) Y (kPanel x cols) = V_B^T Bk[:, cols], cols = [j0, jn) (Gram, if asked) + [cbeg, cend)
   {
-    const int ntile = (m - j0 + 7) >> 3;
-    for (int nt = warp; nt < ntile; nt += kSW) {
+    const int col0 = gram ? j0 : cbeg;
+    const int ntile = (cend - col0 + 7) >> 3;
+    for (int nt = warp; nt < ntile; nt += nw) {
       double c[kPanel / 8][2];
 #pragma unroll
       for (int mt = 0; mt < kPanel / 8; ++mt) c[mt][0] = c[mt][1] = 0.0;
-      const int bcol = j0 + nt * 8 + gr;          // B fragment: column gr, row gc
-      const bool bok = bcol < m;
+      const int bcol = col0 + nt * 8 + gr;        // B fragment: column gr, row gc
+      const bool bok = bcol < cend && (bcol < jn || bcol >= cbeg);
 #pragma unroll 4
       for (int k0 = 0; k0 < kSmall; k0 += 4) {
         const double *rowp = Bk + (size_t)(k0 + gc) * kLdA;
@@ -339,14 +351,14 @@ __device__ void qr_trailing_wy(double *Rp, double *Bk, const double *tau, double
       for (int mt = 0; mt < kPanel / 8; ++mt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int col = j0 + nt * 8 + 2 * gc + e;
-          if (col < m) Ysm[(mt * 8 + gr) * kYld + col] = c[mt][e];
+          const int col = col0 + nt * 8 + 2 * gc + e;
+          if (col < cend && (col < jn || col >= cbeg)) Ysm[(mt * 8 + gr) * kYld + col] = c[mt][e];
         }
     }
   }
-  __syncthreads();
-  // (2) per trailing column: Z = forward substitution; R rows j0..jn-1 updated
-  for (int c = jn + tid; c < m; c += kST) {
+  wy_sync(nw);
+  // (2) per updated column: Z = forward substitution; R rows j0..jn-1 updated
+  for (int c = cbeg + tid; c < cend; c += nw * 32) {
     double z[kPanel];
 #pragma unroll
     for (int jj = 0; jj < kPanel; ++jj) {
@@ -362,11 +374,11 @@ __device__ void qr_trailing_wy(double *Rp, double *Bk, const double *tau, double
       }
     }
   }
-  __syncthreads();
-  // (3) B[:, jn:m] -= V_B Z      (tiles of 8 rows x 8 columns, K = np <= 16)
+  wy_sync(nw);
+  // (3) B[:, cbeg:cend] -= V_B Z      (tiles of 8 rows x 8 columns, K = np <= kPanel)
   {
-    const int nct = (m - jn + 7) >> 3;
-    for (int rt = warp; rt < kSmall / 8; rt += kSW) {
+    const int nct = (cend - cbeg + 7) >> 3;
+    for (int rt = warp; rt < kSmall / 8; rt += nw) {
       double af[kPanel / 4];                        // -V_B fragments for this row tile
 #pragma unroll
       for (int ks = 0; ks < kPanel / 4; ++ks) {
@@ -374,26 +386,26 @@ __device__ void qr_trailing_wy(double *Rp, double *Bk, const double *tau, double
         af[ks] = (kk < np) ? -Bk[(size_t)(rt * 8 + gr) * kLdA + j0 + kk] : 0.0;
       }
       for (int ct = 0; ct < nct; ++ct) {
-        const int cb = jn + ct * 8;
+        const int cb = cbeg + ct * 8;
         double *crow = Bk + (size_t)(rt * 8 + gr) * kLdA;
         const int cc0 = cb + 2 * gc;
-        double c0 = (cc0 < m) ? crow[cc0] : 0.0, c1 = (cc0 + 1 < m) ? crow[cc0 + 1] : 0.0;
+        double c0 = (cc0 < cend) ? crow[cc0] : 0.0, c1 = (cc0 + 1 < cend) ? crow[cc0 + 1] : 0.0;
         const int zc = cb + gr;
 #pragma unroll
         for (int ks = 0; ks < kPanel / 4; ++ks) {
           const int kk = ks * 4 + gc;
-          const double zb = (kk < np && zc < m) ? Ysm[kk * kYld + zc] : 0.0;
+          const double zb = (kk < np && zc < cend) ? Ysm[kk * kYld + zc] : 0.0;
           dmma884(c0, c1, af[ks], zb);
         }
-        if (cc0 < m) crow[cc0] = c0;
-        if (cc0 + 1 < m) crow[cc0 + 1] = c1;
+        if (cc0 < cend) crow[cc0] = c0;
+        if (cc0 + 1 < cend) crow[cc0 + 1] = c1;
       }
     }
   }
-  __syncthreads();
+  wy_sync(nw);
 }
 
-__device__ void qr_of_TH(const double *T, int m, int n, double *Rp, double *Bk, double *tau, double *Ysm) {
+__device__ __noinline__ void qr_of_TH(const double *T, int m, int n, double *Rp, double *Bk, double *tau, double *Ysm) {
   const int tid = threadIdx.x, warp = tid >> 5;
   for (int i = tid; i < kRpDoubles; i += kST) Rp[i] = 0.0;
   for (int c0 = 0; c0 < n; c0 += kSmall) {
@@ -404,11 +416,18 @@ __device__ void qr_of_TH(const double *T, int m, int n, double *Rp, double *Bk, 
       Bk[i * kLdA + j] = (i < nb) ? T[(size_t)j * n + c0 + i] : 0.0;
     }
     __syncthreads();
+    // one-panel lookahead: the next panel's columns are updated first (all warps), then
+    // warp 0 factors it while warps 1.. update the remaining columns (named barrier 1)
+    if (warp == 0) qr_panel(Rp, Bk, tau, m, 0);
+    __syncthreads();
     for (int j0 = 0; j0 < m; j0 += kPanel) {
       const int jn = min(j0 + kPanel, m);
-      if (warp == 0) qr_panel(Rp, Bk, tau, m, j0);
+      if (jn >= m) break;
+      const int jn2 = min(jn + kPanel, m);
+      qr_trailing_wy(Rp, Bk, tau, Ysm, m, j0, jn, jn, jn2, true, 0, kSW);
+      if (warp == 0) qr_panel(Rp, Bk, tau, m, jn);
+      else if (jn2 < m) qr_trailing_wy(Rp, Bk, tau, Ysm, m, j0, jn, jn2, m, false, 1, kSW - 1);
       __syncthreads();
-      if (jn < m) qr_trailing_wy(Rp, Bk, tau, Ysm, m, j0, jn);
     }
   }
 }
