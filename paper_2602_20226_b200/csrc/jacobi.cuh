@@ -38,6 +38,9 @@ __device__ unsigned long long g_jprof[4];
 #ifndef QTT_JAC_SCALED
 #define QTT_JAC_SCALED 0
 #endif
+#ifndef QTT_JAC_GRAMCHECK
+#define QTT_JAC_GRAMCHECK 1
+#endif
 #ifndef QTT_JAC_SMEMBC
 #define QTT_JAC_SMEMBC 1
 #endif
@@ -165,7 +168,12 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm,
   const double al2 = doit ? fma(-t, ga, al) : al;
   const double be2 = doit ? fma(t, ga, be) : be;
   const bool collapse = doit && (al2 < 1.5e-8 * al || be2 < 1.5e-8 * be);
-  if (__any_sync(0xffffffffu, doit)) rot = 1;
+  if (__any_sync(0xffffffffu, doit)) rot |= 1;
+#if QTT_JAC_GRAMCHECK
+  // bit 1: some pair of this sweep was still far from converged (|cos| >= 1e-6), so the
+  // next sweep cannot be skipped by the Gram check (jacobi_blocked)
+  if (__any_sync(0xffffffffu, ga * ga >= 1e-12 * (al * be))) rot |= 2;
+#endif
   __syncwarp();
   QTT_JPROF_T(jt2);
 #if QTT_JAC_SCALED
@@ -284,6 +292,54 @@ __device__ __forceinline__ void rotate_circle(double (&X)[2 * WB][RPL], int *slo
   __syncwarp();
 }
 
+// True iff |a_i . a_j| <= tolg * |a_i| |a_j| for every pair of the first pc columns of A (column-
+// major, leading dimension kLdA, 32*RPL rows, zero padding beyond the matrix).  Column norms by
+// warp reductions, off-diagonal Gram entries by DMMA (m8n8k4) over the upper-triangular 8 x 8
+// tiles.  All threads call it; uses scratch[0 .. 128) and *flag.
+__device__ __forceinline__ void dmma884_j(double &c0, double &c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+template <int NW, int RPL>
+__device__ bool gram_converged(const double *A, int pc, double tolg, double *scratch, int *flag) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double *nn = scratch;                         // [128] squared column norms
+  for (int j = warp; j < pc; j += NW) {
+    double s = 0.0;
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) { const double v = A[(size_t)j * kLdA + lane + 32 * t]; s = fma(v, v, s); }
+    s = warp_sum(s);
+    if (lane == 0) nn[j] = s;
+  }
+  if (threadIdx.x == 0) *flag = 0;
+  __syncthreads();
+  const int gr = lane >> 2, gc = lane & 3, nt = pc >> 3;
+  const double tol2 = tolg * tolg;
+  bool bad = false;
+  for (int t = warp; t < nt * (nt + 1) / 2; t += NW) {
+    int ti = 0, rem = t;                        // t -> (ti <= tj) upper-triangular tile
+    while (rem >= nt - ti) { rem -= nt - ti; ++ti; }
+    const int tj = ti + rem;
+    double c0 = 0.0, c1 = 0.0;
+    const double *ai = A + (size_t)(ti * 8 + gr) * kLdA, *aj = A + (size_t)(tj * 8 + gr) * kLdA;
+#pragma unroll 8
+    for (int k0 = 0; k0 < 32 * RPL; k0 += 4) dmma884_j(c0, c1, ai[k0 + gc], aj[k0 + gc]);
+    const int i = ti * 8 + gr;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int j = tj * 8 + 2 * gc + e;
+      const double g = e ? c1 : c0;
+      if (j > i && nn[i] > 0.0 && nn[j] > 0.0 && g * g > tol2 * (nn[i] * nn[j])) bad = true;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+  __syncthreads();
+  const bool ok = (*flag == 0);
+  __syncthreads();
+  return ok;
+}
+
 // Returns the number of sweeps executed (== kJacobiMaxSweeps: not converged).
 template <int RPL, int WB, int NW>
 __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
@@ -354,11 +410,19 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
     }
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
-    if (lane == 0 && rot) *flag = 1;
+    if (lane == 0 && rot) atomicOr(flag, rot);
     __syncthreads();
     const int any = *flag;
     __syncthreads();
-    if (!any) { ++sweep; break; }
+    if (!(any & 1)) { ++sweep; break; }
+#if QTT_JAC_GRAMCHECK
+    // Every pair of this sweep started within |cos| < 1e-6, so by the quadratic convergence of
+    // cyclic Jacobi the next sweep is (almost always) the verification sweep that rotates
+    // nothing.  Check that directly on the Gram matrix (DMMA, ~1/10 of a sweep) with the same
+    // threshold as the sweep's own test (whose register dot products carry rounding of the
+    // same ~sqrt(m) eps order); a failed check just runs the sweep.
+    if (!(any & 2) && gram_converged<NW, RPL>(A, 2 * NW * WB, tol, scratch, flag)) { ++sweep; break; }
+#endif
   }
   return sweep;
 }
