@@ -23,17 +23,22 @@ namespace qtt {
 // GEMM staging).
 __host__ __device__ constexpr long long orth_reg_smem(int rpl, int c, int r, int rows_prev) {
   return (long long)(c < r ? c : r) * (32 * rpl) + 2 * 64 + (long long)(c < r ? c : r) * r +
-         (long long)rows_prev * r + 2 * 16 * 64;
+         (long long)rows_prev * r + 2 * 16 * 64 + 8 * kWarps;
 }
 
 // Warp all-reduce of N partial sums (N a power of two <= 32): tot[i] = sum over lanes of v[i].
+// Butterfly reduce-scatter, then the N totals go out through the warp's shared-memory slot
+// buf[0..N) (one store per total, broadcast loads) instead of N 64-bit shuffles.
 template <int N>
-__device__ __forceinline__ void warp_allreduce_vec(double (&v)[N], double (&tot)[N]) {
+__device__ __forceinline__ void warp_allreduce_vec(double (&v)[N], double (&tot)[N], double *buf) {
   const int lane = threadIdx.x & 31;
   halve<N, 16, N>(v, lane);
   constexpr int sh = 5 - ilog2<N>();
+  __syncwarp();                                    // previous readers of buf are done
+  if ((lane & ((1 << sh) - 1)) == 0) buf[lane >> sh] = v[0];
+  __syncwarp();
 #pragma unroll
-  for (int i = 0; i < N; ++i) tot[i] = __shfl_sync(0xffffffffu, v[0], i << sh);
+  for (int i = 0; i < N; ++i) tot[i] = buf[i];
 }
 
 template <int RPL, int NCW>
@@ -78,7 +83,8 @@ __device__ __forceinline__ void orth_form_reflector(double (&X)[NCW][RPL], int j
 // Apply reflector j to this warp's columns col > j (only slot `only` if only >= 0, all
 // slots but -2-only if only <= -2, every slot if only == -1); FORM_Q: every column, no mask.
 template <int RPL, int NCW, bool FORM_Q = false>
-__device__ __forceinline__ void orth_apply(double (&X)[NCW][RPL], int j, const double *vbuf, double tau, int only) {
+__device__ __forceinline__ void orth_apply(double (&X)[NCW][RPL], int j, const double *vbuf, double tau, int only,
+                                           double *wbuf) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int CP = 32 * RPL;
   double v[RPL];
@@ -92,7 +98,7 @@ __device__ __forceinline__ void orth_apply(double (&X)[NCW][RPL], int j, const d
     for (int t = 0; t < RPL; ++t) acc = fma(v[t], X[ss][t], acc);
     p[ss] = acc;
   }
-  warp_allreduce_vec<NCW>(p, tot);
+  warp_allreduce_vec<NCW>(p, tot, wbuf);
 #pragma unroll
   for (int ss = 0; ss < NCW; ++ss) {
     const int col = warp + kWarps * ss;
@@ -121,6 +127,7 @@ __device__ int orth_site_reg(double *core, int c, int r, double *prev, int rows_
   double *Rb = taus + 2 * 64;                       // k x r, upper trapezoidal
   double *Psm = Rb + (size_t)k * r;                 // rows_prev x r
   double *gst = Psm + (size_t)rows_prev * r;        // GEMM staging (2 x 16 x 64)
+  double *wbuf = gst + 2 * 16 * 64 + (threadIdx.x >> 5) * 8;   // per-warp all-reduce slot
 
   double X[NCW][RPL];
 #pragma unroll
@@ -136,18 +143,31 @@ __device__ int orth_site_reg(double *core, int c, int r, double *prev, int rows_
   for (int i = tid; i < k * r; i += kThreads) Rb[i] = 0.0;
   if (warp == 0) orth_form_reflector<RPL, NCW>(X, 0, c, vbuf, taus);
   __syncthreads();
+  // The owner of column j+1 applies reflector j to that column only, forms reflector j+1 and
+  // defers reflector j on its other columns to the next step (where it is not the owner), so
+  // the per-step critical path is one column update + one reflector, not a full update more.
+  int pend = -1, pend_slot = 0;
   for (int j = 0; j < k; ++j) {
     const double tau = taus[j];
     const int nxt = j + 1;
     if (nxt < k && warp == (nxt % kWarps)) {
       const int sn = nxt / kWarps;
-      if (tau != 0.0) orth_apply<RPL, NCW>(X, j, vbuf, tau, sn);
+      if (tau != 0.0) orth_apply<RPL, NCW>(X, j, vbuf, tau, sn, wbuf);
       orth_form_reflector<RPL, NCW>(X, nxt, c, vbuf, taus);
-      if (tau != 0.0) orth_apply<RPL, NCW>(X, j, vbuf, tau, -2 - sn);
-    } else if (tau != 0.0) {
-      orth_apply<RPL, NCW>(X, j, vbuf, tau, -1);
+      pend = j; pend_slot = sn;
+    } else {
+      if (pend >= 0) {
+        const double tp = taus[pend];
+        if (tp != 0.0) orth_apply<RPL, NCW>(X, pend, vbuf, tp, -2 - pend_slot, wbuf);
+        pend = -1;
+      }
+      if (tau != 0.0) orth_apply<RPL, NCW>(X, j, vbuf, tau, -1, wbuf);
     }
     __syncthreads();
+  }
+  if (pend >= 0) {                                  // owner of the last column: finish its update
+    const double tp = taus[pend];
+    if (tp != 0.0) orth_apply<RPL, NCW>(X, pend, vbuf, tp, -2 - pend_slot, wbuf);
   }
   // R: column col holds R[i][col] in rows i <= min(col, k-1)
 #pragma unroll
@@ -169,7 +189,7 @@ __device__ int orth_site_reg(double *core, int c, int r, double *prev, int rows_
   const int jtop = min(k - 1, warp + kWarps * (NCW - 1));  // highest column this warp owns
   for (int j = jtop; j >= 0; --j) {
     const double tau = taus[j];
-    if (tau != 0.0) orth_apply<RPL, NCW, true>(X, j, vbuf, tau, -1);
+    if (tau != 0.0) orth_apply<RPL, NCW, true>(X, j, vbuf, tau, -1, wbuf);
   }
   __syncthreads();                                   // Rb complete; reflectors no longer read
   // core q <- Q^T: row kk = column kk of Q (coalesced along rows of Q)
