@@ -41,6 +41,9 @@ __device__ unsigned long long g_jprof[4];
 #ifndef QTT_JAC_GRAMCHECK
 #define QTT_JAC_GRAMCHECK 1
 #endif
+#ifndef QTT_JAC_DIVFREE
+#define QTT_JAC_DIVFREE 1
+#endif
 #ifndef QTT_JAC_SMEMBC
 #define QTT_JAC_SMEMBC 1
 #endif
@@ -160,11 +163,22 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm,
   const double g2 = ga + ga;
   const bool doit = (ga * ga > (tol * tol) * (al * be)) && (al > 0.0) && (be > 0.0);
   const double x2 = fma(d, d, g2 * g2);
+#if QTT_JAC_DIVFREE
+  // same angle without a division: y = 1/sqrt(d^2 + 4 g^2), c^2 = (1 + |d| y)/2, z = 1/c,
+  // s = sign(d) g y z, t = s z
+  const double y = doit ? fast_rsqrt(x2) : 0.0;
+  const double c2 = doit ? fma(0.5 * fabs(d), y, 0.5) : 1.0;
+  const double z = doit ? fast_rsqrt(c2) : 1.0;
+  const double c = c2 * z;
+  const double s = copysign(1.0, d) * ga * y * z;
+  const double t = s * z;
+#else
   const double h = doit ? x2 * fast_rsqrt(x2) : 1.0;
   const double den = fabs(d) + h;
   const double t = doit ? copysign(1.0, d) * g2 * fast_rcp(den) : 0.0;
   const double c = fast_rsqrt(fma(t, t, 1.0));
   const double s = c * t;
+#endif
   const double al2 = doit ? fma(-t, ga, al) : al;
   const double be2 = doit ? fma(t, ga, be) : be;
   const bool collapse = doit && (al2 < 1.5e-8 * al || be2 < 1.5e-8 * be);
