@@ -432,6 +432,77 @@ __device__ __noinline__ void qr_of_TH(const double *T, int m, int n, double *Rp,
   }
 }
 
+// a2 for "ij,j->i" on DMMA, fused with the MPO epilogue (no X round trip through global):
+//   X[(c,w),(j,r')] = sum_r G[(c,w),r] x_q[r,(j,r')]     (M = chi*w, K = r, N = dj*r2)
+//   T[c,i,w',r']    = sum_{w,j} X[c,w,j,r'] W[w,i,j,w']
+// x_q is staged in Xs (K x 136, == 8 mod 16: conflict-free B fragments), W in Ws; every warp
+// takes 8-row tiles of X (8/w whole c's, since w divides 8), accumulates 8 x N with m8n8k4
+// DMMA (A fragments straight from G in L2), parks the tile in its Xt slot (8 x 129) and
+// forms the tile's T rows.  Requires w in {1,2,4,8}, N <= 128, padded K * 136 <= kSmall *
+// kLdA, w * d * dj * w2 <= 16 * kYld.
+constexpr int kXsLd = 136, kXtLd = 129;
+
+__device__ __forceinline__ bool contract_dmma_ok(int w, int K, int N, int wsz) {
+  return (w == 1 || w == 2 || w == 4 || w == 8) && N <= 128 && ((K + 3) & ~3) * kXsLd <= kSmall * kLdA &&
+         wsz <= 16 * kYld;
+}
+
+__device__ void contract_dmma(const double *G, const double *Xq, const double *Oq, double *T, int chi, int w, int K,
+                              int dj, int r2, int d, int w2, double *Xs, double *Xt, double *Ws) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gr = lane >> 2, gc = lane & 3;
+  const int M = chi * w, N = dj * r2, wsz = w * d * dj * w2;
+  const int Kp = (K + 3) & ~3;
+  for (int idx = tid; idx < Kp * N; idx += kST) {          // coalesced along N
+    const int k = idx / N, n = idx - k * N;
+    Xs[k * kXsLd + n] = (k < K) ? Xq[(size_t)k * N + n] : 0.0;
+  }
+  for (int i = tid; i < wsz; i += kST) Ws[i] = Oq[i];
+  __syncthreads();
+  double *xt = Xt + warp * 8 * kXtLd;
+  const int ntn = (N + 7) >> 3;
+  const int cpt = 8 / w;                                   // c's per 8-row tile
+  for (int mt = warp; mt * 8 < M; mt += kSW) {
+    double acc[16][2];
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+    const int arow = mt * 8 + gr;
+    const double *ga = G + (size_t)arow * K;
+    for (int k0 = 0; k0 < Kp; k0 += 4) {
+      const int k = k0 + gc;
+      const double av = (arow < M && k < K) ? ga[k] : 0.0;
+      const double *xb = Xs + k * kXsLd + gr;
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt)
+        if (nt < ntn) dmma884(acc[nt][0], acc[nt][1], av, xb[nt * 8]);
+    }
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt)
+      if (nt < ntn) {
+        xt[gr * kXtLd + nt * 8 + 2 * gc] = acc[nt][0];
+        xt[gr * kXtLd + nt * 8 + 2 * gc + 1] = acc[nt][1];
+      }
+    __syncwarp();
+    // T rows of this tile's c's: lane -> r' (strided), loop (i, w') and (w, j)
+    for (int cl = 0; cl < cpt; ++cl) {
+      const int c = mt * cpt + cl;
+      if (c >= chi) break;
+      const double *xr = xt + cl * w * kXtLd;
+      for (int rr = lane; rr < r2; rr += 32) {
+        for (int ii = 0; ii < d; ++ii)
+          for (int w2i = 0; w2i < w2; ++w2i) {
+            double sacc = 0.0;
+            for (int ww = 0; ww < w; ++ww)
+              for (int jj = 0; jj < dj; ++jj)
+                sacc = fma(xr[ww * kXtLd + jj * r2 + rr], Ws[((ww * d + ii) * dj + jj) * w2 + w2i], sacc);
+            T[((size_t)(c * d + ii) * w2 + w2i) * r2 + rr] = sacc;
+          }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, double *smem) {
   double *Rp = smem;                         // packed R (QR) / GEMM staging / scratch
   double *Rs = Rp + kRpDoubles;              // kSmall x kLdA: QR block, then A (col-major)
@@ -465,7 +536,9 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
     __syncthreads();
   }
   // ---------------------------------------------------------------- a2: contraction
-  if (a.kind == MATVEC) {
+  if (a.kind == MATVEC && kSW == 8 && contract_dmma_ok(w, r, dj * r2, w * d * dj * w2)) {
+    contract_dmma(G, Xq, Oq, T, chi, w, r, dj, r2, d, w2, Rs, Rp, Ysm);
+  } else if (a.kind == MATVEC) {
     const int M = chi * w, K = r, N = dj * r2;     // X[(c,w),(j,r')] = G[(c,w),r] x_q[r,(j,r')]
     cta_gemm<kST>(M, N, K, [&](int i, int k) { return G[(size_t)i * K + k]; },
              [&](int k, int j) { return Xq[(size_t)k * N + j]; },
