@@ -122,7 +122,7 @@ __device__ __forceinline__ constexpr int slot_j(int a) {
 
 template <int RPL, int WB, int MODE, int SH = 0>
 __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm, double *dsc, double *esc,
-                                          const int *slot_col, double tol, int &rot) {
+                                          double2 *csb, const int *slot_col, double tol, int &rot) {
   constexpr int NP = (MODE != 1) ? WB : 2 * (WB / 2);   // pairs in this round
   constexpr int NV = (NP <= 4) ? 4 : (NP <= 8) ? 8 : (NP <= 16) ? 16 : 32;
   const int lane = threadIdx.x & 31;
@@ -193,17 +193,22 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm,
 #if QTT_JAC_SCALED
   // scaled (Anda-Park) rotation: true column = dsc * register column; the register columns
   // take X_i -= t (d_j/d_i) X_j, X_j += t (d_i/d_j) X_i and the scales take the cosine
+#if !QTT_JAC_DIVFREE
   const double z = fma(t, t, 1.0) * c;                 // 1/c
+#endif
   const double t1 = t * (dj * ei), t2 = t * (di * ej);
   if (lane < NP) {
     nrm[ci] = al2; nrm[cj] = be2;
     dsc[ci] = di * c; dsc[cj] = dj * c; esc[ci] = ei * z; esc[cj] = ej * z;
+    csb[lane] = make_double2(t1, t2);
   }
   (void)s;
+  __syncwarp();
 #pragma unroll
   for (int a2 = 0; a2 < NP; ++a2) {
     const int i = slot_i<WB, MODE, SH>(a2), j = slot_j<WB, MODE, SH>(a2);
-    const double u1 = __shfl_sync(0xffffffffu, t1, a2), u2 = __shfl_sync(0xffffffffu, t2, a2);
+    const double2 tt2 = csb[a2];
+    const double u1 = tt2.x, u2 = tt2.y;
 #pragma unroll
     for (int tt = 0; tt < RPL; ++tt) {
       const double x = X[i][tt], y = X[j][tt];
@@ -214,7 +219,6 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm,
 #elif QTT_JAC_SMEMBC
   // (c, s) of every pair through shared memory: one 16-byte store per pair, one broadcast
   // 16-byte load per pair and lane (instead of two 64-bit shuffles per pair)
-  double2 *csb = reinterpret_cast<double2 *>(esc);   // esc is free without scaled rotations
   if (lane < NP) { nrm[ci] = al2; nrm[cj] = be2; csb[lane] = make_double2(c, s); }
   __syncwarp();
 #pragma unroll
@@ -274,10 +278,10 @@ __device__ __forceinline__ void rotate_Jn(double (&X)[2 * WB][RPL], int *slot_co
 
 template <int RPL, int WB, int SH, int U>
 __device__ __forceinline__ void cross_rounds(double (&X)[2 * WB][RPL], double *nrm, double *dsc, double *esc,
-                                             const int *slot_col, double tol, int &rot) {
+                                             double2 *csb, const int *slot_col, double tol, int &rot) {
   if constexpr (SH < U) {
-    jac_round<RPL, WB, 0, SH>(X, nrm, dsc, esc, slot_col, tol, rot);
-    cross_rounds<RPL, WB, SH + 1, U>(X, nrm, dsc, esc, slot_col, tol, rot);
+    jac_round<RPL, WB, 0, SH>(X, nrm, dsc, esc, csb, slot_col, tol, rot);
+    cross_rounds<RPL, WB, SH + 1, U>(X, nrm, dsc, esc, csb, slot_col, tol, rot);
   }
 }
 
@@ -365,6 +369,7 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
   double *dsc = scratch + NW * 2 * WB + warp * 2 * WB;                     // column scales (scaled rotations)
   double *esc = scratch + NW * 4 * WB + warp * 2 * WB;                     // 1 / column scales
   int *slot_col = reinterpret_cast<int *>(scratch + NW * 6 * WB) + warp * 2 * WB;
+  double2 *csb = reinterpret_cast<double2 *>(scratch + NW * 8 * WB + warp * 2 * WB);   // rotation broadcast
   int sweep = 0;
   for (; sweep < kJacobiMaxSweeps; ++sweep) {
     int rot = 0;
@@ -393,7 +398,7 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
         if (r == 0) {
 #pragma unroll 1
           for (int u = 0; u < WB - 1; ++u) {
-            jac_round<RPL, WB, 1>(X, nrm, dsc, esc, slot_col, tol, rot);
+            jac_round<RPL, WB, 1>(X, nrm, dsc, esc, csb, slot_col, tol, rot);
             rotate_circle<RPL, WB>(X, slot_col);
           }
         }
@@ -402,7 +407,7 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
         constexpr int U = (WB < QTT_JAC_UNROLL) ? WB : QTT_JAC_UNROLL;
 #pragma unroll 1
         for (int u = 0; u < WB; u += U) {
-          cross_rounds<RPL, WB, 0, U>(X, nrm, dsc, esc, slot_col, tol, rot);
+          cross_rounds<RPL, WB, 0, U>(X, nrm, dsc, esc, csb, slot_col, tol, rot);
           if constexpr (U < WB) rotate_Jn<RPL, WB, U>(X, slot_col);
         }
       }
