@@ -374,23 +374,40 @@ struct JacArgs {
   int *status;
 };
 
-__device__ __forceinline__ void rot_pair(double *ci, double *cj, int m, double tol, int &rot) {
+// One Jacobi pair (one warp): exact dot product, column norms nrm_i / nrm_j carried in shared
+// memory by the rotation identities (exact refresh on cancellation, LAPACK dgesvj practice),
+// division-free MUFU-seeded angle (same formulas as the small path, jacobi.cuh).
+__device__ __forceinline__ double col_norm2(const double *c, int m) {
   const int lane = threadIdx.x & 31;
-  double al = 0.0, be = 0.0, ga = 0.0;
-  for (int r = lane; r < m; r += 32) {
-    const double x = ci[r], y = cj[r];
-    al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
-  }
-  al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
-  if (ga != 0.0 && al > 0.0 && be > 0.0 && fabs(ga) > tol * sqrt(al) * sqrt(be)) {
+  double s = 0.0;
+  for (int r = lane; r < m; r += 32) s = fma(c[r], c[r], s);
+  return warp_sum(s);
+}
+
+__device__ __forceinline__ void rot_pair(double *ci, double *cj, double *nrm_i, double *nrm_j, int m, double tol,
+                                         int &rot) {
+  const int lane = threadIdx.x & 31;
+  double ga = 0.0;
+  for (int r = lane; r < m; r += 32) ga = fma(ci[r], cj[r], ga);
+  ga = warp_sum(ga);
+  const double al = *nrm_i, be = *nrm_j;
+  if (al > 0.0 && be > 0.0 && ga * ga > (tol * tol) * (al * be)) {
     const double d = be - al, g2 = ga + ga;
-    const double t = copysign(1.0, d) * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
-    const double c = 1.0 / sqrt(fma(t, t, 1.0)), s = c * t;
+    const double y = fast_rsqrt(fma(d, d, g2 * g2));
+    const double c2 = fma(0.5 * fabs(d), y, 0.5);
+    const double z = fast_rsqrt(c2);
+    const double c = c2 * z, s = copysign(1.0, d) * ga * y * z, t = s * z;
     for (int r = lane; r < m; r += 32) {
-      const double x = ci[r], y = cj[r];
-      ci[r] = fma(c, x, -s * y);
-      cj[r] = fma(s, x, c * y);
+      const double x = ci[r], yv = cj[r];
+      ci[r] = fma(c, x, -s * yv);
+      cj[r] = fma(s, x, c * yv);
     }
+    double al2 = fma(-t, ga, al), be2 = fma(t, ga, be);
+    __syncwarp();
+    if (al2 < 1.5e-8 * al) al2 = col_norm2(ci, m);
+    if (be2 < 1.5e-8 * be) be2 = col_norm2(cj, m);
+    if (lane == 0) { *nrm_i = al2; *nrm_j = be2; }
+    __syncwarp();
     rot = 1;
   }
 }
@@ -402,6 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
   const int NB = 2 * ((p + 2 * WB - 1) / (2 * WB));     // even number of blocks
   const double tol = (double)max(m, 1) * DBL_EPSILON;
   double *S = smj;                                      // [2*WB][m]
+  double *nrmS = S + (size_t)2 * WB * m;                // [2*WB] column norms of the loaded blocks
   __shared__ int s_rot;
   int sweep = 0;
   for (; sweep < 60; ++sweep) {
@@ -421,6 +439,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
           S[idx] = (col < p) ? a.A[(size_t)col * m + row] : 0.0;
         }
         __syncthreads();
+        for (int c = warp; c < 2 * WB; c += kWarps) {            // exact norms at block load
+          const double v = col_norm2(S + (size_t)c * m, m);
+          if ((tid & 31) == 0) nrmS[c] = v;
+        }
+        __syncthreads();
         if (r == 0 && WB > 1) {           // intra-block pairs (circle method on WB players)
           for (int u = 0; u < WB - 1; ++u) {
             for (int pr = warp; pr < WB; pr += kWarps) {
@@ -428,14 +451,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
               const int k1 = tt, k2 = WB - 1 - tt;
               const int i = base + ((k1 == 0) ? 0 : 1 + (k1 - 1 + u) % (WB - 1));
               const int j = base + ((k2 == 0) ? 0 : 1 + (k2 - 1 + u) % (WB - 1));
-              rot_pair(S + (size_t)i * m, S + (size_t)j * m, m, tol, rot);
+              rot_pair(S + (size_t)i * m, S + (size_t)j * m, nrmS + i, nrmS + j, m, tol, rot);
             }
             __syncthreads();
           }
         }
         for (int sft = 0; sft < WB; ++sft) {     // cross pairs (a, WB + (a+sft)%WB)
           for (int pr = warp; pr < WB; pr += kWarps)
-            rot_pair(S + (size_t)pr * m, S + (size_t)(WB + (pr + sft) % WB) * m, m, tol, rot);
+            rot_pair(S + (size_t)pr * m, S + (size_t)(WB + (pr + sft) % WB) * m, nrmS + pr,
+                     nrmS + WB + (pr + sft) % WB, m, tol, rot);
           __syncthreads();
         }
         for (int idx = tid; idx < 2 * WB * m; idx += kThreads) {
@@ -658,14 +682,15 @@ static qtt_status_t plan_sweep(int L, const std::vector<int> &d, const std::vect
   P.RB = ((P.RB + 31) / 32) * 32;
   while (P.RB > kQrRowsMax) { set_error("large path: n = %lld too large", P.ncap); return QTT_EUNSUPPORTED; }
   P.qr_smem = sizeof(double) * ((size_t)2 * kNb * P.RB + 32 + kNb * kNb + 2 * kNb + kNb * 64);
-  // Jacobi: block width so that 2*WB*m*8 <= 200 KB and #pairs <= #SMs
+  // Jacobi: ~64 blocks of WB columns (a grid barrier per block round dominates a sweep, so
+  // fewer, wider blocks beat one block pair per SM: cfg3 1504 -> 1160 ms), capped by smem
   int WB = 1;
-  while (WB < 64 && (P.pcap + 2 * WB - 1) / (2 * WB) > g_sms) WB *= 2;
-  while (WB > 1 && 2 * WB * P.mcap * 8 > 200 * 1024) WB /= 2;
-  if (2 * WB * P.mcap * 8 > 200 * 1024) { set_error("large path: m = %lld too large", P.mcap); return QTT_EUNSUPPORTED; }
+  while (WB < 64 && (P.pcap + WB - 1) / WB > 64) WB *= 2;
+  while (WB > 1 && 2 * WB * (P.mcap + 1) * 8 > 200 * 1024) WB /= 2;
+  if (2 * WB * (P.mcap + 1) * 8 > 200 * 1024) { set_error("large path: m = %lld too large", P.mcap); return QTT_EUNSUPPORTED; }
   P.WB = WB;
   P.Gjac = (int)std::min<long long>(g_sms, std::max<long long>(1, (P.pcap + 2 * WB - 1) / (2 * WB)));
-  P.jac_smem = sizeof(double) * 2 * WB * P.mcap;
+  P.jac_smem = sizeof(double) * (2 * WB * P.mcap + 2 * WB);
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
   P.off_G = take(8 * P.gcap);
