@@ -122,7 +122,7 @@ __device__ __forceinline__ constexpr int slot_j(int a) {
 
 template <int RPL, int WB, int MODE, int SH = 0>
 __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm, double *dsc, double *esc,
-                                          double2 *csb, const int *slot_col, double tol, int &rot) {
+                                          double2 *csb, const int *slot_col, double tol, double noise, int &rot) {
   constexpr int NP = (MODE != 1) ? WB : 2 * (WB / 2);   // pairs in this round
   constexpr int NV = (NP <= 4) ? 4 : (NP <= 8) ? 8 : (NP <= 16) ? 16 : 32;
   const int lane = threadIdx.x & 31;
@@ -161,7 +161,9 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm,
   // c = 1/sqrt(1+t^2), s = c t.  Rotate only if |g| > tol sqrt(a b) (squared test).
   const double d = be - al;
   const double g2 = ga + ga;
-  const bool doit = (ga * ga > (tol * tol) * (al * be)) && (al > 0.0) && (be > 0.0);
+  // noise = eps^2 ||A||_F^2: a column at rounding-noise level is treated as converged (its
+  // relative orthogonality is below fp64 resolution; see large.cu rot_pair)
+  const bool doit = (ga * ga > (tol * tol) * (al * be)) && (al > noise) && (be > noise);
   const double x2 = fma(d, d, g2 * g2);
 #if QTT_JAC_DIVFREE
   // same angle without a division: y = 1/sqrt(d^2 + 4 g^2), c^2 = (1 + |d| y)/2, z = 1/c,
@@ -186,7 +188,7 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm,
 #if QTT_JAC_GRAMCHECK
   // bit 1: some pair of this sweep was still far from converged (|cos| >= 1e-6), so the
   // next sweep cannot be skipped by the Gram check (jacobi_blocked)
-  if (__any_sync(0xffffffffu, ga * ga >= 1e-12 * (al * be))) rot |= 2;
+  if (__any_sync(0xffffffffu, al > noise && be > noise && ga * ga >= 1e-12 * (al * be))) rot |= 2;
 #endif
   __syncwarp();
   QTT_JPROF_T(jt2);
@@ -278,10 +280,10 @@ __device__ __forceinline__ void rotate_Jn(double (&X)[2 * WB][RPL], int *slot_co
 
 template <int RPL, int WB, int SH, int U>
 __device__ __forceinline__ void cross_rounds(double (&X)[2 * WB][RPL], double *nrm, double *dsc, double *esc,
-                                             double2 *csb, const int *slot_col, double tol, int &rot) {
+                                             double2 *csb, const int *slot_col, double tol, double noise, int &rot) {
   if constexpr (SH < U) {
-    jac_round<RPL, WB, 0, SH>(X, nrm, dsc, esc, csb, slot_col, tol, rot);
-    cross_rounds<RPL, WB, SH + 1, U>(X, nrm, dsc, esc, csb, slot_col, tol, rot);
+    jac_round<RPL, WB, 0, SH>(X, nrm, dsc, esc, csb, slot_col, tol, noise, rot);
+    cross_rounds<RPL, WB, SH + 1, U>(X, nrm, dsc, esc, csb, slot_col, tol, noise, rot);
   }
 }
 
@@ -320,7 +322,7 @@ __device__ __forceinline__ void dmma884_j(double &c0, double &c1, double a, doub
 }
 
 template <int NW, int RPL>
-__device__ bool gram_converged(const double *A, int pc, double tolg, double *scratch, int *flag) {
+__device__ bool gram_converged(const double *A, int pc, double tolg, double noise, double *scratch, int *flag) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double *nn = scratch;                         // [128] squared column norms
   for (int j = warp; j < pc; j += NW) {
@@ -348,7 +350,7 @@ __device__ bool gram_converged(const double *A, int pc, double tolg, double *scr
     for (int e = 0; e < 2; ++e) {
       const int j = tj * 8 + 2 * gc + e;
       const double g = e ? c1 : c0;
-      if (j > i && nn[i] > 0.0 && nn[j] > 0.0 && g * g > tol2 * (nn[i] * nn[j])) bad = true;
+      if (j > i && nn[i] > noise && nn[j] > noise && g * g > tol2 * (nn[i] * nn[j])) bad = true;
     }
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
@@ -359,8 +361,10 @@ __device__ bool gram_converged(const double *A, int pc, double tolg, double *scr
 }
 
 // Returns the number of sweeps executed (== kJacobiMaxSweeps: not converged).
+// noise_ok: the caller truncates with eps > 1e-14, so columns at rounding-noise level can
+// never be kept and need not be orthogonalised (eps = 0 keeps them: they must be orthonormal)
 template <int RPL, int WB, int NW>
-__device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
+__device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch, bool noise_ok) {
   constexpr int NB = 2 * NW;          // 2*NW blocks of WB columns (one block pair per warp)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double tol = (double)max(m, 1) * DBL_EPSILON;
@@ -370,6 +374,23 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
   double *esc = scratch + NW * 4 * WB + warp * 2 * WB;                     // 1 / column scales
   int *slot_col = reinterpret_cast<int *>(scratch + NW * 6 * WB) + warp * 2 * WB;
   double2 *csb = reinterpret_cast<double2 *>(scratch + NW * 8 * WB + warp * 2 * WB);   // rotation broadcast
+  double noise;                                                            // eps^2 ||A||_F^2
+  {
+    double sq = 0.0;
+    for (int idx = threadIdx.x; idx < 2 * NW * WB * 32 * RPL; idx += NW * 32) {
+      const double v = A[(size_t)(idx / (32 * RPL)) * kLdA + idx % (32 * RPL)];
+      sq = fma(v, v, sq);
+    }
+    sq = warp_sum(sq);
+    __syncthreads();
+    if (lane == 0) scratch[warp] = sq;
+    __syncthreads();
+    double tot = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) tot += scratch[w];             // fixed order: deterministic
+    noise = noise_ok ? DBL_EPSILON * DBL_EPSILON * tot : 0.0;
+    __syncthreads();
+  }
   int sweep = 0;
   for (; sweep < kJacobiMaxSweeps; ++sweep) {
     int rot = 0;
@@ -398,7 +419,7 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
         if (r == 0) {
 #pragma unroll 1
           for (int u = 0; u < WB - 1; ++u) {
-            jac_round<RPL, WB, 1>(X, nrm, dsc, esc, csb, slot_col, tol, rot);
+            jac_round<RPL, WB, 1>(X, nrm, dsc, esc, csb, slot_col, tol, noise, rot);
             rotate_circle<RPL, WB>(X, slot_col);
           }
         }
@@ -407,7 +428,7 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
         constexpr int U = (WB < QTT_JAC_UNROLL) ? WB : QTT_JAC_UNROLL;
 #pragma unroll 1
         for (int u = 0; u < WB; u += U) {
-          cross_rounds<RPL, WB, 0, U>(X, nrm, dsc, esc, csb, slot_col, tol, rot);
+          cross_rounds<RPL, WB, 0, U>(X, nrm, dsc, esc, csb, slot_col, tol, noise, rot);
           if constexpr (U < WB) rotate_Jn<RPL, WB, U>(X, slot_col);
         }
       }
@@ -440,7 +461,7 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
     // nothing.  Check that directly on the Gram matrix (DMMA, ~1/10 of a sweep) with the same
     // threshold as the sweep's own test (whose register dot products carry rounding of the
     // same ~sqrt(m) eps order); a failed check just runs the sweep.
-    if (!(any & 2) && gram_converged<NW, RPL>(A, 2 * NW * WB, tol, scratch, flag)) { ++sweep; break; }
+    if (!(any & 2) && gram_converged<NW, RPL>(A, 2 * NW * WB, tol, noise, scratch, flag)) { ++sweep; break; }
 #endif
   }
   return sweep;
@@ -449,10 +470,10 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch) {
 // Dispatch on the padded sizes: RPL = ceil(m/32) in {1,2,4}, WB = ceil(p/(2 NW)) (powers of 2,
 // 2*NW*WB <= 128 columns).  The caller zero-pads rows to 32*RPL and columns to 2*NW*WB.
 template <int NW>
-__device__ __forceinline__ int jacobi_dispatch(double *A, int m, int p, int *flag, double *nrm_all) {
+__device__ __forceinline__ int jacobi_dispatch(double *A, int m, int p, int *flag, double *nrm_all, bool noise_ok) {
   const int rpl = (m <= 32) ? 1 : (m <= 64) ? 2 : 4;
   const int wb = (p <= 2 * NW) ? 1 : (p <= 4 * NW) ? 2 : (p <= 8 * NW) ? 4 : 8;
-#define QTT_JAC(R, W) if (rpl == R && wb == W) return jacobi_blocked<R, W, NW>(A, m, flag, nrm_all);
+#define QTT_JAC(R, W) if (rpl == R && wb == W) return jacobi_blocked<R, W, NW>(A, m, flag, nrm_all, noise_ok);
   QTT_JAC(1, 1) QTT_JAC(1, 2) QTT_JAC(1, 4)
   QTT_JAC(2, 1) QTT_JAC(2, 2) QTT_JAC(2, 4)
   QTT_JAC(4, 1) QTT_JAC(4, 2) QTT_JAC(4, 4)

@@ -369,6 +369,8 @@ struct JacArgs {
   double *A;               // m x p column-major, ld m
   GridBar *bar;
   int *flags;              // [3] rotating 'rotated in sweep s' flags
+  double *part;            // [NB/2] per-block-pair squared norms (sweep 0) -> ||A||_F^2
+  int noise_ok;            // eps > 1e-14: noise-level columns are truncated anyway (rot_pair)
   int G, WB;               // CTAs, block width (columns)
   int *sweeps_out;
   int *status;
@@ -376,7 +378,12 @@ struct JacArgs {
 
 // One Jacobi pair (one warp): exact dot product, column norms nrm_i / nrm_j carried in shared
 // memory by the rotation identities (exact refresh on cancellation, LAPACK dgesvj practice),
-// division-free MUFU-seeded angle (same formulas as the small path, jacobi.cuh).
+// division-free MUFU-seeded angle (same formulas as the small path, jacobi.cuh).  Pairs with
+// a column at rounding-noise level (|a|^2 <= noise = eps^2 ||A||_F^2) are left alone: their
+// relative orthogonality is below what fp64 can resolve, rotating them moves O(eps ||A||)
+// mass, and they would otherwise keep the sweeps going (cfg4's rank-deficient sites).  Only
+// when the truncation eps > 1e-14 guarantees such columns are discarded (eps = 0 -- the
+// exact a1 sweeps -- keeps them, and then they must come out orthonormal).
 __device__ __forceinline__ double col_norm2(const double *c, int m) {
   const int lane = threadIdx.x & 31;
   double s = 0.0;
@@ -385,13 +392,13 @@ __device__ __forceinline__ double col_norm2(const double *c, int m) {
 }
 
 __device__ __forceinline__ void rot_pair(double *ci, double *cj, double *nrm_i, double *nrm_j, int m, double tol,
-                                         int &rot) {
+                                         double noise, int &rot) {
   const int lane = threadIdx.x & 31;
   double ga = 0.0;
   for (int r = lane; r < m; r += 32) ga = fma(ci[r], cj[r], ga);
   ga = warp_sum(ga);
   const double al = *nrm_i, be = *nrm_j;
-  if (al > 0.0 && be > 0.0 && ga * ga > (tol * tol) * (al * be)) {
+  if (al > noise && be > noise && ga * ga > (tol * tol) * (al * be)) {
     const double d = be - al, g2 = ga + ga;
     const double y = fast_rsqrt(fma(d, d, g2 * g2));
     const double c2 = fma(0.5 * fabs(d), y, 0.5);
@@ -421,6 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
   double *S = smj;                                      // [2*WB][m]
   double *nrmS = S + (size_t)2 * WB * m;                // [2*WB] column norms of the loaded blocks
   __shared__ int s_rot;
+  double noise = 0.0;                                   // eps^2 ||A||_F^2, known after block round 0
   int sweep = 0;
   for (; sweep < 60; ++sweep) {
     // 3 rotating flags: slot s%3 collects "rotated in sweep s".  Slot (s+1)%3 was last read at
@@ -444,6 +452,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
           if ((tid & 31) == 0) nrmS[c] = v;
         }
         __syncthreads();
+        if (sweep == 0 && r == 0 && tid == 0) {                 // this pair's share of ||A||_F^2
+          double sq = 0.0;
+          for (int c = 0; c < 2 * WB; ++c) sq += nrmS[c];
+          a.part[t] = sq;
+        }
         if (r == 0 && WB > 1) {           // intra-block pairs (circle method on WB players)
           for (int u = 0; u < WB - 1; ++u) {
             for (int pr = warp; pr < WB; pr += kWarps) {
@@ -451,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
               const int k1 = tt, k2 = WB - 1 - tt;
               const int i = base + ((k1 == 0) ? 0 : 1 + (k1 - 1 + u) % (WB - 1));
               const int j = base + ((k2 == 0) ? 0 : 1 + (k2 - 1 + u) % (WB - 1));
-              rot_pair(S + (size_t)i * m, S + (size_t)j * m, nrmS + i, nrmS + j, m, tol, rot);
+              rot_pair(S + (size_t)i * m, S + (size_t)j * m, nrmS + i, nrmS + j, m, tol, noise, rot);
             }
             __syncthreads();
           }
@@ -459,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
         for (int sft = 0; sft < WB; ++sft) {     // cross pairs (a, WB + (a+sft)%WB)
           for (int pr = warp; pr < WB; pr += kWarps)
             rot_pair(S + (size_t)pr * m, S + (size_t)(WB + (pr + sft) % WB) * m, nrmS + pr,
-                     nrmS + WB + (pr + sft) % WB, m, tol, rot);
+                     nrmS + WB + (pr + sft) % WB, m, tol, noise, rot);
           __syncthreads();
         }
         for (int idx = tid; idx < 2 * WB * m; idx += kThreads) {
@@ -470,6 +483,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
         __syncthreads();
       }
       grid_sync(a.bar, a.G, 11);
+      if (sweep == 0 && r == 0) {                               // every block was in round 0 once
+        double tot = 0.0;
+        for (int t = 0; t < NB / 2; ++t) tot += __ldcg(a.part + t);     // fixed order
+        noise = a.noise_ok ? DBL_EPSILON * DBL_EPSILON * tot : 0.0;
+      }
     }
     if (tid == 0) s_rot = 0;
     __syncthreads();
@@ -810,7 +828,8 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
     // a4
     {
       JacArgs ja;
-      ja.dims = Bf.dims; ja.A = Bf.A; ja.bar = Bf.bar + 1; ja.flags = Bf.flags; ja.G = P.Gjac; ja.WB = P.WB;
+      ja.dims = Bf.dims; ja.A = Bf.A; ja.bar = Bf.bar + 1; ja.flags = Bf.flags; ja.part = Bf.part; ja.G = P.Gjac; ja.WB = P.WB;
+      ja.noise_ok = io.eps > 1e-14;
       ja.sweeps_out = io.sweeps ? io.sweeps + q : Bf.sweeps_scratch; ja.status = io.status;
       QTT_CUDA_TRY(cudaMemsetAsync(Bf.flags, 0, sizeof(int) * 3, s));
       qtt_status_t st = coop_launch((const void *)k_jacobi_coop, P.Gjac, P.jac_smem, &ja, s);
