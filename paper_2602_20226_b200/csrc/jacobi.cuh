@@ -32,9 +32,6 @@ __device__ unsigned long long g_jprof[4];
 #define QTT_JPROF_T(v)
 #define QTT_JPROF_ADD(i, d)
 #endif
-#ifndef QTT_JAC_STAGGER
-#define QTT_JAC_STAGGER 0
-#endif
 #ifndef QTT_JAC_SCALED
 #define QTT_JAC_SCALED 0
 #endif
@@ -409,12 +406,6 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch, bool
       if (lane < 2 * WB) { slot_col[lane] = lane; dsc[lane] = 1.0; esc[lane] = 1.0; }
       __syncwarp();
       warp_norms<RPL, WB>(X, nrm, dsc, slot_col);
-#if QTT_JAC_STAGGER
-      if (warp >= NW / 2) {      // experiment: offset the two warps of each SM sub-partition
-        const long long t0 = clock64();
-        while (clock64() - t0 < QTT_JAC_STAGGER) { }
-      }
-#endif
       if constexpr (WB > 1) {
         if (r == 0) {
 #pragma unroll 1
