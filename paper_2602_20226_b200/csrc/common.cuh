@@ -111,17 +111,36 @@ __device__ void cta_gemm(int M, int N, int K, FA A, FB B, FS store, double *sm) 
 // quadratic steps give ~1e-24 << 2^-53: full fp64 accuracy for the normal range used here.
 // (Rotation parameters need c^2+s^2 = 1 to working precision, which s = c*t with
 // c = rsqrt(1+t^2) guarantees.)
+#ifndef QTT_RSQRT_HALLEY
+#define QTT_RSQRT_HALLEY 1
+#endif
+
 __device__ __forceinline__ double fast_rcp(double x) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#if QTT_RSQRT_HALLEY
+  // one third-order step y (1 + e + e^2), e = 1 - x y: error ~e^3 ~ 1e-18 << 2^-53
+  const double e = fma(-x, y, 1.0);
+  return fma(y, fma(e, e, e), y);
+#else
   double e = fma(-x, y, 1.0);
   y = fma(y, e, y);
   e = fma(-x, y, 1.0);
   return fma(y, e, y);
+#endif
 }
 __device__ __forceinline__ double fast_rsqrt(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#if QTT_RSQRT_HALLEY
+  // one third-order step: y (1 + e/2 + 3e^2/8), e = 1 - x y^2; seed error <= 1e-6 leaves
+  // ~(5/16) e^3 ~ 3e-19 << 2^-53 -- one dependent step shorter than two Newton steps
+  const double h = x * y;
+  const double e = fma(-h, y, 1.0);
+  const double t = fma(0.375, e, 0.5);
+  const double ye = y * e;
+  return fma(ye, t, y);
+#else
 #pragma unroll
   for (int it = 0; it < 2; ++it) {
     const double h = x * y;
@@ -129,6 +148,7 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
     y = fma(0.5 * y, e, y);
   }
   return y;
+#endif
 }
 
 // LAPACK dlarfg convention: x = [alpha; x2], ||x2||^2 = xnorm2.  Returns tau and beta and

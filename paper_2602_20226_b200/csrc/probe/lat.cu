@@ -133,3 +133,25 @@ extern "C" int qtt_probe_tput(double *out, int iters, int blocks, void *stream) 
   k_tput<<<blocks, 256, 0, (cudaStream_t)stream>>>(out, iters);
   return (int)cudaGetLastError();
 }
+
+// accuracy of the one-step Halley rsqrt used by the rotation parameters (common.cuh)
+__global__ void k_rsqrt_err(double *out, int n) {
+  double er = 0.0;
+  for (int i = threadIdx.x + blockIdx.x * blockDim.x; i < n; i += blockDim.x * gridDim.x) {
+    const double e = -40.0 + 80.0 * ((double)i + 0.5) / n;
+    const double x = exp2(e) * (1.0 + 0.37 * sin((double)i));
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double h = x * y, ee = fma(-h, y, 1.0), t = fma(0.375, ee, 0.5), ye = y * ee;
+    y = fma(ye, t, y);
+    er = fmax(er, fabs(y * sqrt(x) - 1.0));
+  }
+  for (int o = 16; o > 0; o >>= 1) er = fmax(er, __shfl_xor_sync(0xffffffffu, er, o));
+  if ((threadIdx.x & 31) == 0) atomicMax((unsigned long long *)out, (unsigned long long)__double_as_longlong(er));
+}
+
+extern "C" int qtt_probe_rsqrt_err(double *out, void *stream) {
+  cudaMemsetAsync(out, 0, sizeof(double), (cudaStream_t)stream);
+  k_rsqrt_err<<<64, 256, 0, (cudaStream_t)stream>>>(out, 1 << 22);
+  return (int)cudaGetLastError();
+}

@@ -18,3 +18,7 @@ for _ in range(2):
 torch.cuda.synchronize()
 v = out.cpu().tolist()
 print({"shfl32_cycles_per_instr_per_SM": v[0], "lds64_bcast_cycles_per_instr_per_SM": v[1]})
+out.zero_()
+lib.qtt_probe_rsqrt_err(ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(s.cuda_stream))
+torch.cuda.synchronize()
+print({"halley_rsqrt_max_rel_err": out[0].item()})
