@@ -183,7 +183,7 @@ struct QrArgs {
   double *part;        // [G][kNb * mcap]  partial sums
   double *wtot;        // [kNb * mcap]     reduced W
   double *gram;        // [kNb * kNb]      reduced Y^T Y
-  double *bc;          // broadcast scalars: [0] alpha
+  double *bc;          // broadcast row-j values of the panel columns [2][32] (column parity)
   GridBar *bar;
   int G, RB, mcap;
 };
@@ -213,57 +213,54 @@ __global__ void __launch_bounds__(kThreads, 1) k_qr_coop(QrArgs a) {
       P[cc * a.RB + i] = a.Tw[(size_t)(j0 + cc) * n + r0 + i];
     }
     __syncthreads();
-    // norm partial of column j0
+    // Column steps with ONE grid barrier each: every CTA reduces, over its rows r > j, the
+    // products x_j . x_cc for cc >= jj (cc == jj: the squared norm below the diagonal); the
+    // owner of row j publishes x_cc[j].  Then v_j . x_cc = x_cc[j] + scale * sum_{r>j} x_j x_cc
+    // (v_j = [1; scale x_j(r > j)]) needs no second reduction.  part / bc are double-buffered
+    // by column parity (a slot is rewritten two barriers later, after every CTA read it).
     for (int jj = 0; jj < nb; ++jj) {
-      const int j = j0 + jj;
-      {
-        double s = 0.0;
-        for (int i = tid; i < nr; i += kThreads)
-          if (r0 + i > j) s = fma(P[jj * a.RB + i], P[jj * a.RB + i], s);
-        s = block_sum_l(s, red);
-        if (tid == 0) {
-          a.part[(size_t)g * kNb * a.mcap] = s;
-          if (j >= r0 && j < r1) a.bc[0] = P[jj * a.RB + (j - r0)];
+      const int j = j0 + jj, slot = (j & 1) * 32;
+      for (int cc = jj + warp; cc < nb; cc += kWarps) {
+        double d = 0.0;
+        for (int i = lane; i < nr; i += 32)
+          if (r0 + i > j) d = fma(P[jj * a.RB + i], P[cc * a.RB + i], d);
+        d = warp_sum(d);
+        if (lane == 0) {
+          a.part[(size_t)g * kNb * a.mcap + slot + cc] = d;
+          if (j >= r0 && j < r1) a.bc[slot + cc] = P[cc * a.RB + (j - r0)];
         }
       }
       grid_sync(a.bar, G, 1);
       double tj, beta, scale;
       {
         double s = 0.0;
-        for (unsigned gg = 0; gg < G; ++gg) s += a.part[(size_t)gg * kNb * a.mcap];
-        householder(a.bc[0], s, tj, beta, scale);
+        for (unsigned gg = 0; gg < G; ++gg) s += __ldcg(a.part + (size_t)gg * kNb * a.mcap + slot + jj);
+        householder(__ldcg(a.bc + slot + jj), s, tj, beta, scale);
       }
       if (tid == 0) tau[jj] = tj;
+      if (tid < kNb) {
+        double w = 0.0;
+        if (tid > jj && tid < nb && tj != 0.0) {
+          double sd = 0.0;
+          for (unsigned gg = 0; gg < G; ++gg) sd += __ldcg(a.part + (size_t)gg * kNb * a.mcap + slot + tid);
+          w = tj * fma(scale, sd, __ldcg(a.bc + slot + tid));
+        }
+        dots[tid] = w;
+      }
+      __syncthreads();
+      // per row (one thread owns a row of the panel): trailing panel columns -= w_cc v, then
       // v: rows > j scaled; row j -> beta (R diagonal), v_j = 1 implicit
       for (int i = tid; i < nr; i += kThreads) {
         const int r = r0 + i;
-        if (r > j) P[jj * a.RB + i] *= scale;
-        else if (r == j) P[jj * a.RB + i] = beta;
-      }
-      __syncthreads();
-      // dots with the remaining panel columns: sum_{r >= j} v_r P[cc][r]
-      for (int cc = jj + 1 + warp; cc < nb; cc += kWarps) {
-        double s = 0.0;
-        for (int i = lane; i < nr; i += 32) {
-          const int r = r0 + i;
-          if (r > j) s = fma(P[jj * a.RB + i], P[cc * a.RB + i], s);
-          else if (r == j) s += P[cc * a.RB + i];
+        const double x = P[jj * a.RB + i];
+        if (r > j) {
+          const double v = x * scale;
+          for (int cc = jj + 1; cc < nb; ++cc) P[cc * a.RB + i] = fma(-dots[cc], v, P[cc * a.RB + i]);
+          P[jj * a.RB + i] = v;
+        } else if (r == j) {
+          for (int cc = jj + 1; cc < nb; ++cc) P[cc * a.RB + i] -= dots[cc];
+          P[jj * a.RB + i] = beta;
         }
-        s = warp_sum(s);
-        if (lane == 0) a.part[(size_t)g * kNb * a.mcap + 1 + cc] = s;
-      }
-      grid_sync(a.bar, G, 2);
-      if (tid < kNb) {
-        double s = 0.0;
-        if (tid > jj && tid < nb)
-          for (unsigned gg = 0; gg < G; ++gg) s += a.part[(size_t)gg * kNb * a.mcap + 1 + tid];
-        dots[tid] = tj * s;
-      }
-      __syncthreads();
-      for (int idx = tid; idx < (nb - jj - 1) * nr; idx += kThreads) {
-        const int cc = jj + 1 + idx / nr, i = idx % nr, r = r0 + i;
-        if (r > j) P[cc * a.RB + i] = fma(-dots[cc], P[jj * a.RB + i], P[cc * a.RB + i]);
-        else if (r == j) P[cc * a.RB + i] -= dots[cc];
       }
       __syncthreads();
     }
@@ -719,7 +716,7 @@ static qtt_status_t plan_sweep(int L, const std::vector<int> &d, const std::vect
   P.off_part = take(8 * ((size_t)P.Gqr * kNb * P.mcap + (size_t)P.Gqr * kNb * kNb + 16));
   P.off_wtot = take(8 * (size_t)kNb * P.mcap);
   P.off_gram = take(8 * kNb * kNb);
-  P.off_bc = take(8 * 16);
+  P.off_bc = take(8 * 64);
   P.off_s2 = take(8 * P.pcap);
   P.off_perm = take(4 * P.pcap);
   P.off_flags = take(4 * 4);
