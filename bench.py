@@ -399,8 +399,14 @@ def run_reference(args, rank, world):
     """--impl reference: the CPU oracle (as it stands) on the host cores, same workload/metric."""
     if rank != 0:
         return
+    # the line carries the GPU arm's config (full workload); each step times a bounded sample
+    # of it (the first members of rank 0's shard), described in cpu_baseline.sample
+    full_members = args.members_per_gpu
     args.members_per_gpu = max(1, args.cpu_members // 4) if args.workload == "cfg5" else 1
     subs, kind, probs, xs, ops, cfg = build_workload(args, 0)
+    if args.workload == "cfg5":
+        cfg = dict(cfg, members_per_gpu=full_members, global_batch=full_members * max(world, 1),
+                   parallelism=f"dp{max(world, 1)} (members sharded, 1 all-reduce/step)")
     for _ in range(args.warmup):
         oracle_sample(kind, probs, 1)
     vals = []
@@ -414,7 +420,8 @@ def run_reference(args, rank, world):
     L = len(probs[0].x.cores)
     line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "scaling": "weak" if args.workload == "cfg5" else "replicas", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators, BASELINE.json configs)", "impl": "reference",
             "config": cfg,
             "cpu_baseline": dict(info, value=round(value, 3),
                                  sample=f"each step: {len(probs)} members x {L} sites of the workload (oracle)"),

@@ -992,7 +992,9 @@ extern "C" int qtt_debug_jprof(unsigned long long *host, int reset) {
 extern "C" {
 
 const char *qtt_last_error(void) { return qtt::g_err; }
-const char *qtt_version(void) { return "libqtt 0.1 (sm_100a, fp64 zip-up small-member path)"; }
+const char *qtt_version(void) {
+  return "libqtt 0.2 (sm_100a; fp64 zip-up: small- and large-member paths; fp32 variant with 3xTF32 tcgen05 contractions)";
+}
 
 qtt_status_t qtt_zipup_capacity(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
                                 int32_t max_rank, int32_t *cap) {
