@@ -366,6 +366,7 @@ struct JacArgs {
   double *A;               // m x p column-major, ld m
   GridBar *bar;
   int *flags;              // [3] rotating 'rotated in sweep s' flags
+  int *ver;                // [NB] block versions: block b holds the result of global round ver[b]-1
   double *part;            // [NB/2] per-block-pair squared norms (sweep 0) -> ||A||_F^2
   int noise_ok;            // eps > 1e-14: noise-level columns are truncated anyway (rot_pair)
   int G, WB;               // CTAs, block width (columns)
@@ -434,9 +435,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
     if (g == 0 && tid == 0) a.flags[(sweep + 1) % 3] = 0;
     int rot = 0;
     for (int r = 0; r < NB - 1; ++r) {
+      const int R = sweep * (NB - 1) + r;          // global block round
       for (int t = g; t < NB / 2; t += a.G) {
         const int I = (t == 0) ? 0 : 1 + (t - 1 + r) % (NB - 1);
         const int J = 1 + (NB - 2 - t + r) % (NB - 1);
+        // dataflow instead of a grid barrier per block round: wait until both blocks carry the
+        // result of round R - 1 (their producers pulled earlier rounds, so no deadlock)
+        if (tid == 0) {
+          int v;
+          long long spins = 0;
+          do {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(a.ver + I) : "memory");
+            if (v >= R) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(a.ver + J) : "memory");
+            if (v < R) __nanosleep(32);
+            if (++spins > (1LL << 26)) { atomicOr(a.status, ST_NOCONV); break; }   // report, do not hang
+          } while (v < R);
+          __threadfence();
+        }
+        __syncthreads();
         // load the two blocks (zero columns beyond p)
         for (int idx = tid; idx < 2 * WB * m; idx += kThreads) {
           const int c = idx / m, row = idx % m;
@@ -478,8 +494,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
           if (col < p) a.A[(size_t)col * m + row] = S[idx];
         }
         __syncthreads();
+        if (tid == 0) {
+          __threadfence();
+          asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a.ver + I), "r"(R + 1) : "memory");
+          asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a.ver + J), "r"(R + 1) : "memory");
+        }
       }
-      grid_sync(a.bar, a.G, 11);
+      if (sweep == 0 && r == 0) grid_sync(a.bar, a.G, 11);     // ||A||_F^2 partials complete
       if (sweep == 0 && r == 0) {                               // every block was in round 0 once
         double tot = 0.0;
         for (int t = 0; t < NB / 2; ++t) tot += __ldcg(a.part + t);     // fixed order
@@ -645,7 +666,7 @@ __global__ void k_mirror_l(MirrorL a) {
 
 struct SweepBufs {
   double *G, *X, *T, *Tw, *A, *part, *wtot, *gram, *bc, *s2;
-  int *perm, *flags, *sweeps_scratch;
+  int *perm, *flags, *ver, *sweeps_scratch;
   GridBar *bar;
   SiteDims *dims;
   GemmSpec *spec;
@@ -679,7 +700,7 @@ struct SweepPlan {
   int Gqr, RB, Gjac, WB;
   size_t qr_smem, jac_smem;
   size_t off_G, off_X, off_T, off_Tw, off_A, off_part, off_wtot, off_gram, off_bc, off_s2, off_perm, off_flags,
-      off_sw, off_bar, off_dims, off_spec, total;
+      off_ver, off_sw, off_bar, off_dims, off_spec, total;
 };
 
 static qtt_status_t plan_sweep(int L, const std::vector<int> &d, const std::vector<int> &dj, const std::vector<int> &xr,
@@ -720,6 +741,7 @@ static qtt_status_t plan_sweep(int L, const std::vector<int> &d, const std::vect
   P.off_s2 = take(8 * P.pcap);
   P.off_perm = take(4 * P.pcap);
   P.off_flags = take(4 * 4);
+  P.off_ver = take(4 * ((size_t)P.pcap + 2));
   P.off_sw = take(4 * 4);
   P.off_bar = take(sizeof(GridBar) * 2);
   P.off_dims = take(sizeof(SiteDims));
@@ -762,6 +784,7 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
   Bf.Tw = (double *)(ws + P.off_Tw); Bf.A = (double *)(ws + P.off_A); Bf.part = (double *)(ws + P.off_part);
   Bf.wtot = (double *)(ws + P.off_wtot); Bf.gram = (double *)(ws + P.off_gram); Bf.bc = (double *)(ws + P.off_bc);
   Bf.s2 = (double *)(ws + P.off_s2); Bf.perm = (int *)(ws + P.off_perm); Bf.flags = (int *)(ws + P.off_flags);
+  Bf.ver = (int *)(ws + P.off_ver);
   Bf.sweeps_scratch = (int *)(ws + P.off_sw); Bf.bar = (GridBar *)(ws + P.off_bar);
   Bf.dims = (SiteDims *)(ws + P.off_dims); Bf.spec = (GemmSpec *)(ws + P.off_spec);
   static bool attr = false;
@@ -825,10 +848,11 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
     // a4
     {
       JacArgs ja;
-      ja.dims = Bf.dims; ja.A = Bf.A; ja.bar = Bf.bar + 1; ja.flags = Bf.flags; ja.part = Bf.part; ja.G = P.Gjac; ja.WB = P.WB;
+      ja.dims = Bf.dims; ja.A = Bf.A; ja.bar = Bf.bar + 1; ja.flags = Bf.flags; ja.ver = Bf.ver; ja.part = Bf.part; ja.G = P.Gjac; ja.WB = P.WB;
       ja.noise_ok = io.eps > 1e-14;
       ja.sweeps_out = io.sweeps ? io.sweeps + q : Bf.sweeps_scratch; ja.status = io.status;
       QTT_CUDA_TRY(cudaMemsetAsync(Bf.flags, 0, sizeof(int) * 3, s));
+      QTT_CUDA_TRY(cudaMemsetAsync(Bf.ver, 0, sizeof(int) * (P.pcap + 2), s));
       qtt_status_t st = coop_launch((const void *)k_jacobi_coop, P.Gjac, P.jac_smem, &ja, s);
       if (st != QTT_OK) return st;
     }
