@@ -268,6 +268,75 @@ class ZipupPlan:
                            self.workspace, self.cycles)
 
 
+class HostPipeline:
+    """qtt_zipup on batches that live in (pinned) host memory, `depth` batches in flight.
+
+    Buffer set i = k % depth holds batch k's device inputs and its ZipupPlan (outputs +
+    workspace).  The host->device copy of batch k runs on a copy stream, the zip-up on the
+    compute stream, the device->host copy of its results on a second copy stream; events
+    order each set's reuse, so the copies of batches k+1 and k-1 overlap the zip-up of batch k.
+    Host buffers given to step() must stay untouched until finish() (or the batch's d2h event).
+    """
+
+    def __init__(self, subscripts: str, op: Optional[DeviceTrains], x: DeviceTrains, eps: float,
+                 max_rank: int, depth: int = 2, flags: int = 0, device="cuda"):
+        def clone(t):
+            return None if t is None else DeviceTrains([torch.empty_like(c) for c in t.cores], list(t.ranks),
+                                                        list(t.d_out), None if t.d_in is None else list(t.d_in))
+        self.sets = []
+        for _ in range(depth):
+            xi, oi = clone(x), clone(op)
+            self.sets.append((oi, xi, ZipupPlan(subscripts, oi, xi, eps, max_rank, flags, device=device)))
+        self.h2d = torch.cuda.Stream(device=device)
+        self.d2h = torch.cuda.Stream(device=device)
+        self.comp_done = [torch.cuda.Event() for _ in range(depth)]
+        self.d2h_done = [torch.cuda.Event() for _ in range(depth)]
+        self.used = [False] * depth
+        self.k = 0
+
+    def begin(self, stream=None):
+        """Order both copy streams after everything already enqueued on `stream`."""
+        s = stream if stream is not None else torch.cuda.current_stream()
+        self.h2d.wait_stream(s)
+        self.d2h.wait_stream(s)
+
+    def step(self, host_x: Sequence[torch.Tensor], host_op: Optional[Sequence[torch.Tensor]],
+             host_out: Sequence[torch.Tensor], host_ranks: torch.Tensor, host_delta2: torch.Tensor,
+             host_norm2: torch.Tensor, stream=None) -> ZipupResult:
+        s = stream if stream is not None else torch.cuda.current_stream()
+        i = self.k % len(self.sets)
+        op, x, plan = self.sets[i]
+        with torch.cuda.stream(self.h2d):
+            if self.used[i]:
+                self.h2d.wait_event(self.comp_done[i])          # batch k-depth has read set i's inputs
+            for dst, src in zip(x.cores, host_x):
+                dst.copy_(src, non_blocking=True)
+            if op is not None:
+                for dst, src in zip(op.cores, host_op):
+                    dst.copy_(src, non_blocking=True)
+        s.wait_stream(self.h2d)
+        if self.used[i]:
+            s.wait_event(self.d2h_done[i])                      # batch k-depth's results are out
+        res = plan.run(op, x, stream=s)
+        self.comp_done[i].record(s)
+        with torch.cuda.stream(self.d2h):
+            self.d2h.wait_event(self.comp_done[i])
+            for dst, src in zip(host_out, plan.out.cores):
+                dst.copy_(src, non_blocking=True)
+            host_ranks.copy_(res.ranks, non_blocking=True)
+            host_delta2.copy_(res.delta2, non_blocking=True)
+            host_norm2.copy_(res.norm2, non_blocking=True)
+            self.d2h_done[i].record(self.d2h)
+        self.used[i] = True
+        self.k += 1
+        return res
+
+    def finish(self, stream=None):
+        """Make `stream` wait for every outstanding device->host copy."""
+        s = stream if stream is not None else torch.cuda.current_stream()
+        s.wait_stream(self.d2h)
+
+
 def zipup(subscripts: str, op: Optional[DeviceTrains], x: DeviceTrains, eps: float, max_rank: int,
           flags: int = 0, sigma_stride: int = 0, stream=None) -> ZipupResult:
     return ZipupPlan(subscripts, op, x, eps, max_rank, flags, sigma_stride, sweeps=True).run(op, x, stream)

@@ -198,3 +198,45 @@ def test_round_redundant_and_max_rank(lib):
         assert ranks == tt.ranks_of(ref)
         yv, rv = tt.to_dense_vector(lib.member_cores(rr.out, ranks, 0)), tt.to_dense_vector(ref)
         assert np.linalg.norm(yv - rv) <= 1e-10 * np.linalg.norm(rv)
+
+
+def test_host_pipeline_batches(lib):
+    """qtt.HostPipeline: three different host batches streamed through two buffer sets; each
+    batch's host-side results (copied back by the pipeline) match the oracle."""
+    import torch
+    dims = [2] * 10
+    batches = []
+    for k in range(3):
+        xs = [gen.random_mps(dims, 12, np.random.default_rng(900 + 10 * k + b)).cores for b in range(2)]
+        ops = [gen.random_mpo(dims, 3, np.random.default_rng(950 + 10 * k + b), 0.5).cores for b in range(2)]
+        batches.append((xs, ops))
+    stack = lambda ts: [np.stack([t[q] for t in ts]) for q in range(len(dims))]
+    xd = lib.to_device(stack(batches[0][0]))
+    od = lib.to_device(stack(batches[0][1]), mpo=True)
+    pipe = lib.HostPipeline("ij,j->i", od, xd, 1e-10, 16, depth=2)
+    plan0 = pipe.sets[0][2]
+    hosts = []
+    pipe.begin()
+    for xs, ops in batches:
+        hx = [torch.from_numpy(c).pin_memory() for c in stack(xs)]
+        ho = [torch.from_numpy(c).pin_memory() for c in stack(ops)]
+        hout = [torch.empty(c.shape, dtype=c.dtype).pin_memory() for c in plan0.out.cores]
+        hr = torch.empty(tuple(plan0.ranks.shape), dtype=torch.int32).pin_memory()
+        hd = torch.empty(tuple(plan0.delta2.shape), dtype=torch.float64).pin_memory()
+        hn = torch.empty(tuple(plan0.norm2.shape), dtype=torch.float64).pin_memory()
+        pipe.step(hx, ho, hout, hr, hd, hn)
+        hosts.append((hx, ho, hout, hr, hd, hn))
+    pipe.finish()
+    torch.cuda.synchronize()
+    from oracle.zipup import zipup as ozip
+    from oracle import tt
+    for (xs, ops), (_, _, hout, hr, hd, hn) in zip(batches, hosts):
+        for b in range(2):
+            ranks = hr[b].tolist()
+            cores = [hout[q][b].reshape(-1)[:ranks[q] * 2 * ranks[q + 1]].numpy().reshape(ranks[q], 2, ranks[q + 1])
+                     for q in range(len(dims))]
+            ref = ozip("matvec", ops[b], xs[b], 1e-10, 16)
+            assert ranks == ref["ranks"]
+            y, yr = tt.to_dense_vector(cores), tt.to_dense_vector(ref["cores"])
+            assert np.linalg.norm(y - yr) <= 1e-11 * np.linalg.norm(yr)
+            assert abs(float(hn[b]) - ref["norm"] ** 2) <= 1e-11 * ref["norm"] ** 2
