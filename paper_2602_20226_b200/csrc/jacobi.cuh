@@ -160,11 +160,15 @@ __device__ __forceinline__ void jac_round(double (&X)[2 * WB][RPL], double *nrm,
   const double g2 = ga + ga;
   // noise = eps^2 ||A||_F^2: a column at rounding-noise level is treated as converged (its
   // relative orthogonality is below fp64 resolution; see large.cu rot_pair)
-  const bool doit = (ga * ga > (tol * tol) * (al * be)) && (al > noise) && (be > noise);
   const double x2 = fma(d, d, g2 * g2);
+  // x2 >= DBL_MIN: the MUFU rsqrt seed flushes a subnormal argument to zero.  jacobi_blocked
+  // scales A so ||A||_F^2 is in [1, 4), so only columns below ~1e-150 relative can fail this
+  const bool doit = (ga * ga > (tol * tol) * (al * be)) && (al > noise) && (be > noise) && (x2 >= DBL_MIN);
 #if QTT_JAC_DIVFREE
   // same angle without a division: y = 1/sqrt(d^2 + 4 g^2), c^2 = (1 + |d| y)/2, z = 1/c,
   // s = sign(d) g y z, t = s z
+  // the angle depends on d : g only; below ~1e-280 the MUFU seed of rsqrt would flush the
+  // (subnormal) argument to zero, so tiny pairs (exact sweeps, noise = 0) are rescaled first
   const double y = doit ? fast_rsqrt(x2) : 0.0;
   const double c2 = doit ? fma(0.5 * fabs(d), y, 0.5) : 1.0;
   const double z = doit ? fast_rsqrt(c2) : 1.0;
@@ -372,6 +376,7 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch, bool
   int *slot_col = reinterpret_cast<int *>(scratch + NW * 6 * WB) + warp * 2 * WB;
   double2 *csb = reinterpret_cast<double2 *>(scratch + NW * 8 * WB + warp * 2 * WB);   // rotation broadcast
   double noise;                                                            // eps^2 ||A||_F^2
+  double scale = 1.0;
   {
     double sq = 0.0;
     for (int idx = threadIdx.x; idx < 2 * NW * WB * 32 * RPL; idx += NW * 32) {
@@ -385,7 +390,20 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch, bool
     double tot = 0.0;
 #pragma unroll
     for (int w = 0; w < NW; ++w) tot += scratch[w];             // fixed order: deterministic
+    // exact power-of-two scaling to ||A||_F^2 in [1, 4) (undone after the sweeps): keeps
+    // d^2 + 4 g^2 of every non-negligible pair clear of the subnormal range (jac_round)
+    if (tot > 0.0 && isfinite(tot)) {
+      const int e = -(ilogb(tot) >> 1);
+      if (e != 0) {
+        scale = ldexp(1.0, e);
+        tot = ldexp(tot, 2 * e);
+      }
+    }
     noise = noise_ok ? DBL_EPSILON * DBL_EPSILON * tot : 0.0;
+    __syncthreads();
+    if (scale != 1.0)
+      for (int idx = threadIdx.x; idx < 2 * NW * WB * 32 * RPL; idx += NW * 32)
+        A[(size_t)(idx / (32 * RPL)) * kLdA + idx % (32 * RPL)] *= scale;
     __syncthreads();
   }
   int sweep = 0;
@@ -454,6 +472,12 @@ __device__ int jacobi_blocked(double *A, int m, int *flag, double *scratch, bool
     // same ~sqrt(m) eps order); a failed check just runs the sweep.
     if (!(any & 2) && gram_converged<NW, RPL>(A, 2 * NW * WB, tol, noise, scratch, flag)) { ++sweep; break; }
 #endif
+  }
+  if (scale != 1.0) {
+    const double inv = 1.0 / scale;
+    for (int idx = threadIdx.x; idx < 2 * NW * WB * 32 * RPL; idx += NW * 32)
+      A[(size_t)(idx / (32 * RPL)) * kLdA + idx % (32 * RPL)] *= inv;
+    __syncthreads();
   }
   return sweep;
 }

@@ -389,23 +389,68 @@ __device__ __forceinline__ double col_norm2(const double *c, int m) {
   return warp_sum(s);
 }
 
+// Rotation of one pair given (al, be, ga); shared by the scalar and the paired-row variants.
+__device__ __forceinline__ bool rot_params(double al, double be, double ga, double tol, double noise, double &c,
+                                           double &s, double &t) {
+  if (!(al > noise && be > noise && ga * ga > (tol * tol) * (al * be))) return false;
+  double d = be - al, g = ga;
+  double x = fma(d, d, 4.0 * g * g);
+  if (x < 1e-280) {              // tiny columns (exact sweeps, noise = 0): the angle depends on
+    const double sc = fast_rcp(fmax(fabs(d), fabs(g)));  // d : g only -- rescale before the
+    d *= sc; g *= sc;                                     // flush-to-zero MUFU seed
+    x = fma(d, d, 4.0 * g * g);
+  }
+  const double y = fast_rsqrt(x);
+  const double c2 = fma(0.5 * fabs(d), y, 0.5);
+  const double z = fast_rsqrt(c2);
+  c = c2 * z;
+  s = copysign(1.0, d) * g * y * z;
+  t = s * z;
+  return true;
+}
+
 __device__ __forceinline__ void rot_pair(double *ci, double *cj, double *nrm_i, double *nrm_j, int m, double tol,
                                          double noise, int &rot) {
   const int lane = threadIdx.x & 31;
-  double ga = 0.0;
-  for (int r = lane; r < m; r += 32) ga = fma(ci[r], cj[r], ga);
+  double ga;
+  const bool paired = (m & 1) == 0;        // columns start 16-byte aligned: rows in pairs
+  if (paired) {
+    const double2 *xi = reinterpret_cast<const double2 *>(ci), *xj = reinterpret_cast<const double2 *>(cj);
+    const int n2 = m >> 1;
+    double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+    int r = lane;
+    for (; r + 32 < n2; r += 64) {          // four independent chains, two 16-byte loads per column
+      const double2 x0 = xi[r], y0 = xj[r], x1 = xi[r + 32], y1 = xj[r + 32];
+      g0 = fma(x0.x, y0.x, g0); g1 = fma(x0.y, y0.y, g1);
+      g2 = fma(x1.x, y1.x, g2); g3 = fma(x1.y, y1.y, g3);
+    }
+    if (r < n2) { const double2 x0 = xi[r], y0 = xj[r]; g0 = fma(x0.x, y0.x, g0); g1 = fma(x0.y, y0.y, g1); }
+    ga = (g0 + g1) + (g2 + g3);
+  } else {
+    double g0 = 0.0, g1 = 0.0;
+    int r = lane;
+    for (; r + 32 < m; r += 64) { g0 = fma(ci[r], cj[r], g0); g1 = fma(ci[r + 32], cj[r + 32], g1); }
+    if (r < m) g0 = fma(ci[r], cj[r], g0);
+    ga = g0 + g1;
+  }
   ga = warp_sum(ga);
   const double al = *nrm_i, be = *nrm_j;
-  if (al > noise && be > noise && ga * ga > (tol * tol) * (al * be)) {
-    const double d = be - al, g2 = ga + ga;
-    const double y = fast_rsqrt(fma(d, d, g2 * g2));
-    const double c2 = fma(0.5 * fabs(d), y, 0.5);
-    const double z = fast_rsqrt(c2);
-    const double c = c2 * z, s = copysign(1.0, d) * ga * y * z, t = s * z;
-    for (int r = lane; r < m; r += 32) {
-      const double x = ci[r], yv = cj[r];
-      ci[r] = fma(c, x, -s * yv);
-      cj[r] = fma(s, x, c * yv);
+  double c, s, t;
+  if (rot_params(al, be, ga, tol, noise, c, s, t)) {
+    if (paired) {
+      double2 *xi = reinterpret_cast<double2 *>(ci), *xj = reinterpret_cast<double2 *>(cj);
+      const int n2 = m >> 1;
+      for (int r = lane; r < n2; r += 32) {
+        const double2 x = xi[r], y = xj[r];
+        xi[r] = make_double2(fma(c, x.x, -s * y.x), fma(c, x.y, -s * y.y));
+        xj[r] = make_double2(fma(s, x.x, c * y.x), fma(s, x.y, c * y.y));
+      }
+    } else {
+      for (int r = lane; r < m; r += 32) {
+        const double x = ci[r], yv = cj[r];
+        ci[r] = fma(c, x, -s * yv);
+        cj[r] = fma(s, x, c * yv);
+      }
     }
     double al2 = fma(-t, ga, al), be2 = fma(t, ga, be);
     __syncwarp();
@@ -414,6 +459,48 @@ __device__ __forceinline__ void rot_pair(double *ci, double *cj, double *nrm_i, 
     if (lane == 0) { *nrm_i = al2; *nrm_j = be2; }
     __syncwarp();
     rot = 1;
+  }
+}
+
+// Block I of the Jacobi column partition (columns [I*WB, I*WB+WB) of the column-major m x p
+// matrix) is one contiguous run of WB*m doubles: copied with 16-byte accesses, 4 in flight
+// per thread, zero beyond column p.
+__device__ __forceinline__ void block_copy_in(double *dst, const double *A, int I, int WB, int m, int p) {
+  const int nv = max(0, min(WB, p - I * WB));
+  const long long n = (long long)nv * m, ntot = (long long)WB * m;
+  const double *src = A + (size_t)I * WB * m;
+  const int tid = threadIdx.x;
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    const double2 *s2 = reinterpret_cast<const double2 *>(src);
+    double2 *d2 = reinterpret_cast<double2 *>(dst);
+    const long long n2 = n >> 1;
+    long long i = tid;
+    for (; i + 3 * kThreads < n2; i += 4 * kThreads) {
+      const double2 v0 = __ldcg(s2 + i), v1 = __ldcg(s2 + i + kThreads), v2 = __ldcg(s2 + i + 2 * kThreads),
+                    v3 = __ldcg(s2 + i + 3 * kThreads);
+      d2[i] = v0; d2[i + kThreads] = v1; d2[i + 2 * kThreads] = v2; d2[i + 3 * kThreads] = v3;
+    }
+    for (; i < n2; i += kThreads) d2[i] = __ldcg(s2 + i);
+    if ((n & 1) && tid == 0) dst[n - 1] = __ldcg(src + n - 1);
+  } else {
+    for (long long i = tid; i < n; i += kThreads) dst[i] = __ldcg(src + i);
+  }
+  for (long long i = n + tid; i < ntot; i += kThreads) dst[i] = 0.0;
+}
+
+__device__ __forceinline__ void block_copy_out(const double *src, double *A, int I, int WB, int m, int p) {
+  const int nv = max(0, min(WB, p - I * WB));
+  const long long n = (long long)nv * m;
+  double *dst = A + (size_t)I * WB * m;
+  const int tid = threadIdx.x;
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    const double2 *s2 = reinterpret_cast<const double2 *>(src);
+    double2 *d2 = reinterpret_cast<double2 *>(dst);
+    const long long n2 = n >> 1;
+    for (long long i = tid; i < n2; i += kThreads) __stcg(d2 + i, s2[i]);
+    if ((n & 1) && tid == 0) __stcg(dst + n - 1, src[n - 1]);
+  } else {
+    for (long long i = tid; i < n; i += kThreads) __stcg(dst + i, src[i]);
   }
 }
 
@@ -426,7 +513,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
   double *S = smj;                                      // [2*WB][m]
   double *nrmS = S + (size_t)2 * WB * m;                // [2*WB] column norms of the loaded blocks
   __shared__ int s_rot;
-  double noise = 0.0;                                   // eps^2 ||A||_F^2, known after block round 0
+  __shared__ double s_red[kWarps];
+  // ||A||_F^2 over CTA slices of the m x p matrix, then an exact power-of-two scale to
+  // ||A||_F^2 in [1, 4) (applied at the round-0 block loads, undone at the end): keeps the
+  // squares in the rotation test clear of underflow for any input magnitude
+  double noise, scale = 1.0;
+  {
+    const long long n = (long long)m * p;
+    double sq = 0.0;
+    for (long long i = (long long)g * kThreads + tid; i < n; i += (long long)a.G * kThreads) {
+      const double v = __ldcg(a.A + i);
+      sq = fma(v, v, sq);
+    }
+    sq = warp_sum(sq);
+    if ((tid & 31) == 0) s_red[warp] = sq;
+    __syncthreads();
+    if (tid == 0) {
+      double b = 0.0;
+      for (int w = 0; w < kWarps; ++w) b += s_red[w];
+      a.part[g] = b;
+    }
+    grid_sync(a.bar, a.G, 11);
+    double tot = 0.0;
+    for (int t = 0; t < a.G; ++t) tot += __ldcg(a.part + t);     // fixed order: deterministic
+    if (tot > 0.0 && isfinite(tot)) {
+      const int e = -(ilogb(tot) >> 1);
+      scale = ldexp(1.0, e);
+      tot = ldexp(tot, 2 * e);
+    }
+    noise = a.noise_ok ? DBL_EPSILON * DBL_EPSILON * tot : 0.0;
+  }
   int sweep = 0;
   for (; sweep < 60; ++sweep) {
     // 3 rotating flags: slot s%3 collects "rotated in sweep s".  Slot (s+1)%3 was last read at
@@ -454,10 +570,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
         }
         __syncthreads();
         // load the two blocks (zero columns beyond p)
-        for (int idx = tid; idx < 2 * WB * m; idx += kThreads) {
-          const int c = idx / m, row = idx % m;
-          const int col = (c < WB) ? I * WB + c : J * WB + (c - WB);
-          S[idx] = (col < p) ? a.A[(size_t)col * m + row] : 0.0;
+        block_copy_in(S, a.A, I, WB, m, p);
+        block_copy_in(S + (size_t)WB * m, a.A, J, WB, m, p);
+        if (sweep == 0 && r == 0 && scale != 1.0) {             // every block is loaded once in round 0
+          __syncthreads();
+          for (int i = tid; i < 2 * WB * m; i += kThreads) S[i] *= scale;
         }
         __syncthreads();
         for (int c = warp; c < 2 * WB; c += kWarps) {            // exact norms at block load
@@ -465,11 +582,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
           if ((tid & 31) == 0) nrmS[c] = v;
         }
         __syncthreads();
-        if (sweep == 0 && r == 0 && tid == 0) {                 // this pair's share of ||A||_F^2
-          double sq = 0.0;
-          for (int c = 0; c < 2 * WB; ++c) sq += nrmS[c];
-          a.part[t] = sq;
-        }
         if (r == 0 && WB > 1) {           // intra-block pairs (circle method on WB players)
           for (int u = 0; u < WB - 1; ++u) {
             for (int pr = warp; pr < WB; pr += kWarps) {
@@ -488,23 +600,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
                      nrmS + WB + (pr + sft) % WB, m, tol, noise, rot);
           __syncthreads();
         }
-        for (int idx = tid; idx < 2 * WB * m; idx += kThreads) {
-          const int c = idx / m, row = idx % m;
-          const int col = (c < WB) ? I * WB + c : J * WB + (c - WB);
-          if (col < p) a.A[(size_t)col * m + row] = S[idx];
-        }
+        block_copy_out(S, a.A, I, WB, m, p);
+        block_copy_out(S + (size_t)WB * m, a.A, J, WB, m, p);
         __syncthreads();
         if (tid == 0) {
           __threadfence();
           asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a.ver + I), "r"(R + 1) : "memory");
           asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a.ver + J), "r"(R + 1) : "memory");
         }
-      }
-      if (sweep == 0 && r == 0) grid_sync(a.bar, a.G, 11);     // ||A||_F^2 partials complete
-      if (sweep == 0 && r == 0) {                               // every block was in round 0 once
-        double tot = 0.0;
-        for (int t = 0; t < NB / 2; ++t) tot += __ldcg(a.part + t);     // fixed order
-        noise = a.noise_ok ? DBL_EPSILON * DBL_EPSILON * tot : 0.0;
       }
     }
     if (tid == 0) s_rot = 0;
@@ -515,6 +618,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
     grid_sync(a.bar, a.G, 12);
     const int any = *((volatile int *)(a.flags + (sweep % 3)));
     if (!any) { ++sweep; break; }
+  }
+  if (scale != 1.0) {              // the last grid barrier ordered every block store before this
+    const double inv = 1.0 / scale;
+    const long long n = (long long)m * p;
+    for (long long i = (long long)g * kThreads + tid; i < n; i += (long long)a.G * kThreads)
+      __stcg(a.A + i, __ldcg(a.A + i) * inv);
   }
   if (g == 0 && tid == 0) {
     *a.sweeps_out = sweep;

@@ -112,3 +112,13 @@ def test_cfg5_full_batch_sampled_members(lib):
         cores, ranks, sig, d2, n2 = member(lib, res, b)
         p = probs[b]
         compare("matvec", p.op.cores, p.x.cores, p.eps, p.max_rank, cores, ranks, sig, d2, n2, dense=False)
+
+
+@pytest.mark.parametrize("scale", [1e-140, 1e140])
+def test_large_extreme_magnitudes(lib, scale):
+    """Large-member path (m = 256) on inputs scaled to 1e-140 / 1e+140 (cooperative Jacobi
+    prescale, c.f. test_gpu_zipup.test_extreme_magnitudes)."""
+    p = gen.cfg2(Lx=6, R=64, max_rank=128)
+    x = list(p.x.cores)
+    x[0] = x[0] * scale
+    check(lib, "matvec", p.op.cores, x, p.eps, p.max_rank)

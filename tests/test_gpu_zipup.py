@@ -240,3 +240,14 @@ def test_host_pipeline_batches(lib):
             y, yr = tt.to_dense_vector(cores), tt.to_dense_vector(ref["cores"])
             assert np.linalg.norm(y - yr) <= 1e-11 * np.linalg.norm(yr)
             assert abs(float(hn[b]) - ref["norm"] ** 2) <= 1e-11 * ref["norm"] ** 2
+
+
+@pytest.mark.parametrize("scale", [1e-140, 1e140])
+def test_extreme_magnitudes(lib, scale):
+    """Inputs scaled to 1e-140 / 1e+140 (norm^2 near the fp64 range ends): the Jacobi's
+    squared tests (g^2 vs a b) would under/overflow without its power-of-two prescale."""
+    dims = [2] * 12
+    x = gen.random_mps(dims, 16, np.random.default_rng(31)).cores
+    x[0] = x[0] * scale
+    op = gen.random_mpo(dims, 3, np.random.default_rng(32), 0.5).cores
+    check(lib, "matvec", op, x, 1e-10, 24)
