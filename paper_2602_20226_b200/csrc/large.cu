@@ -462,6 +462,81 @@ __device__ __forceinline__ void rot_pair(double *ci, double *cj, double *nrm_i, 
   }
 }
 
+// The WB cross rounds of a block pair with column a of each pair register-resident: warp w
+// (< WB) holds column w of block I as R2 double2 per lane (m <= 64 R2, m even) for all WB
+// rounds, so each round streams only the partner column WB + (w + sft) % WB through shared
+// memory (one read, one write) -- a third of the shared-memory traffic of rot_pair, which
+// bounds the rounds (128 B/clk per SM).
+#ifndef QTT_COOP_REG
+#define QTT_COOP_REG 1
+#endif
+template <int R2>
+__device__ __forceinline__ void cross_rounds_reg(double *S, double *nrmS, int WB, int m, double tol, double noise,
+                                                 int &rot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n2 = m >> 1;
+  const bool act = warp < WB;
+  double2 xa[R2];
+  double al = 0.0;
+  if (act) {
+    const double2 *src = reinterpret_cast<const double2 *>(S + (size_t)warp * m);
+#pragma unroll
+    for (int k = 0; k < R2; ++k) xa[k] = (lane + 32 * k < n2) ? src[lane + 32 * k] : make_double2(0.0, 0.0);
+    al = nrmS[warp];
+  }
+  for (int sft = 0; sft < WB; ++sft) {
+    if (act) {
+      const int jb = WB + (warp + sft) % WB;
+      double2 *yb = reinterpret_cast<double2 *>(S + (size_t)jb * m);
+      double2 yv[R2];
+#pragma unroll
+      for (int k = 0; k < R2; ++k) yv[k] = (lane + 32 * k < n2) ? yb[lane + 32 * k] : make_double2(0.0, 0.0);
+      double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+#pragma unroll
+      for (int k = 0; k < R2; k += 2) {
+        g0 = fma(xa[k].x, yv[k].x, g0); g1 = fma(xa[k].y, yv[k].y, g1);
+        if (k + 1 < R2) { g2 = fma(xa[k + 1].x, yv[k + 1].x, g2); g3 = fma(xa[k + 1].y, yv[k + 1].y, g3); }
+      }
+      const double ga = warp_sum((g0 + g1) + (g2 + g3));
+      const double be = nrmS[jb];
+      double c, s, t;
+      if (rot_params(al, be, ga, tol, noise, c, s, t)) {
+        double sa = 0.0, sb = 0.0;
+#pragma unroll
+        for (int k = 0; k < R2; ++k) {
+          const double2 x = xa[k], y = yv[k];
+          xa[k] = make_double2(fma(c, x.x, -s * y.x), fma(c, x.y, -s * y.y));
+          yv[k] = make_double2(fma(s, x.x, c * y.x), fma(s, x.y, c * y.y));
+          if (lane + 32 * k < n2) yb[lane + 32 * k] = yv[k];
+        }
+        double al2 = fma(-t, ga, al), be2 = fma(t, ga, be);
+        if (al2 < 1.5e-8 * al) {          // cancellation: exact refresh from the registers
+#pragma unroll
+          for (int k = 0; k < R2; ++k) { sa = fma(xa[k].x, xa[k].x, sa); sa = fma(xa[k].y, xa[k].y, sa); }
+          al2 = warp_sum(sa);
+        }
+        if (be2 < 1.5e-8 * be) {
+#pragma unroll
+          for (int k = 0; k < R2; ++k) { sb = fma(yv[k].x, yv[k].x, sb); sb = fma(yv[k].y, yv[k].y, sb); }
+          be2 = warp_sum(sb);
+        }
+        al = al2;
+        if (lane == 0) nrmS[jb] = be2;
+        rot = 1;
+      }
+    }
+    __syncthreads();
+  }
+  if (act) {
+    double2 *dst = reinterpret_cast<double2 *>(S + (size_t)warp * m);
+#pragma unroll
+    for (int k = 0; k < R2; ++k)
+      if (lane + 32 * k < n2) dst[lane + 32 * k] = xa[k];
+    if (lane == 0) nrmS[warp] = al;
+  }
+  __syncthreads();
+}
+
 // Block I of the Jacobi column partition (columns [I*WB, I*WB+WB) of the column-major m x p
 // matrix) is one contiguous run of WB*m doubles: copied with 16-byte accesses, 4 in flight
 // per thread, zero beyond column p.
@@ -594,12 +669,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
             __syncthreads();
           }
         }
-        for (int sft = 0; sft < WB; ++sft) {     // cross pairs (a, WB + (a+sft)%WB)
-          for (int pr = warp; pr < WB; pr += kWarps)
-            rot_pair(S + (size_t)pr * m, S + (size_t)(WB + (pr + sft) % WB) * m, nrmS + pr,
-                     nrmS + WB + (pr + sft) % WB, m, tol, noise, rot);
-          __syncthreads();
-        }
+        // cross pairs (a, WB + (a+sft)%WB), sft = 0..WB-1
+        const bool regs = QTT_COOP_REG && (m & 1) == 0 && WB <= kWarps;
+        if (regs && m <= 256) cross_rounds_reg<4>(S, nrmS, WB, m, tol, noise, rot);
+        else if (regs && m <= 512) cross_rounds_reg<8>(S, nrmS, WB, m, tol, noise, rot);
+        // (m <= 1024 in registers, R2 = 16, needs all 255 registers and measured slower on cfg4)
+        else
+          for (int sft = 0; sft < WB; ++sft) {
+            for (int pr = warp; pr < WB; pr += kWarps)
+              rot_pair(S + (size_t)pr * m, S + (size_t)(WB + (pr + sft) % WB) * m, nrmS + pr,
+                       nrmS + WB + (pr + sft) % WB, m, tol, noise, rot);
+            __syncthreads();
+          }
         block_copy_out(S, a.A, I, WB, m, p);
         block_copy_out(S + (size_t)WB * m, a.A, J, WB, m, p);
         __syncthreads();
