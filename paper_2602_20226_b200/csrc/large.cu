@@ -19,6 +19,7 @@
 // invariant).
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 #include <algorithm>
 #include <vector>
@@ -367,7 +368,8 @@ struct JacArgs {
   GridBar *bar;
   int *flags;              // [3] rotating 'rotated in sweep s' flags
   int *ver;                // [NB] block versions: block b holds the result of global round ver[b]-1
-  double *part;            // [NB/2] per-block-pair squared norms (sweep 0) -> ||A||_F^2
+  double *part;            // [G] per-CTA partial sums of ||A||_F^2
+  double *nrm;             // [p] carried squared column norms between block rounds
   int noise_ok;            // eps > 1e-14: noise-level columns are truncated anyway (rot_pair)
   int G, WB;               // CTAs, block width (columns)
   int *sweeps_out;
@@ -652,9 +654,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
           for (int i = tid; i < 2 * WB * m; i += kThreads) S[i] *= scale;
         }
         __syncthreads();
-        for (int c = warp; c < 2 * WB; c += kWarps) {            // exact norms at block load
-          const double v = col_norm2(S + (size_t)c * m, m);
-          if ((tid & 31) == 0) nrmS[c] = v;
+        if (r == 0) {                     // exact norms once per sweep (every block is in round 0)
+          for (int c = warp; c < 2 * WB; c += kWarps) {
+            const double v = col_norm2(S + (size_t)c * m, m);
+            if ((tid & 31) == 0) nrmS[c] = v;
+          }
+        } else if (tid < 2 * WB) {        // otherwise the norms carried with the columns
+          const int col = (tid < WB) ? I * WB + tid : J * WB + tid - WB;
+          nrmS[tid] = (col < p) ? __ldcg(a.nrm + col) : 0.0;
         }
         __syncthreads();
         if (r == 0 && WB > 1) {           // intra-block pairs (circle method on WB players)
@@ -683,6 +690,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
           }
         block_copy_out(S, a.A, I, WB, m, p);
         block_copy_out(S + (size_t)WB * m, a.A, J, WB, m, p);
+        if (tid < 2 * WB) {
+          const int col = (tid < WB) ? I * WB + tid : J * WB + tid - WB;
+          if (col < p) __stcg(a.nrm + col, nrmS[tid]);
+        }
         __syncthreads();
         if (tid == 0) {
           __threadfence();
@@ -908,10 +919,15 @@ static qtt_status_t plan_sweep(int L, const std::vector<int> &d, const std::vect
   P.RB = ((P.RB + 31) / 32) * 32;
   while (P.RB > kQrRowsMax) { set_error("large path: n = %lld too large", P.ncap); return QTT_EUNSUPPORTED; }
   P.qr_smem = sizeof(double) * ((size_t)2 * kNb * P.RB + 32 + kNb * kNb + 2 * kNb + kNb * 64);
-  // Jacobi: ~64 blocks of WB columns (a grid barrier per block round dominates a sweep, so
-  // fewer, wider blocks beat one block pair per SM: cfg3 1504 -> 1160 ms), capped by smem
-  int WB = 1;
-  while (WB < 64 && (P.pcap + WB - 1) / WB > 64) WB *= 2;
+  // Jacobi: blocks of WB = kWarps columns -- every warp has a pair in each cross round, and a
+  // block round (dataflow wait + block copies) is amortised over WB rounds (measured: cfg2
+  // 134 -> 101 ms against ~64 blocks of 4; cfg3 already had WB = 8), capped by smem
+  int WB = kWarps;
+  if (const char *e = getenv("QTT_COOP_WB")) {         // A/B knob (diagnostics): a power of two <= 64
+    const int w = std::max(1, std::min(64, atoi(e)));
+    WB = 1;
+    while (2 * WB <= w) WB *= 2;
+  }
   while (WB > 1 && 2 * WB * (P.mcap + 1) * 8 > 200 * 1024) WB /= 2;
   if (2 * WB * (P.mcap + 1) * 8 > 200 * 1024) { set_error("large path: m = %lld too large", P.mcap); return QTT_EUNSUPPORTED; }
   P.WB = WB;
@@ -1038,7 +1054,7 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
     // a4
     {
       JacArgs ja;
-      ja.dims = Bf.dims; ja.A = Bf.A; ja.bar = Bf.bar + 1; ja.flags = Bf.flags; ja.ver = Bf.ver; ja.part = Bf.part; ja.G = P.Gjac; ja.WB = P.WB;
+      ja.dims = Bf.dims; ja.A = Bf.A; ja.bar = Bf.bar + 1; ja.flags = Bf.flags; ja.ver = Bf.ver; ja.part = Bf.part; ja.nrm = Bf.s2; ja.G = P.Gjac; ja.WB = P.WB;
       ja.noise_ok = io.eps > 1e-14;
       ja.sweeps_out = io.sweeps ? io.sweeps + q : Bf.sweeps_scratch; ja.status = io.status;
       QTT_CUDA_TRY(cudaMemsetAsync(Bf.flags, 0, sizeof(int) * 3, s));
