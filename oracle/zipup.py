@@ -56,15 +56,20 @@ def zipup(kind: str, op: Optional[Sequence[np.ndarray]], x: Sequence[np.ndarray]
       sigmas  : singular values of every T_q (q < L-1), descending
       norm    : ||y||_F = ||C_{L-1}||_F (left-canonical output)
     """
-    X = right_orthonormalize([np.asarray(c, dtype=np.float64) for c in x])       # step 1
+    # float64, or complex128 when an operand is complex (the Fourier chain, PAPER.md:533-566);
+    # every step below is written for both (M^T = QR gives right-orthonormal rows in the
+    # complex sense too: Q^T conj(Q) = conj(Q^H Q) = I; the SVD carry is diag(s) V^H)
+    cplx = any(np.iscomplexobj(c) for c in x) or (op is not None and any(np.iscomplexobj(c) for c in op))
+    dt = np.complex128 if cplx else np.float64
+    X = right_orthonormalize([np.asarray(c, dtype=dt) for c in x])                # step 1
     if kind == "truncate":
         O = None
     else:
-        O = [np.asarray(c, dtype=np.float64) for c in op]
+        O = [np.asarray(c, dtype=dt) for c in op]
         if orth_operator:
             O = right_orthonormalize(O)
     L = len(X)
-    G = np.ones((1, 1, 1))                    # carry (chi, w, r)
+    G = np.ones((1, 1, 1), dtype=dt)          # carry (chi, w, r)
     cores: List[np.ndarray] = []
     delta2: List[float] = []
     sigmas: List[np.ndarray] = []

@@ -421,3 +421,55 @@ def cfg5_batch_arrays(members: Sequence[int], L: int = 40, R: int = 64, W: int =
     xs = [np.stack([p.x.cores[q] for p in probs]) for q in range(L)]
     ops = [np.stack([p.op.cores[q] for p in probs]) for q in range(L)]
     return probs, xs, ops
+
+
+# ----------------------------------------------------------------------------- Fourier (f2)
+
+def qft_trains(bases_i: Sequence[int]) -> List[Train]:
+    """The n rank-b_q factors of the DFT matrix M(i, j) = v^(i j), v = exp(-2 pi i / N)
+    (Eq. for T(i_q, j)).  i = sum_q c^i_q i_q (big-endian, bases_i),
+    j = sum_r c^j_r j_r with the reversed bases, and site k carries the digit pair
+    (i_k, j_{n-k+1}) -- both of base b_k -- as one leg of size b_k^2 (i slow, j fast).
+    Factor q = sum_s delta(s, i_q) prod_r exp(-2 pi i s c^i_q c^j_r j_r / N): a rank-b_q
+    train whose bond carries s (block-diagonal cores; ones to sum s at the ends).  The
+    phases are reduced mod N in integers before cos/sin.  Complex128 cores."""
+    b = [int(x) for x in bases_i]
+    n = len(b)
+    N = int(np.prod(b))
+    ci = digit_factors(b)
+    bj = b[::-1]
+    cj = digit_factors(bj)
+    trains = []
+    for q in range(n):
+        bq = b[q]
+        cores = []
+        for k in range(n):
+            bk = b[k]
+            r = n - 1 - k                       # site k carries j_r (0-based r), base bj[r] == bk
+            core = np.zeros((bq, bk * bk, bq), dtype=np.complex128)
+            for s in range(bq):
+                for ik in range(bk):
+                    if k == q and ik != s:
+                        continue
+                    for jr in range(bk):
+                        e = (s * ci[q] * cj[r] * jr) % N
+                        core[s, ik * bk + jr, s] = np.exp(-2j * np.pi * e / N)
+            if k == 0:
+                core = core.sum(axis=0, keepdims=True)
+            if k == n - 1:
+                core = core.sum(axis=2, keepdims=True)
+            cores.append(core)
+        trains.append(Train(cores))
+    return trains
+
+
+def qft_dense_order(bases_i: Sequence[int]):
+    """(shape, permutation) turning the dense tensor of a QFT-layout train (axes
+    (i_1, j_n, i_2, j_{n-1}, ...)) into the N x N matrix with rows i and columns j."""
+    b = [int(x) for x in bases_i]
+    n = len(b)
+    shape = []
+    for k in range(n):
+        shape += [b[k], b[k]]
+    perm = [2 * k for k in range(n)] + [2 * (n - 1 - r) + 1 for r in range(n)]
+    return shape, perm
