@@ -19,7 +19,8 @@
  *     core_elems(q) = ranks[q] * d_out[q] * (d_in[q] if n_legs == 2) * ranks[q+1].
  *     For OUTPUT trains `ranks` are the bond CAPACITIES; every member's core is written
  *     packed at its actual ranks inside its capacity-sized slot.
- *   - dtype: IEEE float64 throughout (the paper's precision).
+ *   - dtype: IEEE float64 (the paper's precision) unless a train says otherwise
+ *     (qtt_trains_t.dtype: the fp32 and complex128 variants of qtt_zipup).
  *   - Calls are stream-ordered on `stream` (a cudaStream_t passed as void*), asynchronous
  *     (no host synchronisation) and reentrant; there is no global mutable state except
  *     the thread-local error string.
@@ -59,11 +60,12 @@ typedef struct {
   const int32_t *ranks;   /* host [L+1] bond dims (inputs) / bond capacities (outputs);
                              ranks[0] == ranks[L] == 1                                     */
   void *const *cores;     /* host [L] device pointers, batch-strided as described above    */
-  int32_t dtype;          /* element type of the cores: QTT_F64 (0, default) or QTT_F32 (1);
-                             QTT_F32 is accepted by qtt_zipup only (see there)              */
+  int32_t dtype;          /* element type of the cores: QTT_F64 (0, default), QTT_F32 (1) or
+                             QTT_C128 (2: complex double, interleaved re/im); QTT_F32 and
+                             QTT_C128 are accepted by qtt_zipup only (see there)            */
 } qtt_trains_t;
 
-enum { QTT_F64 = 0, QTT_F32 = 1 };
+enum { QTT_F64 = 0, QTT_F32 = 1, QTT_C128 = 2 };
 
 /* Flags for qtt_zipup. */
 enum {
@@ -117,6 +119,12 @@ size_t qtt_zipup_workspace_bytes(const char *subscripts, const qtt_trains_t *op,
  *                accumulation); QR, Jacobi SVD and truncation run in fp64; the output cores
  *                are rounded to binary32.  Mixed dtypes return QTT_EINVAL.  Accuracy target:
  *                relative Frobenius error <= 1e-4 + eps against the fp64 oracle (c-A28).
+ *   complex128 (the tensorized Fourier transform of PAPER.md:533-566 as a
+ *                chain of Hadamard zip-ups): when x, op and out all have dtype QTT_C128 the
+ *                cores are complex doubles (interleaved re, im; 16 bytes).  Same steps in
+ *                complex arithmetic (T^H is the conjugate transpose, the carry is U_k^H T, the
+ *                Jacobi rotations carry the phase of a_i^H a_j); delta2, norm2 and sigma stay
+ *                real f64.  One CTA per member (complex.cu); diag->phase_cycles is ignored.
  */
 typedef struct {
   double *sigma;          /* device f64 [B*(L-1)*sigma_stride]: singular values of every site

@@ -1,0 +1,530 @@
+// complex.cu -- complex128 zip-up (the tensorized Fourier transform
+// of PAPER.md:533-566 is a chain of Hadamard zip-ups of complex trains).
+//
+// Same steps as the fp64 path (qtt.h qtt_zipup) in complex
+// arithmetic, one CTA (256 threads) per member running every step for that member:
+//   a1  right-orthonormalise each operand: for q = L-1..1, Householder QR of M^T
+//       (M = core q unfolded (r, legs r')), core q <- Q^T, core q-1 <- core q-1 R^T
+//       (Q^T has orthonormal rows in the complex sense)
+//   a2  T[(c,i),(w',r')] = sum G[c,w,r] x[r,j,r'] op[w,i,j,w']  (Eq. einsum)
+//   a3  Householder QR of T^H when m <= n (A = R^H), else A = T
+//   a4  one-sided complex Jacobi on the columns of A: pair (i, j) with a = |a_i|^2,
+//       b = |a_j|^2, g = a_i^H a_j = |g| e^{i phi}; zeta = (b - a) / (2|g|),
+//       t = sign(zeta) / (|zeta| + hypot(1, zeta)), c = 1/sqrt(1+t^2), s = c t;
+//       a_i <- c a_i - s e^{-i phi} a_j,  a_j <- s e^{i phi} a_i + c a_j
+//       (the real rotation of the 2x2 Gram matrix after removing the phase of g);
+//       sweeps until no pair has |g|^2 > tol^2 a b (tol = m eps); noise-level columns as c-A31
+//   a5  truncation rule of SPEC.md:299 (tail sums smallest first), delta2
+//   a6  C_q = U[:, :k] (chi, d, k), carry G <- U_k^H T
+//   a7  last site C_{L-1} = T, norm2 = ||T||_F^2.
+// The member's operands, carry and site matrices live in its slice of the workspace (global
+// memory, L1/L2 resident at the Fourier chain's sizes: rank <= 64, d <= 8).  This is the
+// complex row's first, plain version: no tensor cores, no register blocking.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "large.cuh"
+
+namespace qtt {
+
+namespace cplx {
+
+struct Z {
+  double x, y;
+};
+__device__ __forceinline__ Z mk(double a, double b) { return Z{a, b}; }
+__device__ __forceinline__ Z add(Z a, Z b) { return Z{a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ Z sub(Z a, Z b) { return Z{a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ Z mul(Z a, Z b) { return Z{a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x}; }
+__device__ __forceinline__ Z conj(Z a) { return Z{a.x, -a.y}; }
+__device__ __forceinline__ Z scl(double s, Z a) { return Z{s * a.x, s * a.y}; }
+__device__ __forceinline__ double abs2(Z a) { return a.x * a.x + a.y * a.y; }
+// acc += conj(a) * b
+__device__ __forceinline__ Z cfma(Z a, Z b, Z acc) {
+  return Z{fma(a.x, b.x, fma(a.y, b.y, acc.x)), fma(a.x, b.y, fma(-a.y, b.x, acc.y))};
+}
+// acc += a * b
+__device__ __forceinline__ Z zfma(Z a, Z b, Z acc) {
+  return Z{fma(a.x, b.x, fma(-a.y, b.y, acc.x)), fma(a.x, b.y, fma(a.y, b.x, acc.y))};
+}
+__device__ __forceinline__ Z warp_zsum(Z v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
+
+constexpr int kMaxSweeps = 60;
+
+struct Args {
+  int L, B, kind, op_batch;
+  int d[64], dj[64], xr0[65], or0[65], cap[65];
+  long long xoff[65], ooff[65];        // per-member element offsets of the compact operand copies
+  const Z *xsrc[64];
+  const Z *osrc[64];
+  Z *Cq[64];
+  long long Cq_bs[64];
+  long long x_bs[64], o_bs[64];        // member stride of the input cores (elements)
+  Z *ws;                               // per-member complex scratch
+  long long ws_member;                 // complex elements per member
+  long long xo_n, oo_n, g_n, t_n;      // sizes of the member's regions
+  char *iws;                           // per-member int/double scratch
+  long long iws_member;                // bytes per member
+  int pmax;
+  int *yr;                             // out_ranks [B][L+1]
+  double *delta2, *norm2, *sigma;
+  int sigma_stride;
+  int *sweeps, *status;
+  double eps;
+  int max_rank, orth_op;
+};
+
+// In-place Householder QR of the column-major rows x cols matrix H (ld = rows), K =
+// min(rows, cols) reflectors (LAPACK zgeqr2 conventions: H_j = I - tau_j v_j v_j^H,
+// v_j[j] = 1, beta real on the diagonal; H_j^H applied to the trailing columns).
+__device__ void house_qr(Z *H, int rows, int cols, Z *tau, double *red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int K = min(rows, cols);
+  __shared__ Z s_scal;
+  for (int j = 0; j < K; ++j) {
+    Z *v = H + (size_t)j * rows;
+    double xn = 0.0;
+    for (int i = j + 1 + tid; i < rows; i += kThreads) xn += abs2(v[i]);
+    xn = block_sum(xn, red);
+    if (tid == 0) {
+      const Z alpha = v[j];
+      Z t{0.0, 0.0};
+      Z inv{0.0, 0.0};
+      if (xn == 0.0 && alpha.y == 0.0) {
+        t = Z{0.0, 0.0};
+      } else {
+        const double beta = -copysign(sqrt(abs2(alpha) + xn), alpha.x);
+        t = Z{(beta - alpha.x) / beta, -alpha.y / beta};
+        const Z den = Z{alpha.x - beta, alpha.y};          // 1 / (alpha - beta)
+        const double dd = abs2(den);
+        inv = Z{den.x / dd, -den.y / dd};
+        v[j] = Z{beta, 0.0};
+      }
+      tau[j] = t;
+      s_scal = inv;
+    }
+    __syncthreads();
+    const Z inv = s_scal;
+    const Z t = tau[j];
+    if (t.x != 0.0 || t.y != 0.0)
+      for (int i = j + 1 + tid; i < rows; i += kThreads) v[i] = mul(v[i], inv);
+    __syncthreads();
+    // trailing columns: c <- c - conj(tau) v (v^H c), one warp per column
+    if (t.x != 0.0 || t.y != 0.0) {
+      const Z ct = conj(t);
+      for (int c = j + 1 + warp; c < cols; c += kWarps) {
+        Z *col = H + (size_t)c * rows;
+        Z w{0.0, 0.0};
+        for (int i = j + lane; i < rows; i += 32) {
+          const Z vi = (i == j) ? Z{1.0, 0.0} : v[i];
+          w = cfma(vi, col[i], w);
+        }
+        w = warp_zsum(w);
+        const Z f = mul(ct, w);
+        for (int i = j + lane; i < rows; i += 32) {
+          const Z vi = (i == j) ? Z{1.0, 0.0} : v[i];
+          col[i] = sub(col[i], mul(f, vi));
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Q (rows x K, column-major, ld = rows) = H_0 H_1 ... H_{K-1} applied to the first K columns
+// of the identity (LAPACK zung2r), from the reflectors left in H by house_qr.
+__device__ void form_q(const Z *H, int rows, int K, const Z *tau, Z *Q) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < rows * K; idx += kThreads) {
+    const int i = idx % rows, c = idx / rows;
+    Q[idx] = Z{(i == c) ? 1.0 : 0.0, 0.0};
+  }
+  __syncthreads();
+  for (int j = K - 1; j >= 0; --j) {
+    const Z t = tau[j];
+    if (t.x == 0.0 && t.y == 0.0) continue;
+    const Z *v = H + (size_t)j * rows;
+    for (int c = j + warp; c < K; c += kWarps) {
+      Z *col = Q + (size_t)c * rows;
+      Z w{0.0, 0.0};
+      for (int i = j + lane; i < rows; i += 32) {
+        const Z vi = (i == j) ? Z{1.0, 0.0} : v[i];
+        w = cfma(vi, col[i], w);
+      }
+      w = warp_zsum(w);
+      const Z f = mul(t, w);
+      for (int i = j + lane; i < rows; i += 32) {
+        const Z vi = (i == j) ? Z{1.0, 0.0} : v[i];
+        col[i] = sub(col[i], mul(f, vi));
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// One-sided Jacobi on the columns of A (rows x p, column-major, ld = rows).  Returns sweeps.
+__device__ int jacobi(Z *A, int rows, int p, double noise_eps, double *red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double tol = (double)max(rows, 1) * DBL_EPSILON;
+  __shared__ int s_rot;
+  double tot = 0.0;
+  for (int i = tid; i < rows * p; i += kThreads) tot += abs2(A[i]);
+  tot = block_sum(tot, red);
+  const double noise = noise_eps * tot;
+  const int n = p + (p & 1);
+  int sweep = 0;
+  for (; sweep < kMaxSweeps; ++sweep) {
+    if (tid == 0) s_rot = 0;
+    __syncthreads();
+    int rot = 0;
+    for (int r = 0; r < n - 1; ++r) {
+      for (int pr = warp; pr < n / 2; pr += kWarps) {
+        // circle method: position 0 fixed, the others rotate
+        const int k1 = pr, k2 = n - 1 - pr;
+        const int ci = (k1 == 0) ? 0 : 1 + (k1 - 1 + r) % (n - 1);
+        const int cj = 1 + (k2 - 1 + r) % (n - 1);
+        if (ci >= p || cj >= p) continue;
+        Z *ai = A + (size_t)ci * rows, *aj = A + (size_t)cj * rows;
+        double al = 0.0, be = 0.0;
+        Z g{0.0, 0.0};
+        for (int i = lane; i < rows; i += 32) {
+          const Z x = ai[i], y = aj[i];
+          al += abs2(x);
+          be += abs2(y);
+          g = cfma(x, y, g);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        g = warp_zsum(g);
+        const double ag2 = abs2(g);
+        if (al > noise && be > noise && ag2 > tol * tol * al * be) {
+          const double ag = sqrt(ag2);
+          const Z ph = Z{g.x / ag, g.y / ag};             // e^{i phi}
+          const double zeta = (be - al) / (2.0 * ag);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          const Z sp = scl(s, ph), sm = scl(s, conj(ph));
+          for (int i = lane; i < rows; i += 32) {
+            const Z x = ai[i], y = aj[i];
+            ai[i] = sub(scl(c, x), mul(sm, y));
+            aj[i] = add(mul(sp, x), scl(c, y));
+          }
+          rot = 1;
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+    }
+    if (rot) s_rot = 1;
+    __syncthreads();
+    const int any = s_rot;
+    __syncthreads();
+    if (!any) { ++sweep; break; }
+  }
+  return sweep;
+}
+
+// a1 for one operand of member b: copy its cores into the compact slots `dst` (offsets off[q])
+// and right-orthonormalise in place; rk[0..L] receives the ranks.
+__device__ void orth_operand(const Args &a, const Z *const *src, const long long *sbs, int member, const int *legs,
+                             const int *r0, const long long *off, Z *dst, int *rk, bool orth, Z *H, Z *Q, Z *tau,
+                             double *red) {
+  const int tid = threadIdx.x;
+  const int L = a.L;
+  for (int q = 0; q < L; ++q) {
+    const long long n = (long long)r0[q] * legs[q] * r0[q + 1];
+    const Z *s = src[q] + (size_t)member * sbs[q];
+    for (long long i = tid; i < n; i += kThreads) dst[off[q] + i] = s[i];
+  }
+  if (tid == 0)
+    for (int q = 0; q <= L; ++q) rk[q] = r0[q];
+  __syncthreads();
+  if (!orth) return;
+  for (int q = L - 1; q >= 1; --q) {
+    const int r = rk[q], c = legs[q] * rk[q + 1];
+    Z *core = dst + off[q];
+    // H = M^T (c x r, column-major): H[j + i c] = M[i, j] = core[i c + j] -- the same storage
+    for (int idx = tid; idx < r * c; idx += kThreads) H[idx] = core[idx];
+    __syncthreads();
+    house_qr(H, c, r, tau, red);
+    const int k = min(r, c);
+    form_q(H, c, k, tau, Q);                      // Q: c x k
+    // core q <- Q^T (k x c): core[kk c + j] = Q[j + kk c]
+    for (int idx = tid; idx < k * c; idx += kThreads) core[idx] = Q[idx];
+    // core q-1 (rows = r_{q-1} legs_{q-1}, cols r) <- core q-1 R^T (cols k); R = k x r upper
+    // (in H: R[i, j] = H[i + j c] for i <= j)
+    Z *prev = dst + off[q - 1];
+    const int pr = rk[q - 1] * legs[q - 1];
+    // stage prev into Q's space is not needed: compute into the tail of Q (pr x k)
+    Z *tmp = Q + (size_t)c * k;
+    for (int idx = tid; idx < pr * k; idx += kThreads) {
+      const int row = idx / k, kk = idx % k;
+      Z acc{0.0, 0.0};
+      for (int j = kk; j < r; ++j) acc = zfma(prev[(size_t)row * r + j], H[kk + (size_t)j * c], acc);   // R^T[j,kk] = R[kk,j]
+      tmp[idx] = acc;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < pr * k; idx += kThreads) prev[idx] = tmp[idx];
+    if (tid == 0) rk[q] = k;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_zipup_c(Args a) {
+  const int b = blockIdx.x, tid = threadIdx.x, L = a.L, L1 = L + 1;
+  __shared__ double red[kWarps];
+  __shared__ double s_sc[4];
+  Z *w = a.ws + (size_t)b * a.ws_member;
+  Z *Xo = w, *Oo = Xo + a.xo_n, *G = Oo + a.oo_n, *T = G + a.g_n, *H = T + a.t_n, *Q = H + a.t_n,
+    *tau = Q + 2 * a.t_n;
+  char *iw = a.iws + (size_t)b * a.iws_member;
+  double *sg = (double *)iw;                      // [pmax]
+  double *tail = sg + a.pmax;                     // [pmax + 1]
+  int *perm = (int *)(tail + a.pmax + 1);         // [pmax]
+  int *xr = perm + a.pmax, *orr = xr + L1;        // [L+1] each
+  const int ob = (a.op_batch == 1) ? 0 : b;
+
+  // ---- a1
+  {
+    int legs[64];
+    for (int q = 0; q < L; ++q) legs[q] = a.dj[q];
+    orth_operand(a, a.xsrc, a.x_bs, b, legs, a.xr0, a.xoff, Xo, xr, true, H, Q, tau, red);
+    if (a.kind != TRUNCATE) {
+      for (int q = 0; q < L; ++q) legs[q] = (a.kind == MATVEC) ? a.d[q] * a.dj[q] : a.d[q];
+      orth_operand(a, a.osrc, a.o_bs, ob, legs, a.or0, a.ooff, Oo, orr, a.orth_op != 0, H, Q, tau, red);
+    } else if (tid == 0) {
+      for (int q = 0; q <= L; ++q) orr[q] = 1;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) G[0] = Z{1.0, 0.0};
+  int chi = 1;
+  __syncthreads();
+  for (int q = 0; q < L; ++q) {
+    const int d = a.d[q], dj = a.dj[q];
+    const int w = orr[q], w2 = orr[q + 1], r = xr[q], r2 = xr[q + 1];
+    const int m = chi * d, n = w2 * r2;
+    const Z *X = Xo + a.xoff[q], *O = Oo + a.ooff[q];
+    // ---- a2: T[(c,i),(w',r')]
+    for (int idx = tid; idx < m * n; idx += kThreads) {
+      const int rr2 = idx % r2, ww2 = (idx / r2) % w2, ii = (idx / n) % d, c = idx / (n * d);
+      Z acc{0.0, 0.0};
+      if (a.kind == TRUNCATE) {
+        for (int rr = 0; rr < r; ++rr) acc = zfma(G[(size_t)c * r + rr], X[((size_t)rr * dj + ii) * r2 + rr2], acc);
+      } else if (a.kind == HADAMARD) {
+        for (int ww = 0; ww < w; ++ww) {
+          const Z o = O[((size_t)ww * d + ii) * w2 + ww2];
+          Z s{0.0, 0.0};
+          for (int rr = 0; rr < r; ++rr) s = zfma(G[((size_t)c * w + ww) * r + rr], X[((size_t)rr * d + ii) * r2 + rr2], s);
+          acc = zfma(o, s, acc);
+        }
+      } else {
+        for (int ww = 0; ww < w; ++ww)
+          for (int jj = 0; jj < dj; ++jj) {
+            const Z o = O[(((size_t)ww * d + ii) * dj + jj) * w2 + ww2];
+            Z s{0.0, 0.0};
+            for (int rr = 0; rr < r; ++rr)
+              s = zfma(G[((size_t)c * w + ww) * r + rr], X[((size_t)rr * dj + jj) * r2 + rr2], s);
+            acc = zfma(o, s, acc);
+          }
+      }
+      T[idx] = acc;
+    }
+    __syncthreads();
+    Z *Cq = a.Cq[q] + (size_t)b * a.Cq_bs[q];
+    // ---- a7: last site
+    if (q == L - 1) {
+      double s = 0.0;
+      for (int i = tid; i < m * n; i += kThreads) { Cq[i] = T[i]; s += abs2(T[i]); }
+      s = block_sum(s, red);
+      if (tid == 0) {
+        a.norm2[b] = s;
+        a.delta2[(size_t)b * L + q] = 0.0;
+        a.yr[(size_t)b * L1 + L] = 1;
+        if (L == 1) a.yr[(size_t)b * L1] = 1;
+        if (a.sweeps) a.sweeps[(size_t)b * L + q] = 0;
+        if (!isfinite(s)) atomicOr(a.status, 1);
+      }
+      return;
+    }
+    // ---- a3: A (m x p, column-major, ld m)
+    int p;
+    Z *A = Q;                                     // reuse: Q is free between a1 and here
+    if (m <= n) {
+      p = m;
+      for (int idx = tid; idx < m * n; idx += kThreads) H[idx] = conj(T[idx]);   // T^H column-major (n x m)
+      __syncthreads();
+      house_qr(H, n, m, tau, red);
+      for (int idx = tid; idx < m * m; idx += kThreads) {       // A = R^H: A[i, j] = conj(R[j, i]), i >= j
+        const int j = idx / m, i = idx % m;
+        A[idx] = (i >= j) ? conj(H[j + (size_t)i * n]) : Z{0.0, 0.0};
+      }
+    } else {
+      p = n;
+      for (int idx = tid; idx < m * n; idx += kThreads) {
+        const int j = idx / m, i = idx % m;
+        A[idx] = T[(size_t)i * n + j];
+      }
+    }
+    __syncthreads();
+    // ---- a4
+    const int sweeps = jacobi(A, m, p, a.eps > 1e-14 ? DBL_EPSILON * DBL_EPSILON : 0.0, red);
+    for (int j = tid; j < p; j += kThreads) {
+      double s = 0.0;
+      for (int i = 0; i < m; ++i) s += abs2(A[(size_t)j * m + i]);
+      if (!isfinite(s)) { atomicOr(a.status, 1); s = 0.0; }
+      sg[j] = s;
+    }
+    __syncthreads();
+    for (int j = tid; j < p; j += kThreads) {
+      const double sj = sg[j];
+      int rank = 0;
+      for (int l = 0; l < p; ++l) rank += (sg[l] > sj) || (sg[l] == sj && l < j);
+      perm[rank] = j;
+    }
+    __syncthreads();
+    // ---- a5
+    if (tid == 0) {
+      double acc = 0.0;
+      tail[p] = 0.0;
+      for (int jj = p - 1; jj >= 0; --jj) { acc += sg[perm[jj]]; tail[jj] = acc; }
+      const double tot = acc, thr = a.eps * a.eps * tot;
+      int k = p;
+      for (int kk = 1; kk <= p; ++kk)
+        if (tail[kk] <= thr) { k = kk; break; }
+      if (a.max_rank > 0) k = min(k, a.max_rank);
+      if (tot == 0.0) k = 1;
+      k = max(k, 1);
+      s_sc[0] = (double)k;
+      s_sc[1] = tail[k];
+      if (sweeps >= kMaxSweeps) atomicOr(a.status, 2);
+    }
+    __syncthreads();
+    const int k = (int)s_sc[0];
+    // ---- a6: U columns, emit, carry
+    for (int idx = tid; idx < k * m; idx += kThreads) {
+      const int kk = idx / m, i = idx % m;
+      const int j = perm[kk];
+      const double s2 = sg[j];
+      Z *col = A + (size_t)j * m;
+      col[i] = (s2 > 0.0) ? scl(1.0 / sqrt(s2), col[i]) : Z{(i == kk) ? 1.0 : 0.0, 0.0};
+    }
+    __syncthreads();
+    for (int idx = tid; idx < m * k; idx += kThreads) {
+      const int i = idx / k, kk = idx % k;
+      Cq[idx] = A[(size_t)perm[kk] * m + i];
+    }
+    if (a.sigma) {
+      double *so = a.sigma + ((size_t)b * (L - 1) + q) * a.sigma_stride;
+      for (int jj = tid; jj < a.sigma_stride; jj += kThreads) so[jj] = (jj < p) ? sqrt(sg[perm[jj]]) : 0.0;
+    }
+    if (tid == 0) {
+      if (a.sweeps) a.sweeps[(size_t)b * L + q] = sweeps;
+      a.yr[(size_t)b * L1 + q + 1] = k;
+      if (q == 0) a.yr[(size_t)b * L1] = 1;
+      a.delta2[(size_t)b * L + q] = s_sc[1];
+    }
+    // G[kk, col] = sum_i conj(U[i, kk]) T[i, col]   (k x n) -> (k, w', r')
+    for (int idx = tid; idx < k * n; idx += kThreads) {
+      const int kk = idx / n, col = idx % n;
+      const Z *u = A + (size_t)perm[kk] * m;
+      Z acc{0.0, 0.0};
+      for (int i = 0; i < m; ++i) acc = cfma(u[i], T[(size_t)i * n + col], acc);
+      G[idx] = acc;
+    }
+    chi = k;
+    __syncthreads();
+  }
+}
+
+}  // namespace cplx
+
+static void complex_sizes(const Shape &S, long long &zmember, long long &imember, long long &xo, long long &oo,
+                          long long &gn, long long &tn, int &pmax) {
+  xo = S.xoff[S.L];
+  oo = std::max<long long>(1, S.ooff[S.L]);
+  gn = S.g_elems;
+  tn = S.t_elems;
+  pmax = 1;
+  long long core_max = 1;
+  for (int q = 0; q < S.L; ++q) {
+    const long long m = (long long)S.cap[q] * S.d[q], n = (long long)S.orr[q + 1] * S.xr[q + 1];
+    pmax = (int)std::max<long long>(pmax, std::max(m, n));
+    core_max = std::max(core_max, (long long)S.xr[q] * S.dj[q] * S.xr[q + 1]);
+    const long long oc = (S.kind == MATVEC) ? (long long)S.orr[q] * S.d[q] * S.dj[q] * S.orr[q + 1]
+                                            : (long long)S.orr[q] * S.d[q] * S.orr[q + 1];
+    core_max = std::max(core_max, oc);
+    // a1 temporaries: prev-core product (rows <= core elems) lives behind Q
+  }
+  tn = std::max(tn, core_max);
+  // regions: Xo, Oo, G, T (tn), H (tn), Q (2 tn: Q / A and the a1 product), tau (pmax)
+  zmember = xo + oo + gn + tn + tn + 2 * tn + std::max<long long>(pmax, 64);
+  zmember = (zmember + 15) & ~15LL;
+  imember = 8LL * (3LL * pmax + 1) + 4LL * (2LL * (S.L + 1)) + 256;
+  imember = (imember + 255) & ~255LL;
+}
+
+size_t complex_workspace_bytes(const Shape &S) {
+  long long zm, im, xo, oo, gn, tn;
+  int pmax;
+  complex_sizes(S, zm, im, xo, oo, gn, tn, pmax);
+  return (size_t)S.B * (size_t)zm * 16 + (size_t)S.B * (size_t)im + 256;
+}
+
+qtt_status_t complex_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags,
+                           const LargeIO &io, void *workspace, size_t workspace_bytes, cudaStream_t s) {
+  if (S.L > 64) { set_error("complex path: n_sites > 64"); return QTT_EUNSUPPORTED; }
+  const size_t need = complex_workspace_bytes(S);
+  if (!workspace || workspace_bytes < need) {
+    set_error("workspace %zu bytes < required %zu", workspace_bytes, need);
+    return QTT_ECAPACITY;
+  }
+  cplx::Args a;
+  memset(&a, 0, sizeof(a));
+  a.L = S.L; a.B = S.B; a.kind = S.kind; a.op_batch = op ? op->batch : 1;
+  for (int q = 0; q < S.L; ++q) {
+    a.d[q] = S.d[q]; a.dj[q] = S.dj[q];
+    a.xsrc[q] = (const cplx::Z *)x->cores[q];
+    a.x_bs[q] = (long long)x->ranks[q] * x->d_out[q] * x->ranks[q + 1];
+    if (op) {
+      a.osrc[q] = (const cplx::Z *)op->cores[q];
+      a.o_bs[q] = (long long)op->ranks[q] * op->d_out[q] * (op->n_legs == 2 ? op->d_in[q] : 1) * op->ranks[q + 1];
+    }
+    a.Cq[q] = (cplx::Z *)io.out->cores[q];
+    a.Cq_bs[q] = (long long)io.out->ranks[q] * S.d[q] * io.out->ranks[q + 1];
+  }
+  for (int q = 0; q <= S.L; ++q) {
+    a.xr0[q] = S.xr[q]; a.or0[q] = S.orr[q]; a.cap[q] = S.cap[q];
+    a.xoff[q] = S.xoff[q]; a.ooff[q] = S.ooff[q];
+  }
+  long long zm, im, xo, oo, gn, tn;
+  int pmax;
+  complex_sizes(S, zm, im, xo, oo, gn, tn, pmax);
+  a.ws = (cplx::Z *)workspace;
+  a.ws_member = zm;
+  a.xo_n = xo; a.oo_n = oo; a.g_n = gn; a.t_n = tn;
+  a.iws = (char *)workspace + (size_t)S.B * zm * 16;
+  a.iws_member = im;
+  a.pmax = pmax;
+  a.yr = io.out_ranks; a.delta2 = io.delta2; a.norm2 = io.norm2; a.sigma = io.sigma;
+  a.sigma_stride = io.sigma_stride; a.sweeps = io.sweeps; a.status = io.status;
+  a.eps = io.eps; a.max_rank = io.max_rank;
+  a.orth_op = (flags & QTT_NO_OPERATOR_ORTH) ? 0 : 1;
+  QTT_CUDA_TRY(cudaMemsetAsync(io.status, 0, sizeof(int32_t), s));
+  cplx::k_zipup_c<<<S.B, kThreads, 0, s>>>(a);
+  QTT_CUDA_TRY(cudaGetLastError());
+  return QTT_OK;
+}
+
+}  // namespace qtt

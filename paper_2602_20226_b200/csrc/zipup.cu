@@ -967,12 +967,13 @@ static qtt_status_t cvt_train(const qtt_trains_t *t, void *const *src, void *con
   return QTT_OK;
 }
 
-// -1: not all fp64 and not all fp32 (error), 0: fp64, 1: fp32
+// -1: mixed (error), 0: fp64, 1: fp32, 2: complex128
 static int train_dtypes(const qtt_trains_t *op, const qtt_trains_t *x, const qtt_trains_t *out) {
   const int dx = x ? x->dtype : QTT_F64;
   const int dop = op ? op->dtype : dx, dout = out ? out->dtype : dx;
   if (dx == QTT_F64 && dop == QTT_F64 && dout == QTT_F64) return 0;
   if (dx == QTT_F32 && dop == QTT_F32 && dout == QTT_F32) return 1;
+  if (dx == QTT_C128 && dop == QTT_C128 && dout == QTT_C128) return 2;
   return -1;
 }
 
@@ -993,7 +994,7 @@ extern "C" {
 
 const char *qtt_last_error(void) { return qtt::g_err; }
 const char *qtt_version(void) {
-  return "libqtt 0.2 (sm_100a; fp64 zip-up: small- and large-member paths; fp32 variant with 3xTF32 tcgen05 contractions)";
+  return "libqtt 0.3 (sm_100a; fp64 zip-up: small- and large-member paths; fp32 variant with 3xTF32 tcgen05 contractions; complex128 zip-up)";
 }
 
 qtt_status_t qtt_zipup_capacity(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
@@ -1010,7 +1011,7 @@ size_t qtt_zipup_workspace_bytes(const char *subscripts, const qtt_trains_t *op,
                                  const qtt_trains_t *out) {
   {
     const int dt = train_dtypes(op, x, out);
-    if (dt < 0) { set_error("mixed dtypes: x, op and out must all be QTT_F64 or all QTT_F32"); return 0; }
+    if (dt < 0) { set_error("mixed dtypes: x, op and out must share one of QTT_F64, QTT_F32, QTT_C128"); return 0; }
     if (dt == 1) {                 // fp32 variant: fp64 staging of all three trains + the fp64 workspace
       F32Stage F;
       f32_stage(op, x, out, nullptr, F);
@@ -1024,6 +1025,7 @@ size_t qtt_zipup_workspace_bytes(const char *subscripts, const qtt_trains_t *op,
     for (int q = 1; q < x->n_sites; ++q) mr = std::max(mr, (int)out->ranks[q]);
   Shape S;
   if (analyse(subscripts, op, x, mr, S) != QTT_OK) return 0;
+  if (train_dtypes(op, x, out) == 2) return complex_workspace_bytes(S);
   if (check_small_path(S) == QTT_OK) return layout(S).total;
   return large_workspace_bytes(S);
 }
@@ -1041,7 +1043,7 @@ qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt
   if (!(eps >= 0.0 && eps < 1.0)) { set_error("eps %g outside [0,1)", eps); return QTT_EINVAL; }
   {
     const int dt = train_dtypes(op, x, out);
-    if (dt < 0) { set_error("mixed dtypes: x, op and out must all be QTT_F64 or all QTT_F32"); return QTT_EINVAL; }
+    if (dt < 0) { set_error("mixed dtypes: x, op and out must share one of QTT_F64, QTT_F32, QTT_C128"); return QTT_EINVAL; }
     if (dt == 1) {                 // fp32 variant (see qtt.h): widen, run with TF32 GEMMs, narrow
       if (!x || !out || !x->cores || !out->cores) { set_error("NULL train"); return QTT_EINVAL; }
       if (!workspace) { set_error("workspace is NULL"); return QTT_EINVAL; }
@@ -1081,6 +1083,15 @@ qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt
   }
   if (sigma && sigma_stride < 1) { set_error("sigma_stride < 1"); return QTT_EINVAL; }
   cudaStream_t s = (cudaStream_t)stream;
+  if (train_dtypes(op, x, out) == 2) {     // complex128 (Fourier chain)
+    g_err[0] = 0;
+    if (events) for (int i = 0; i < 3; ++i) QTT_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[i], s));
+    LargeIO io{out, out_ranks, delta2, norm2, sigma, sigma_stride, sweeps, status, eps, max_rank};
+    qtt_status_t cst = complex_zipup(S, op, x, flags, io, workspace, workspace_bytes, s);
+    if (cst != QTT_OK) return cst;
+    if (events) QTT_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[3], s));
+    return QTT_OK;
+  }
   if (check_small_path(S) != QTT_OK) {
     // large-member path (site matrices with more than 128 rows): one member at a time
     g_err[0] = 0;

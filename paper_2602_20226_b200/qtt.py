@@ -41,7 +41,7 @@ class _Trains(ctypes.Structure):
                 ("ranks", ctypes.POINTER(ctypes.c_int32)), ("cores", ctypes.POINTER(ctypes.c_void_p)),
                 ("dtype", ctypes.c_int32)]
 
-QTT_F64, QTT_F32 = 0, 1
+QTT_F64, QTT_F32, QTT_C128 = 0, 1, 2
 
 
 _lib = None
@@ -131,7 +131,8 @@ class DeviceTrains:
 
     @property
     def dtype_code(self) -> int:
-        return QTT_F32 if self.cores[0].dtype == torch.float32 else QTT_F64
+        dt = self.cores[0].dtype
+        return QTT_F32 if dt == torch.float32 else QTT_C128 if dt == torch.complex128 else QTT_F64
 
     def c_struct(self):
         L = self.n_sites
@@ -151,7 +152,8 @@ def to_device(cores_per_site: Sequence[np.ndarray], device="cuda", mpo: bool = F
               dtype=np.float64) -> DeviceTrains:
     """Upload batch-stacked numpy cores: cores_per_site[q] has shape (B, r, d, r') (MPS)
     or (B, w, d_out, d_in, w') (MPO).  Single trains may be given without the batch axis.
-    dtype np.float32 gives QTT_F32 trains (the fp32 variant of qtt_zipup)."""
+    dtype np.float32 gives QTT_F32 trains (the fp32 variant of qtt_zipup), np.complex128
+    QTT_C128 trains (the complex variant: the Fourier chain)."""
     cs = []
     for c in cores_per_site:
         c = np.asarray(c, dtype=dtype)
@@ -178,8 +180,20 @@ def member_cores(t: DeviceTrains, ranks: Sequence[int], b: int) -> List[np.ndarr
     for q, c in enumerate(t.cores):
         n = ranks[q] * t.d_out[q] * ranks[q + 1]
         flat = c[b].reshape(-1)[:n]
-        out.append(flat.cpu().double().numpy().reshape(ranks[q], t.d_out[q], ranks[q + 1]))
+        flat = flat.cpu()
+        flat = flat if flat.is_complex() else flat.double()
+        out.append(flat.numpy().reshape(ranks[q], t.d_out[q], ranks[q + 1]))
     return out
+
+
+def member_view(t: DeviceTrains, ranks: Sequence[int], b: int) -> DeviceTrains:
+    """Member b of a capacity-sized output as a batch-1 train at its actual `ranks` (host
+    ints): zero-copy views of the packed prefix of each slot, ready to feed the next call."""
+    cores = []
+    for q, c in enumerate(t.cores):
+        n = ranks[q] * t.d_out[q] * ranks[q + 1]
+        cores.append(c[b].reshape(-1)[:n].view(1, ranks[q], t.d_out[q], ranks[q + 1]))
+    return DeviceTrains(cores, [int(r) for r in ranks], list(t.d_out), None)
 
 
 # ------------------------------------------------------------------------- calls
