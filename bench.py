@@ -40,7 +40,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--workload", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "qft"],
+                    help="qft: the tensorized DFT of PAPER.md:533-566 (N = 2^13, max rank 16) as a chain of "
+                         "12 complex Hadamard zip-ups (SURVEY.md §8(f) f2)")
     ap.add_argument("--members-per-gpu", type=int, default=512)
     ap.add_argument("--cpu-members", type=int, default=8, help="oracle sample size (members) for cpu_baseline")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
@@ -224,8 +226,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
+    if args.impl == "reference" and args.workload == "qft":
+        return run_qft_reference(args, rank)
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.workload == "qft":
+        return run_qft(args, rank, world, local)
 
     import torch
     import torch.distributed as dist
@@ -406,6 +412,153 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+QFT_BASES = [2] * 13
+QFT_RANK = 16
+
+
+def _qft_cfg(world):
+    return {"workload": "f2: tensorized DFT N=2^13 (PAPER.md:533-566) as a chain of 12 complex128 Hadamard "
+                        "zip-ups of the rank-2 factor trains, max rank 16, eps 0",
+            "N": 2 ** 13, "sites": 13, "max_rank": QFT_RANK, "members_per_gpu": 1, "global_batch": max(world, 1),
+            "parallelism": f"replicas x{max(world, 1)}",
+            "l2": "working set < L2 (a latency-bound chain of 12 dependent calls): no flush"}
+
+
+def run_qft(args, rank, world, local):
+    """--workload qft: one step = the whole 12-call chain Y_q = zip-up(T_q o Y_{q-1}); the
+    output ranks of each call are read on the host to size the next (member_view), so the
+    timed region includes those 12 small device->host reads."""
+    import torch
+    import torch.distributed as dist
+    from paper_2602_20226_b200 import qtt
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    T = [t.cores for t in gen.qft_trains(QFT_BASES)]
+    dev = [qtt.to_device(t, dtype=np.complex128) for t in T]
+    n = len(QFT_BASES)
+
+    def chain(inputs, sweeps_out=None):
+        y = inputs[0]
+        keep = []
+        for q in range(1, n):
+            plan = qtt.ZipupPlan("i,i->i", inputs[q], y, 0.0, QFT_RANK, sweeps=sweeps_out is not None)
+            res = plan.run(inputs[q], y)
+            ranks = res.ranks[0].cpu().tolist()            # host sizes for the next call
+            if sweeps_out is not None:
+                sweeps_out.append((list(ranks), res.sweeps[0].cpu().tolist(), list(y.ranks), list(inputs[q].ranks)))
+            y = qtt.member_view(res.out, ranks, 0)
+            keep.append(plan)
+        return y, keep
+
+    for _ in range(max(args.warmup, 3)):
+        y, keep = chain(dev)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    clocks.start()
+    time.sleep(0.25)
+    t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        y, keep = chain(dev)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = qdist.max_over_ranks(t0.elapsed_time(t1) / args.steps, "cuda", dist)
+    units = max(world, 1) * (n - 1) * n                 # site steps per chain, all replicas
+    value = units / (ms * 1e-3)
+    # algorithmic flops (complex: 4 real flops per complex multiply-add pair -> x4 the real model)
+    info = []
+    chain(dev, info)
+    torch.cuda.synchronize()
+    fl = 0.0
+    for ranks, sw, yr, tr in info:
+        f = site_flops("hadamard", ranks, yr, tr, [4] * n, [4] * n, sw)
+        fl += 4.0 * sum(sum(v) for v in f)
+    # e2e: factor trains copied from pinned host memory, result cores copied back, every step
+    hT = [[torch.from_numpy(np.ascontiguousarray(c[None])).pin_memory() for c in t] for t in T]
+    h2d = sum(c.numel() * c.element_size() for t in hT for c in t)
+
+    def e2e_step():
+        for dt_, ht in zip(dev, hT):
+            for dst, src in zip(dt_.cores, ht):
+                dst.copy_(src, non_blocking=True)
+        yy, kk = chain(dev)
+        outs = [c.cpu() for c in yy.cores]
+        return sum(c.numel() * c.element_size() for c in outs)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    d2h = 0
+    for _ in range(args.steps):
+        d2h = e2e_step()
+    a1.record(stream)
+    torch.cuda.synchronize()
+    ems = qdist.max_over_ranks(a0.elapsed_time(a1) / args.steps, "cuda", dist)
+    peaks = fp64_peaks(torch, stream)
+    per_sm = max(peaks["dfma_tflops"], peaks["dmma_tflops"]) / torch.cuda.get_device_properties(local).multi_processor_count
+    achieved = fl / (ms * 1e-3) / 1e12
+    cpu = None
+    dist_err = None
+    if rank == 0 and world == 1:
+        from oracle import qft as oqft
+        ycores = qtt.member_cores(y, y.ranks, 0)
+        dist_err = float(np.linalg.norm(oqft.to_matrix(ycores, QFT_BASES) - oqft.dft_matrix(2 ** 13))) / math.sqrt(2 ** 13)
+        if not args.no_cpu_baseline:
+            c0 = time.perf_counter()
+            oqft.chain(T, QFT_RANK)
+            cdt = time.perf_counter() - c0
+            cpu = {"value": (n - 1) * n / cdt, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+                   "sample": f"one full chain (12 zip-ups) with NumPy complex128 + LAPACK zgesdd, {cdt:.2f} s wall"}
+    if rank == 0:
+        line = {"metric": METRIC + " (f2 Fourier chain)", "value": round(value, 3), "unit": UNIT, "n_gpus": max(world, 1),
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+                "scaling": "replicas", "vs_baseline": None, "dtype": "c128",
+                "data": "the paper's closed-form DFT factor trains (gen.qft_trains)", "config": _qft_cfg(world),
+                "roofline": {"kernel": "k_zipup_c (one CTA per member: the chain has one member)", "bound": "alu",
+                             "achieved": round(achieved, 6), "peak": round(per_sm, 4), "unit": "TFLOP/s",
+                             "frac": round(achieved / per_sm, 5), "traffic": None,
+                             "peak_source": "measured FP64 peak / SM count (one CTA runs the member)"},
+                "distance_over_sqrtN": dist_err, "paper_distance": 9.3e-11,
+                "jacobi_sweeps": {"mean": float(np.mean([v for _, sw, _, _ in info for v in sw[:-1]])),
+                                  "max": int(max(v for _, sw, _, _ in info for v in sw))},
+                "cpu_baseline": cpu,
+                "e2e": {"value": units / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                        "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ems, 3)},
+                "gpu_launches": (n - 1) * args.steps, "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_qft_reference(args, rank):
+    if rank != 0:
+        return
+    from oracle import qft as oqft
+    T = [t.cores for t in gen.qft_trains(QFT_BASES)]
+    n = len(QFT_BASES)
+    for _ in range(args.warmup):
+        oqft.chain(T, QFT_RANK)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oqft.chain(T, QFT_RANK)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = (n - 1) * n / dt
+    line = {"metric": METRIC + " (f2 Fourier chain)", "value": round(value, 3), "unit": UNIT, "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+            "scaling": "replicas", "vs_baseline": None, "dtype": "c128", "impl": "reference",
+            "data": "the paper's closed-form DFT factor trains (gen.qft_trains)", "config": _qft_cfg(1),
+            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": "each step: one full chain (oracle)"},
+            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
 
 
 def run_reference(args, rank, world):

@@ -94,10 +94,11 @@ __device__ void house_qr(Z *H, int rows, int cols, Z *tau, double *red) {
   __shared__ Z s_scal;
   for (int j = 0; j < K; ++j) {
     Z *v = H + (size_t)j * rows;
-    double xn = 0.0;
-    for (int i = j + 1 + tid; i < rows; i += kThreads) xn += abs2(v[i]);
-    xn = block_sum(xn, red);
-    if (tid == 0) {
+    if (warp == 0) {                    // reflector: warp 0 alone (norm by butterfly)
+      double xn = 0.0;
+      for (int i = j + 1 + lane; i < rows; i += 32) xn += abs2(v[i]);
+      xn = warp_sum(xn);
+      if (lane == 0) {
       const Z alpha = v[j];
       Z t{0.0, 0.0};
       Z inv{0.0, 0.0};
@@ -113,13 +114,15 @@ __device__ void house_qr(Z *H, int rows, int cols, Z *tau, double *red) {
       }
       tau[j] = t;
       s_scal = inv;
+      }
+      __syncwarp();
+      const Z inv = s_scal;
+      const Z t = tau[j];
+      if (t.x != 0.0 || t.y != 0.0)
+        for (int i = j + 1 + lane; i < rows; i += 32) v[i] = mul(v[i], inv);
     }
     __syncthreads();
-    const Z inv = s_scal;
     const Z t = tau[j];
-    if (t.x != 0.0 || t.y != 0.0)
-      for (int i = j + 1 + tid; i < rows; i += kThreads) v[i] = mul(v[i], inv);
-    __syncthreads();
     // trailing columns: c <- c - conj(tau) v (v^H c), one warp per column
     if (t.x != 0.0 || t.y != 0.0) {
       const Z ct = conj(t);
@@ -176,6 +179,8 @@ __device__ void form_q(const Z *H, int rows, int K, const Z *tau, Z *Q) {
 // One-sided Jacobi on the columns of A (rows x p, column-major, ld = rows).  Returns sweeps.
 __device__ int jacobi(Z *A, int rows, int p, double noise_eps, double *red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int half = lane >> 4, hl = lane & 15;
+  const unsigned hmask = 0xffffu << (16 * half);
   const double tol = (double)max(rows, 1) * DBL_EPSILON;
   __shared__ int s_rot;
   double tot = 0.0;
@@ -189,7 +194,8 @@ __device__ int jacobi(Z *A, int rows, int p, double noise_eps, double *red) {
     __syncthreads();
     int rot = 0;
     for (int r = 0; r < n - 1; ++r) {
-      for (int pr = warp; pr < n / 2; pr += kWarps) {
+      // one pair per half-warp (16 lanes): 16 pairs of a round in flight across the 8 warps
+      for (int pr = 2 * warp + half; pr < n / 2; pr += 2 * kWarps) {
         // circle method: position 0 fixed, the others rotate
         const int k1 = pr, k2 = n - 1 - pr;
         const int ci = (k1 == 0) ? 0 : 1 + (k1 - 1 + r) % (n - 1);
@@ -198,15 +204,19 @@ __device__ int jacobi(Z *A, int rows, int p, double noise_eps, double *red) {
         Z *ai = A + (size_t)ci * rows, *aj = A + (size_t)cj * rows;
         double al = 0.0, be = 0.0;
         Z g{0.0, 0.0};
-        for (int i = lane; i < rows; i += 32) {
+        for (int i = hl; i < rows; i += 16) {
           const Z x = ai[i], y = aj[i];
           al += abs2(x);
           be += abs2(y);
           g = cfma(x, y, g);
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        g = warp_zsum(g);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {            // four independent butterflies interleave
+          al += __shfl_xor_sync(hmask, al, o);
+          be += __shfl_xor_sync(hmask, be, o);
+          g.x += __shfl_xor_sync(hmask, g.x, o);
+          g.y += __shfl_xor_sync(hmask, g.y, o);
+        }
         const double ag2 = abs2(g);
         if (al > noise && be > noise && ag2 > tol * tol * al * be) {
           const double ag = sqrt(ag2);
@@ -215,14 +225,13 @@ __device__ int jacobi(Z *A, int rows, int p, double noise_eps, double *red) {
           const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
           const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
           const Z sp = scl(s, ph), sm = scl(s, conj(ph));
-          for (int i = lane; i < rows; i += 32) {
+          for (int i = hl; i < rows; i += 16) {
             const Z x = ai[i], y = aj[i];
             ai[i] = sub(scl(c, x), mul(sm, y));
             aj[i] = add(mul(sp, x), scl(c, y));
           }
           rot = 1;
         }
-        __syncwarp();
       }
       __syncthreads();
     }
