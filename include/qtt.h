@@ -124,7 +124,8 @@ size_t qtt_zipup_workspace_bytes(const char *subscripts, const qtt_trains_t *op,
  *                cores are complex doubles (interleaved re, im; 16 bytes).  Same steps in
  *                complex arithmetic (T^H is the conjugate transpose, the carry is U_k^H T, the
  *                Jacobi rotations carry the phase of a_i^H a_j); delta2, norm2 and sigma stay
- *                real f64.  One CTA per member (complex.cu); diag->phase_cycles is ignored.
+ *                real f64.  One CTA per member (complex.cu); diag->phase_cycles gets a2, a3,
+ *                a4, a5+a6 per site as for fp64, with the a1 pre-pass in slot [site 0][3].
  */
 typedef struct {
   double *sigma;          /* device f64 [B*(L-1)*sigma_stride]: singular values of every site

@@ -10,7 +10,8 @@
 //   a3  Householder QR of T^H when m <= n (A = R^H), else A = T
 //   a4  one-sided complex Jacobi on the columns of A: pair (i, j) with a = |a_i|^2,
 //       b = |a_j|^2, g = a_i^H a_j = |g| e^{i phi}; zeta = (b - a) / (2|g|),
-//       t = sign(zeta) / (|zeta| + hypot(1, zeta)), c = 1/sqrt(1+t^2), s = c t;
+//       t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), c = 1/sqrt(1+t^2), s = c t (evaluated
+//       division-free with two MUFU-seeded rsqrt, as the fp64 path);
 //       a_i <- c a_i - s e^{-i phi} a_j,  a_j <- s e^{i phi} a_i + c a_j
 //       (the real rotation of the 2x2 Gram matrix after removing the phase of g);
 //       sweeps until no pair has |g|^2 > tol^2 a b (tol = m eps); noise-level columns as c-A31
@@ -83,6 +84,8 @@ struct Args {
   int *sweeps, *status;
   double eps;
   int max_rank, orth_op;
+  int smem;                            // 1: G, T, H, Q/A, tau in dynamic shared memory
+  long long *cycles;                   // optional [B][L][4]: a2, a3, a4, a5-a6 clocks (a1 in [q=0][3])
 };
 
 // In-place Householder QR of the column-major rows x cols matrix H (ld = rows), K =
@@ -219,12 +222,20 @@ __device__ int jacobi(Z *A, int rows, int p, double noise_eps, double *red) {
         }
         const double ag2 = abs2(g);
         if (al > noise && be > noise && ag2 > tol * tol * al * be) {
-          const double ag = sqrt(ag2);
-          const Z ph = Z{g.x / ag, g.y / ag};             // e^{i phi}
-          const double zeta = (be - al) / (2.0 * ag);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-          const Z sp = scl(s, ph), sm = scl(s, conj(ph));
+          // division-free (as the fp64 path): with d = b - a, y = 1/sqrt(d^2 + 4|g|^2),
+          // c^2 = (1 + |d| y)/2, z = 1/c: c = c^2 z and s e^{i phi} = sign(d) y z g
+          double d = be - al, x2 = fma(d, d, 4.0 * ag2);
+          Z gg = g;
+          if (x2 < 1e-280) {             // keep the MUFU rsqrt seed out of the subnormal range
+            const double sc = 1.0 / fmax(fabs(d), sqrt(ag2));
+            d *= sc; gg = scl(sc, g);
+            x2 = fma(d, d, 4.0 * abs2(gg));
+          }
+          const double y = fast_rsqrt(x2);
+          const double c2 = fma(0.5 * fabs(d), y, 0.5);
+          const double z = fast_rsqrt(c2);
+          const double c = c2 * z, f = copysign(1.0, d) * y * z;
+          const Z sp = scl(f, gg), sm = scl(f, conj(gg));
           for (int i = hl; i < rows; i += 16) {
             const Z x = ai[i], y = aj[i];
             ai[i] = sub(scl(c, x), mul(sm, y));
@@ -294,9 +305,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup_c(Args a) {
   const int b = blockIdx.x, tid = threadIdx.x, L = a.L, L1 = L + 1;
   __shared__ double red[kWarps];
   __shared__ double s_sc[4];
+  extern __shared__ Z zsm[];
   Z *w = a.ws + (size_t)b * a.ws_member;
   Z *Xo = w, *Oo = Xo + a.xo_n, *G = Oo + a.oo_n, *T = G + a.g_n, *H = T + a.t_n, *Q = H + a.t_n,
     *tau = Q + 2 * a.t_n;
+  if (a.smem) {                         // the member's matrices fit on chip (the Fourier chain does)
+    T = zsm; H = T + a.t_n; Q = H + a.t_n; G = Q + 2 * a.t_n; tau = G + a.g_n;
+  }
   char *iw = a.iws + (size_t)b * a.iws_member;
   double *sg = (double *)iw;                      // [pmax]
   double *tail = sg + a.pmax;                     // [pmax + 1]
@@ -305,6 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup_c(Args a) {
   const int ob = (a.op_batch == 1) ? 0 : b;
 
   // ---- a1
+  long long tph = clock64();
   {
     int legs[64];
     for (int q = 0; q < L; ++q) legs[q] = a.dj[q];
@@ -318,6 +334,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup_c(Args a) {
     __syncthreads();
   }
   if (tid == 0) G[0] = Z{1.0, 0.0};
+  if (tid == 0 && a.cycles) a.cycles[(size_t)b * L * 4 + 3] = clock64() - tph;
+  tph = clock64();
   int chi = 1;
   __syncthreads();
   for (int q = 0; q < L; ++q) {
@@ -352,6 +370,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup_c(Args a) {
     }
     __syncthreads();
     Z *Cq = a.Cq[q] + (size_t)b * a.Cq_bs[q];
+    if (tid == 0 && a.cycles) a.cycles[((size_t)b * L + q) * 4 + 0] = clock64() - tph;
+    tph = clock64();
     // ---- a7: last site
     if (q == L - 1) {
       double s = 0.0;
@@ -387,13 +407,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup_c(Args a) {
       }
     }
     __syncthreads();
+    if (tid == 0 && a.cycles) a.cycles[((size_t)b * L + q) * 4 + 1] = clock64() - tph;
+    tph = clock64();
     // ---- a4
     const int sweeps = jacobi(A, m, p, a.eps > 1e-14 ? DBL_EPSILON * DBL_EPSILON : 0.0, red);
-    for (int j = tid; j < p; j += kThreads) {
+    for (int j = tid >> 5; j < p; j += kWarps) {
       double s = 0.0;
-      for (int i = 0; i < m; ++i) s += abs2(A[(size_t)j * m + i]);
-      if (!isfinite(s)) { atomicOr(a.status, 1); s = 0.0; }
-      sg[j] = s;
+      for (int i = tid & 31; i < m; i += 32) s += abs2(A[(size_t)j * m + i]);
+      s = warp_sum(s);
+      if ((tid & 31) == 0) {
+        if (!isfinite(s)) { atomicOr(a.status, 1); s = 0.0; }
+        sg[j] = s;
+      }
     }
     __syncthreads();
     for (int j = tid; j < p; j += kThreads) {
@@ -403,6 +428,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup_c(Args a) {
       perm[rank] = j;
     }
     __syncthreads();
+    if (tid == 0 && a.cycles) a.cycles[((size_t)b * L + q) * 4 + 2] = clock64() - tph;
+    tph = clock64();
     // ---- a5
     if (tid == 0) {
       double acc = 0.0;
@@ -453,6 +480,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup_c(Args a) {
       G[idx] = acc;
     }
     chi = k;
+    if (tid == 0 && a.cycles && q > 0) a.cycles[((size_t)b * L + q) * 4 + 3] = clock64() - tph;
+    tph = clock64();
     __syncthreads();
   }
 }
@@ -492,7 +521,8 @@ size_t complex_workspace_bytes(const Shape &S) {
 }
 
 qtt_status_t complex_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags,
-                           const LargeIO &io, void *workspace, size_t workspace_bytes, cudaStream_t s) {
+                           const LargeIO &io, void *workspace, size_t workspace_bytes, cudaStream_t s,
+                           long long *cycles) {
   if (S.L > 64) { set_error("complex path: n_sites > 64"); return QTT_EUNSUPPORTED; }
   const size_t need = complex_workspace_bytes(S);
   if (!workspace || workspace_bytes < need) {
@@ -530,8 +560,18 @@ qtt_status_t complex_zipup(const Shape &S, const qtt_trains_t *op, const qtt_tra
   a.sigma_stride = io.sigma_stride; a.sweeps = io.sweeps; a.status = io.status;
   a.eps = io.eps; a.max_rank = io.max_rank;
   a.orth_op = (flags & QTT_NO_OPERATOR_ORTH) ? 0 : 1;
+  a.cycles = cycles;
   QTT_CUDA_TRY(cudaMemsetAsync(io.status, 0, sizeof(int32_t), s));
-  cplx::k_zipup_c<<<S.B, kThreads, 0, s>>>(a);
+  const size_t smem = (size_t)(4 * tn + gn + std::max(pmax, 64)) * 16;
+  a.smem = smem <= 200 * 1024 ? 1 : 0;
+  if (a.smem) {
+    static bool attr = false;
+    if (!attr) {
+      QTT_CUDA_TRY(cudaFuncSetAttribute(cplx::k_zipup_c, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+  }
+  cplx::k_zipup_c<<<S.B, kThreads, a.smem ? smem : 0, s>>>(a);
   QTT_CUDA_TRY(cudaGetLastError());
   return QTT_OK;
 }

@@ -34,7 +34,8 @@ size_t large_workspace_bytes(const Shape &S);
 // complex128 path (complex.cu): one CTA per member, every step
 size_t complex_workspace_bytes(const Shape &S);
 qtt_status_t complex_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags,
-                           const struct LargeIO &io, void *workspace, size_t workspace_bytes, cudaStream_t s);
+                           const struct LargeIO &io, void *workspace, size_t workspace_bytes, cudaStream_t s,
+                           long long *cycles = nullptr);
 qtt_status_t large_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags,
                          const LargeIO &io, void *workspace, size_t workspace_bytes, cudaStream_t s);
 

@@ -1087,7 +1087,7 @@ qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt
     g_err[0] = 0;
     if (events) for (int i = 0; i < 3; ++i) QTT_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[i], s));
     LargeIO io{out, out_ranks, delta2, norm2, sigma, sigma_stride, sweeps, status, eps, max_rank};
-    qtt_status_t cst = complex_zipup(S, op, x, flags, io, workspace, workspace_bytes, s);
+    qtt_status_t cst = complex_zipup(S, op, x, flags, io, workspace, workspace_bytes, s, cycles);
     if (cst != QTT_OK) return cst;
     if (events) QTT_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[3], s));
     return QTT_OK;
