@@ -34,7 +34,7 @@ namespace qtt {
 
 namespace cplx {
 
-struct Z {
+struct __align__(16) Z {
   double x, y;
 };
 __device__ __forceinline__ Z mk(double a, double b) { return Z{a, b}; }
@@ -207,7 +207,17 @@ __device__ int jacobi(Z *A, int rows, int p, double noise_eps, double *red) {
         Z *ai = A + (size_t)ci * rows, *aj = A + (size_t)cj * rows;
         double al = 0.0, be = 0.0;
         Z g{0.0, 0.0};
-        for (int i = hl; i < rows; i += 16) {
+        double al2 = 0.0, be2 = 0.0;
+        Z g2{0.0, 0.0};
+        int i = hl;
+        for (; i + 16 < rows; i += 32) {                // two independent chains
+          const Z x = ai[i], y = aj[i], x1 = ai[i + 16], y1 = aj[i + 16];
+          al += abs2(x); al2 += abs2(x1);
+          be += abs2(y); be2 += abs2(y1);
+          g = cfma(x, y, g); g2 = cfma(x1, y1, g2);
+        }
+        al += al2; be += be2; g = add(g, g2);
+        for (; i < rows; i += 16) {
           const Z x = ai[i], y = aj[i];
           al += abs2(x);
           be += abs2(y);
@@ -236,6 +246,7 @@ __device__ int jacobi(Z *A, int rows, int p, double noise_eps, double *red) {
           const double z = fast_rsqrt(c2);
           const double c = c2 * z, f = copysign(1.0, d) * y * z;
           const Z sp = scl(f, gg), sm = scl(f, conj(gg));
+#pragma unroll 4
           for (int i = hl; i < rows; i += 16) {
             const Z x = ai[i], y = aj[i];
             ai[i] = sub(scl(c, x), mul(sm, y));
