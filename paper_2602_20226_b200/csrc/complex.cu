@@ -189,6 +189,18 @@ __device__ int jacobi(Z *A, int rows, int p, double noise_eps, double *red) {
   double tot = 0.0;
   for (int i = tid; i < rows * p; i += kThreads) tot += abs2(A[i]);
   tot = block_sum(tot, red);
+  // exact power-of-two scaling to ||A||_F^2 in [1, 4), undone at the end (reading c-A33):
+  // keeps |g|^2 and a b of the rotation test clear of under/overflow for any input magnitude
+  double scale = 1.0;
+  if (tot > 0.0 && isfinite(tot)) {
+    const int e = -(ilogb(tot) >> 1);
+    if (e != 0) {
+      scale = ldexp(1.0, e);
+      tot = ldexp(tot, 2 * e);
+      for (int i = tid; i < rows * p; i += kThreads) A[i] = scl(scale, A[i]);
+      __syncthreads();
+    }
+  }
   const double noise = noise_eps * tot;
   const int n = p + (p & 1);
   int sweep = 0;
@@ -262,6 +274,11 @@ __device__ int jacobi(Z *A, int rows, int p, double noise_eps, double *red) {
     const int any = s_rot;
     __syncthreads();
     if (!any) { ++sweep; break; }
+  }
+  if (scale != 1.0) {
+    const double inv = 1.0 / scale;
+    for (int i = tid; i < rows * p; i += kThreads) A[i] = scl(inv, A[i]);
+    __syncthreads();
   }
   return sweep;
 }

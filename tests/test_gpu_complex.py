@@ -130,3 +130,38 @@ def test_qft_paper_distances_2_13(lib):
             assert abs(d - paper) <= 0.06 * paper, (R, d, paper)
         else:
             assert d <= paper, (R, d, paper)
+
+
+def test_complex_batch_shared_operator_and_edges(lib):
+    """Batch of 3 members with one shared complex operator, a single-site train, an all-zero
+    train, and inputs at 1e-140 (the Jacobi's squares stay in range)."""
+    import torch
+    from parity import compare
+    rng = np.random.default_rng(43)
+    dims = [2] * 9
+    xs = [_c(gen.random_mps(dims, 10, rng).cores, rng) for _ in range(3)]
+    op = _c(gen.random_mpo(dims, 3, rng, 0.5).cores, rng)
+    xd = lib.to_device([np.stack([x[q] for x in xs]) for q in range(len(dims))], dtype=np.complex128)
+    od = lib.to_device(op, mpo=True, dtype=np.complex128)
+    plan = lib.ZipupPlan("ij,j->i", od, xd, 1e-10, 16, sigma_stride=64)
+    res = plan.run(od, xd)
+    torch.cuda.synchronize()
+    assert int(res.status.item()) == 0
+    for b in range(3):
+        ranks = res.ranks[b].cpu().tolist()
+        cores = lib.member_cores(res.out, ranks, b)
+        compare("matvec", op, xs[b], 1e-10, 16, cores, ranks, res.sigma[b].cpu().numpy(),
+                res.delta2[b].cpu().numpy(), float(res.norm2[b].item()))
+    # single site
+    x1 = [rng.standard_normal((1, 5, 1)) + 1j * rng.standard_normal((1, 5, 1))]
+    o1 = [rng.standard_normal((1, 5, 1)) + 1j * rng.standard_normal((1, 5, 1))]
+    _check_dense(lib, "hadamard", o1, x1, 0.0, 0)
+    # zero input
+    z = [np.zeros((1, 2, 2), complex), np.zeros((2, 2, 2), complex), np.zeros((2, 2, 1), complex)]
+    r0 = run_c(lib, "i->i", None, z, 1e-8, 4)
+    assert r0.ranks[0].cpu().tolist() == [1, 1, 1, 1] and float(r0.norm2[0].item()) == 0.0
+    # tiny magnitudes
+    a = _c(gen.random_mps([2] * 8, 6, rng).cores, rng)
+    b = _c(gen.random_mps([2] * 8, 6, rng).cores, rng)
+    a[0] = a[0] * 1e-140
+    _check_dense(lib, "hadamard", a, b, 1e-12, 0)
