@@ -69,7 +69,12 @@ enum { QTT_F64 = 0, QTT_F32 = 1, QTT_C128 = 2 };
 
 /* Flags for qtt_zipup. */
 enum {
-  QTT_NO_OPERATOR_ORTH = 1u << 0  /* do not right-orthonormalise the operator (SURVEY c-A2) */
+  QTT_NO_OPERATOR_ORTH = 1u << 0, /* do not right-orthonormalise the operator (SURVEY c-A2) */
+  QTT_WINDOW2 = 1u << 1           /* super-core of N = 2 sites:
+                                     site q's split is (chi d_q) x (d_{q+1} w_{q+2} r_{q+2}), its
+                                     rank capped at w_{q+1} r_{q+1} (the exact product's bond,
+                                     reading c-A35); the last split leaves C_{L-1} = diag(s) V^H.
+                                     Runs on the per-member path (one CTA per member)          */
 };
 
 /* ---------------------------------------------------------------------------------------
@@ -81,9 +86,13 @@ enum {
 qtt_status_t qtt_zipup_capacity(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
                                 int32_t max_rank, int32_t *cap);
 
-/* qtt_zipup_workspace_bytes -- device scratch needed by qtt_zipup for these shapes. */
+/* qtt_zipup_workspace_bytes -- device scratch needed by qtt_zipup for these shapes (flags 0);
+ * qtt_zipup_workspace_bytes_flags -- the same for the given qtt_zipup flags (QTT_WINDOW2
+ * needs the larger window-2 super-cores).  0 on error (qtt_last_error). */
 size_t qtt_zipup_workspace_bytes(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
                                  const qtt_trains_t *out);
+size_t qtt_zipup_workspace_bytes_flags(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                                       const qtt_trains_t *out, uint32_t flags);
 
 /* ---------------------------------------------------------------------------------------
  * qtt_zipup -- y = op(x) truncated by the zip-up sweep (window N = 1).

@@ -99,3 +99,98 @@ def zipup(kind: str, op: Optional[Sequence[np.ndarray]], x: Sequence[np.ndarray]
         ranks.append(k)
     norm = float(np.linalg.norm(cores[-1]))
     return {"cores": cores, "ranks": ranks, "delta2": delta2, "sigmas": sigmas, "norm": norm}
+
+
+def _absorb(kind: str, C: np.ndarray, Xq: np.ndarray, Oq: Optional[np.ndarray]) -> np.ndarray:
+    """Extend the super-core C (chi, P, w, r) -- P the flattened physical indices of the
+    pending sites -- by one site, exactly (Eq. einsum): returns
+    (chi, P, i, w', r')."""
+    if kind == "matvec":
+        return np.einsum("cpwr,rjs,wijv->cpivs", C, Xq, Oq)
+    if kind == "hadamard":
+        return np.einsum("cpab,bis,aiv->cpivs", C, Xq, Oq)
+    if kind == "truncate":
+        return np.einsum("cpr,ris->cpis", C[:, :, 0, :], Xq)[:, :, :, None, :]
+    raise ValueError(kind)
+
+
+def zipup_window(kind: str, op: Optional[Sequence[np.ndarray]], x: Sequence[np.ndarray], eps: float,
+                 max_rank: int, window: int, orth_operator: bool = True,
+                 force_ranks: Optional[Sequence[int]] = None):
+    """Zip-up with a super-core of N = `window` sites ("the first N-cores
+    (1 <= N <= n) are contracted exactly").  Same return dict as zipup().
+
+      1. right-orthonormalise the operands
+      2. contract the first N sites exactly into the super-core S (chi=1, i_0..i_{N-1}, w, r)
+      3. split S (rows (chi, i_first), columns the rest) by SVD, truncated by the rule of
+         SPEC.md:299 and (reading c-A35) by k <= w_{q+1} r_{q+1}, the exact rank of the product
+         at that bond; emit U_k; the carry diag(s_k) V_k^H keeps the pending physical indices
+         (PAPER.md:269)
+      4. extend the carry by the next site and repeat
+      5. when no site is left, the super-core is "fully decomposed": the same
+         split repeated until one physical index remains, which is the last core.
+    window = 1 reproduces zipup(); window = L is the exact product followed by TT-SVD
+    (SPEC.md:394-396).
+    """
+    N = int(window)
+    cplx = any(np.iscomplexobj(c) for c in x) or (op is not None and any(np.iscomplexobj(c) for c in op))
+    dt = np.complex128 if cplx else np.float64
+    X = right_orthonormalize([np.asarray(c, dtype=dt) for c in x])                # step 1
+    O = None
+    if kind != "truncate":
+        O = [np.asarray(c, dtype=dt) for c in op]
+        if orth_operator:
+            O = right_orthonormalize(O)
+    L = len(X)
+    N = max(1, min(N, L))
+    bond = []                                  # w_q * r_q of the exact product at bond q
+    for q in range(L + 1):
+        rx = X[q].shape[0] if q < L else 1
+        ro = (O[q].shape[0] if q < L else 1) if O is not None else 1
+        bond.append(rx * ro)
+    S = np.ones((1, 1, 1, 1), dtype=dt)        # (chi, P, w, r) with P = 1 (no pending site)
+    dims: List[int] = []                       # digit sizes of the pending sites
+    nxt = 0
+    while nxt < N:                                                                 # step 2
+        S = _absorb(kind, S, X[nxt], None if O is None else O[nxt])
+        dims.append(X[nxt].shape[1] if kind != "matvec" else O[nxt].shape[1])
+        S = S.reshape(S.shape[0], -1, S.shape[-2], S.shape[-1])
+        nxt += 1
+    cores: List[np.ndarray] = []
+    delta2: List[float] = []
+    sigmas: List[np.ndarray] = []
+    ranks = [1]
+    q = 0
+    while True:
+        chi = S.shape[0]
+        if q == L - 1:                          # one physical index left: the last core
+            cores.append(S.reshape(chi, dims[0], 1))
+            ranks.append(1)
+            break
+        d0 = dims[0]
+        M = S.reshape(chi * d0, -1)                                                # step 3
+        U, sig, Vh = _svd(M)
+        if float(np.sum(np.abs(sig) ** 2)) == 0.0:
+            k = 1
+            U = np.zeros((M.shape[0], 1), dtype=dt); U[0, 0] = 1.0
+            sig = np.zeros(1); Vh = np.zeros((1, M.shape[1]), dtype=dt)
+        else:
+            k = truncation_rank(sig, eps, max_rank)
+            k = min(k, bond[q + 1])              # c-A35
+        if force_ranks is not None:
+            k = int(force_ranks[q + 1])
+        delta2.append(tail_sum(sig, k))
+        sigmas.append(sig.copy())
+        cores.append(U[:, :k].reshape(chi, d0, k))
+        rest = S.shape[2:]                      # (w, r)
+        dims = dims[1:]
+        S = (sig[:k, None] * Vh[:k]).reshape((k, int(np.prod(dims)) if dims else 1) + rest)
+        ranks.append(k)
+        q += 1
+        if nxt < L:                                                                # step 4
+            S = _absorb(kind, S, X[nxt], None if O is None else O[nxt])
+            dims.append(X[nxt].shape[1] if kind != "matvec" else O[nxt].shape[1])
+            S = S.reshape(S.shape[0], -1, S.shape[-2], S.shape[-1])
+            nxt += 1
+    norm = float(np.linalg.norm(cores[-1]))
+    return {"cores": cores, "ranks": ranks, "delta2": delta2, "sigmas": sigmas, "norm": norm}

@@ -61,19 +61,44 @@ __device__ __forceinline__ Z warp_zsum(Z v) {
   return v;
 }
 
+// the same operations on a real double: the kernel below is instantiated for both
+__device__ __forceinline__ double add(double a, double b) { return a + b; }
+__device__ __forceinline__ double sub(double a, double b) { return a - b; }
+__device__ __forceinline__ double mul(double a, double b) { return a * b; }
+__device__ __forceinline__ double conj(double a) { return a; }
+__device__ __forceinline__ double scl(double s, double a) { return s * a; }
+__device__ __forceinline__ double abs2(double a) { return a * a; }
+__device__ __forceinline__ double cfma(double a, double b, double acc) { return fma(a, b, acc); }
+__device__ __forceinline__ double zfma(double a, double b, double acc) { return fma(a, b, acc); }
+__device__ __forceinline__ double warp_zsum(double v) { return warp_sum(v); }
+__device__ __forceinline__ double re(double a) { return a; }
+__device__ __forceinline__ double im(double) { return 0.0; }
+__device__ __forceinline__ double re(Z a) { return a.x; }
+__device__ __forceinline__ double im(Z a) { return a.y; }
+__device__ __forceinline__ bool nz(double a) { return a != 0.0; }
+__device__ __forceinline__ bool nz(Z a) { return a.x != 0.0 || a.y != 0.0; }
+template <typename S> __device__ __forceinline__ S mk(double r, double i);
+template <> __device__ __forceinline__ double mk<double>(double r, double) { return r; }
+template <> __device__ __forceinline__ Z mk<Z>(double r, double i) { return Z{r, i}; }
+// v + (v of lane ^ o) within `mask`
+__device__ __forceinline__ double shx(double v, unsigned mask, int o) { return v + __shfl_xor_sync(mask, v, o); }
+__device__ __forceinline__ Z shx(Z v, unsigned mask, int o) {
+  return Z{v.x + __shfl_xor_sync(mask, v.x, o), v.y + __shfl_xor_sync(mask, v.y, o)};
+}
+
 constexpr int kMaxSweeps = 60;
 
 struct Args {
   int L, B, kind, op_batch;
   int d[64], dj[64], xr0[65], or0[65], cap[65];
   long long xoff[65], ooff[65];        // per-member element offsets of the compact operand copies
-  const Z *xsrc[64];
-  const Z *osrc[64];
-  Z *Cq[64];
+  const void *xsrc[64];
+  const void *osrc[64];
+  void *Cq[64];
   long long Cq_bs[64];
   long long x_bs[64], o_bs[64];        // member stride of the input cores (elements)
-  Z *ws;                               // per-member complex scratch
-  long long ws_member;                 // complex elements per member
+  void *ws;                            // per-member scratch (scalars of the instantiated type)
+  long long ws_member;                 // scalars per member
   long long xo_n, oo_n, g_n, t_n;      // sizes of the member's regions
   char *iws;                           // per-member int/double scratch
   long long iws_member;                // bytes per member
@@ -86,60 +111,62 @@ struct Args {
   int max_rank, orth_op;
   int smem;                            // 1: G, T, H, Q/A, tau in dynamic shared memory
   long long *cycles;                   // optional [B][L][4]: a2, a3, a4, a5-a6 clocks (a1 in [q=0][3])
+  int window;                          // 1, or 2 (f4)
 };
 
 // In-place Householder QR of the column-major rows x cols matrix H (ld = rows), K =
 // min(rows, cols) reflectors (LAPACK zgeqr2 conventions: H_j = I - tau_j v_j v_j^H,
 // v_j[j] = 1, beta real on the diagonal; H_j^H applied to the trailing columns).
-__device__ void house_qr(Z *H, int rows, int cols, Z *tau, double *red) {
+template <typename S>
+__device__ void house_qr(S *H, int rows, int cols, S *tau, double *red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = min(rows, cols);
-  __shared__ Z s_scal;
+  __shared__ S s_scal;
   for (int j = 0; j < K; ++j) {
-    Z *v = H + (size_t)j * rows;
+    S *v = H + (size_t)j * rows;
     if (warp == 0) {                    // reflector: warp 0 alone (norm by butterfly)
       double xn = 0.0;
       for (int i = j + 1 + lane; i < rows; i += 32) xn += abs2(v[i]);
       xn = warp_sum(xn);
       if (lane == 0) {
-      const Z alpha = v[j];
-      Z t{0.0, 0.0};
-      Z inv{0.0, 0.0};
-      if (xn == 0.0 && alpha.y == 0.0) {
-        t = Z{0.0, 0.0};
+      const S alpha = v[j];
+      S t = mk<S>(0.0, 0.0);
+      S inv = mk<S>(0.0, 0.0);
+      if (xn == 0.0 && im(alpha) == 0.0) {
+        t = mk<S>(0.0, 0.0);
       } else {
-        const double beta = -copysign(sqrt(abs2(alpha) + xn), alpha.x);
-        t = Z{(beta - alpha.x) / beta, -alpha.y / beta};
-        const Z den = Z{alpha.x - beta, alpha.y};          // 1 / (alpha - beta)
-        const double dd = abs2(den);
-        inv = Z{den.x / dd, -den.y / dd};
-        v[j] = Z{beta, 0.0};
+        const double beta = -copysign(sqrt(abs2(alpha) + xn), re(alpha));
+        t = mk<S>((beta - re(alpha)) / beta, -im(alpha) / beta);
+        const double dr = re(alpha) - beta, di = im(alpha);   // 1 / (alpha - beta)
+        const double dd = dr * dr + di * di;
+        inv = mk<S>(dr / dd, -di / dd);
+        v[j] = mk<S>(beta, 0.0);
       }
       tau[j] = t;
       s_scal = inv;
       }
       __syncwarp();
-      const Z inv = s_scal;
-      const Z t = tau[j];
-      if (t.x != 0.0 || t.y != 0.0)
+      const S inv = s_scal;
+      const S t = tau[j];
+      if (nz(t))
         for (int i = j + 1 + lane; i < rows; i += 32) v[i] = mul(v[i], inv);
     }
     __syncthreads();
-    const Z t = tau[j];
+    const S t = tau[j];
     // trailing columns: c <- c - conj(tau) v (v^H c), one warp per column
-    if (t.x != 0.0 || t.y != 0.0) {
-      const Z ct = conj(t);
+    if (nz(t)) {
+      const S ct = conj(t);
       for (int c = j + 1 + warp; c < cols; c += kWarps) {
-        Z *col = H + (size_t)c * rows;
-        Z w{0.0, 0.0};
+        S *col = H + (size_t)c * rows;
+        S w = mk<S>(0.0, 0.0);
         for (int i = j + lane; i < rows; i += 32) {
-          const Z vi = (i == j) ? Z{1.0, 0.0} : v[i];
+          const S vi = (i == j) ? mk<S>(1.0, 0.0) : v[i];
           w = cfma(vi, col[i], w);
         }
         w = warp_zsum(w);
-        const Z f = mul(ct, w);
+        const S f = mul(ct, w);
         for (int i = j + lane; i < rows; i += 32) {
-          const Z vi = (i == j) ? Z{1.0, 0.0} : v[i];
+          const S vi = (i == j) ? mk<S>(1.0, 0.0) : v[i];
           col[i] = sub(col[i], mul(f, vi));
         }
       }
@@ -150,28 +177,29 @@ __device__ void house_qr(Z *H, int rows, int cols, Z *tau, double *red) {
 
 // Q (rows x K, column-major, ld = rows) = H_0 H_1 ... H_{K-1} applied to the first K columns
 // of the identity (LAPACK zung2r), from the reflectors left in H by house_qr.
-__device__ void form_q(const Z *H, int rows, int K, const Z *tau, Z *Q) {
+template <typename S>
+__device__ void form_q(const S *H, int rows, int K, const S *tau, S *Q) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int idx = tid; idx < rows * K; idx += kThreads) {
     const int i = idx % rows, c = idx / rows;
-    Q[idx] = Z{(i == c) ? 1.0 : 0.0, 0.0};
+    Q[idx] = mk<S>((i == c) ? 1.0 : 0.0, 0.0);
   }
   __syncthreads();
   for (int j = K - 1; j >= 0; --j) {
-    const Z t = tau[j];
-    if (t.x == 0.0 && t.y == 0.0) continue;
-    const Z *v = H + (size_t)j * rows;
+    const S t = tau[j];
+    if (!nz(t)) continue;
+    const S *v = H + (size_t)j * rows;
     for (int c = j + warp; c < K; c += kWarps) {
-      Z *col = Q + (size_t)c * rows;
-      Z w{0.0, 0.0};
+      S *col = Q + (size_t)c * rows;
+      S w = mk<S>(0.0, 0.0);
       for (int i = j + lane; i < rows; i += 32) {
-        const Z vi = (i == j) ? Z{1.0, 0.0} : v[i];
+        const S vi = (i == j) ? mk<S>(1.0, 0.0) : v[i];
         w = cfma(vi, col[i], w);
       }
       w = warp_zsum(w);
-      const Z f = mul(t, w);
+      const S f = mul(t, w);
       for (int i = j + lane; i < rows; i += 32) {
-        const Z vi = (i == j) ? Z{1.0, 0.0} : v[i];
+        const S vi = (i == j) ? mk<S>(1.0, 0.0) : v[i];
         col[i] = sub(col[i], mul(f, vi));
       }
     }
@@ -180,7 +208,8 @@ __device__ void form_q(const Z *H, int rows, int K, const Z *tau, Z *Q) {
 }
 
 // One-sided Jacobi on the columns of A (rows x p, column-major, ld = rows).  Returns sweeps.
-__device__ int jacobi(Z *A, int rows, int p, double noise_eps, double *red) {
+template <typename S>
+__device__ int jacobi(S *A, int rows, int p, double noise_eps, double *red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int half = lane >> 4, hl = lane & 15;
   const unsigned hmask = 0xffffu << (16 * half);
@@ -216,38 +245,37 @@ __device__ int jacobi(Z *A, int rows, int p, double noise_eps, double *red) {
         const int ci = (k1 == 0) ? 0 : 1 + (k1 - 1 + r) % (n - 1);
         const int cj = 1 + (k2 - 1 + r) % (n - 1);
         if (ci >= p || cj >= p) continue;
-        Z *ai = A + (size_t)ci * rows, *aj = A + (size_t)cj * rows;
+        S *ai = A + (size_t)ci * rows, *aj = A + (size_t)cj * rows;
         double al = 0.0, be = 0.0;
-        Z g{0.0, 0.0};
+        S g = mk<S>(0.0, 0.0);
         double al2 = 0.0, be2 = 0.0;
-        Z g2{0.0, 0.0};
+        S g2 = mk<S>(0.0, 0.0);
         int i = hl;
         for (; i + 16 < rows; i += 32) {                // two independent chains
-          const Z x = ai[i], y = aj[i], x1 = ai[i + 16], y1 = aj[i + 16];
+          const S x = ai[i], y = aj[i], x1 = ai[i + 16], y1 = aj[i + 16];
           al += abs2(x); al2 += abs2(x1);
           be += abs2(y); be2 += abs2(y1);
           g = cfma(x, y, g); g2 = cfma(x1, y1, g2);
         }
         al += al2; be += be2; g = add(g, g2);
         for (; i < rows; i += 16) {
-          const Z x = ai[i], y = aj[i];
+          const S x = ai[i], y = aj[i];
           al += abs2(x);
           be += abs2(y);
           g = cfma(x, y, g);
         }
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) {            // four independent butterflies interleave
-          al += __shfl_xor_sync(hmask, al, o);
-          be += __shfl_xor_sync(hmask, be, o);
-          g.x += __shfl_xor_sync(hmask, g.x, o);
-          g.y += __shfl_xor_sync(hmask, g.y, o);
+          al = shx(al, hmask, o);
+          be = shx(be, hmask, o);
+          g = shx(g, hmask, o);
         }
         const double ag2 = abs2(g);
         if (al > noise && be > noise && ag2 > tol * tol * al * be) {
           // division-free (as the fp64 path): with d = b - a, y = 1/sqrt(d^2 + 4|g|^2),
           // c^2 = (1 + |d| y)/2, z = 1/c: c = c^2 z and s e^{i phi} = sign(d) y z g
           double d = be - al, x2 = fma(d, d, 4.0 * ag2);
-          Z gg = g;
+          S gg = g;
           if (x2 < 1e-280) {             // keep the MUFU rsqrt seed out of the subnormal range
             const double sc = 1.0 / fmax(fabs(d), sqrt(ag2));
             d *= sc; gg = scl(sc, g);
@@ -257,10 +285,10 @@ __device__ int jacobi(Z *A, int rows, int p, double noise_eps, double *red) {
           const double c2 = fma(0.5 * fabs(d), y, 0.5);
           const double z = fast_rsqrt(c2);
           const double c = c2 * z, f = copysign(1.0, d) * y * z;
-          const Z sp = scl(f, gg), sm = scl(f, conj(gg));
+          const S sp = scl(f, gg), sm = scl(f, conj(gg));
 #pragma unroll 4
           for (int i = hl; i < rows; i += 16) {
-            const Z x = ai[i], y = aj[i];
+            const S x = ai[i], y = aj[i];
             ai[i] = sub(scl(c, x), mul(sm, y));
             aj[i] = add(mul(sp, x), scl(c, y));
           }
@@ -285,14 +313,15 @@ __device__ int jacobi(Z *A, int rows, int p, double noise_eps, double *red) {
 
 // a1 for one operand of member b: copy its cores into the compact slots `dst` (offsets off[q])
 // and right-orthonormalise in place; rk[0..L] receives the ranks.
-__device__ void orth_operand(const Args &a, const Z *const *src, const long long *sbs, int member, const int *legs,
-                             const int *r0, const long long *off, Z *dst, int *rk, bool orth, Z *H, Z *Q, Z *tau,
+template <typename S>
+__device__ void orth_operand(const Args &a, const void *const *src, const long long *sbs, int member, const int *legs,
+                             const int *r0, const long long *off, S *dst, int *rk, bool orth, S *H, S *Q, S *tau,
                              double *red) {
   const int tid = threadIdx.x;
   const int L = a.L;
   for (int q = 0; q < L; ++q) {
     const long long n = (long long)r0[q] * legs[q] * r0[q + 1];
-    const Z *s = src[q] + (size_t)member * sbs[q];
+    const S *s = static_cast<const S *>(src[q]) + (size_t)member * sbs[q];
     for (long long i = tid; i < n; i += kThreads) dst[off[q] + i] = s[i];
   }
   if (tid == 0)
@@ -301,7 +330,7 @@ __device__ void orth_operand(const Args &a, const Z *const *src, const long long
   if (!orth) return;
   for (int q = L - 1; q >= 1; --q) {
     const int r = rk[q], c = legs[q] * rk[q + 1];
-    Z *core = dst + off[q];
+    S *core = dst + off[q];
     // H = M^T (c x r, column-major): H[j + i c] = M[i, j] = core[i c + j] -- the same storage
     for (int idx = tid; idx < r * c; idx += kThreads) H[idx] = core[idx];
     __syncthreads();
@@ -312,13 +341,13 @@ __device__ void orth_operand(const Args &a, const Z *const *src, const long long
     for (int idx = tid; idx < k * c; idx += kThreads) core[idx] = Q[idx];
     // core q-1 (rows = r_{q-1} legs_{q-1}, cols r) <- core q-1 R^T (cols k); R = k x r upper
     // (in H: R[i, j] = H[i + j c] for i <= j)
-    Z *prev = dst + off[q - 1];
+    S *prev = dst + off[q - 1];
     const int pr = rk[q - 1] * legs[q - 1];
     // stage prev into Q's space is not needed: compute into the tail of Q (pr x k)
-    Z *tmp = Q + (size_t)c * k;
+    S *tmp = Q + (size_t)c * k;
     for (int idx = tid; idx < pr * k; idx += kThreads) {
       const int row = idx / k, kk = idx % k;
-      Z acc{0.0, 0.0};
+      S acc = mk<S>(0.0, 0.0);
       for (int j = kk; j < r; ++j) acc = zfma(prev[(size_t)row * r + j], H[kk + (size_t)j * c], acc);   // R^T[j,kk] = R[kk,j]
       tmp[idx] = acc;
     }
@@ -329,13 +358,53 @@ __device__ void orth_operand(const Args &a, const Z *const *src, const long long
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_zipup_c(Args a) {
+// a2 for one site: T[(c,i),(w',r')] = sum G[c,w,r] x[r,j,r'] op[w,i,j,w'] with `rows` carry
+// rows c (for window 2 the rows are (chi, pending digit), so the same formula applies)
+template <typename S>
+__device__ void contract(const Args &a, int rows, int d, int dj, int w, int w2, int r, int r2, const S *G, const S *X,
+                         const S *O, S *T) {
+  const int n = w2 * r2;
+  for (int idx = threadIdx.x; idx < rows * d * n; idx += kThreads) {
+    const int rr2 = idx % r2, ww2 = (idx / r2) % w2, ii = (idx / n) % d, c = idx / (n * d);
+    S acc = mk<S>(0.0, 0.0);
+    if (a.kind == TRUNCATE) {
+      for (int rr = 0; rr < r; ++rr) acc = zfma(G[(size_t)c * r + rr], X[((size_t)rr * dj + ii) * r2 + rr2], acc);
+    } else if (a.kind == HADAMARD) {
+      for (int ww = 0; ww < w; ++ww) {
+        const S o = O[((size_t)ww * d + ii) * w2 + ww2];
+        S t = mk<S>(0.0, 0.0);
+        for (int rr = 0; rr < r; ++rr) t = zfma(G[((size_t)c * w + ww) * r + rr], X[((size_t)rr * d + ii) * r2 + rr2], t);
+        acc = zfma(o, t, acc);
+      }
+    } else {
+      for (int ww = 0; ww < w; ++ww)
+        for (int jj = 0; jj < dj; ++jj) {
+          const S o = O[(((size_t)ww * d + ii) * dj + jj) * w2 + ww2];
+          S t = mk<S>(0.0, 0.0);
+          for (int rr = 0; rr < r; ++rr)
+            t = zfma(G[((size_t)c * w + ww) * r + rr], X[((size_t)rr * dj + jj) * r2 + rr2], t);
+          acc = zfma(o, t, acc);
+        }
+    }
+    T[idx] = acc;
+  }
+  __syncthreads();
+}
+
+// One CTA per member.  Window 1: site q's matrix is T (chi d_q) x (w' r').  Window 2
+// (PAPER.md:266 N = 2): the carry keeps the pending digit, rows
+// (chi_{q}, i_q), and absorbing site q+1 gives the super-core split as (chi d_q) x
+// (d_{q+1} w' r') -- the same memory read with another row/column split; its rank is capped
+// at w_{q+1} r_{q+1} (reading c-A35), and the last split leaves C_{L-1} = diag(s) V^H.
+template <typename S>
+__global__ void __launch_bounds__(kThreads, 1) k_zipup(Args a) {
   const int b = blockIdx.x, tid = threadIdx.x, L = a.L, L1 = L + 1;
   __shared__ double red[kWarps];
   __shared__ double s_sc[4];
-  extern __shared__ Z zsm[];
-  Z *w = a.ws + (size_t)b * a.ws_member;
-  Z *Xo = w, *Oo = Xo + a.xo_n, *G = Oo + a.oo_n, *T = G + a.g_n, *H = T + a.t_n, *Q = H + a.t_n,
+  extern __shared__ __align__(16) unsigned char zsm_raw[];
+  S *zsm = reinterpret_cast<S *>(zsm_raw);
+  S *w0 = static_cast<S *>(a.ws) + (size_t)b * a.ws_member;
+  S *Xo = w0, *Oo = Xo + a.xo_n, *G = Oo + a.oo_n, *T = G + a.g_n, *H = T + a.t_n, *Q = H + a.t_n,
     *tau = Q + 2 * a.t_n;
   if (a.smem) {                         // the member's matrices fit on chip (the Fourier chain does)
     T = zsm; H = T + a.t_n; Q = H + a.t_n; G = Q + 2 * a.t_n; tau = G + a.g_n;
@@ -346,86 +415,74 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup_c(Args a) {
   int *perm = (int *)(tail + a.pmax + 1);         // [pmax]
   int *xr = perm + a.pmax, *orr = xr + L1;        // [L+1] each
   const int ob = (a.op_batch == 1) ? 0 : b;
+  const bool win2 = a.window == 2 && L >= 2;
 
   // ---- a1
   long long tph = clock64();
   {
     int legs[64];
     for (int q = 0; q < L; ++q) legs[q] = a.dj[q];
-    orth_operand(a, a.xsrc, a.x_bs, b, legs, a.xr0, a.xoff, Xo, xr, true, H, Q, tau, red);
+    orth_operand<S>(a, a.xsrc, a.x_bs, b, legs, a.xr0, a.xoff, Xo, xr, true, H, Q, tau, red);
     if (a.kind != TRUNCATE) {
       for (int q = 0; q < L; ++q) legs[q] = (a.kind == MATVEC) ? a.d[q] * a.dj[q] : a.d[q];
-      orth_operand(a, a.osrc, a.o_bs, ob, legs, a.or0, a.ooff, Oo, orr, a.orth_op != 0, H, Q, tau, red);
+      orth_operand<S>(a, a.osrc, a.o_bs, ob, legs, a.or0, a.ooff, Oo, orr, a.orth_op != 0, H, Q, tau, red);
     } else if (tid == 0) {
       for (int q = 0; q <= L; ++q) orr[q] = 1;
     }
     __syncthreads();
   }
-  if (tid == 0) G[0] = Z{1.0, 0.0};
+  if (tid == 0) G[0] = mk<S>(1.0, 0.0);
   if (tid == 0 && a.cycles) a.cycles[(size_t)b * L * 4 + 3] = clock64() - tph;
-  tph = clock64();
-  int chi = 1;
   __syncthreads();
-  for (int q = 0; q < L; ++q) {
-    const int d = a.d[q], dj = a.dj[q];
-    const int w = orr[q], w2 = orr[q + 1], r = xr[q], r2 = xr[q + 1];
-    const int m = chi * d, n = w2 * r2;
-    const Z *X = Xo + a.xoff[q], *O = Oo + a.ooff[q];
-    // ---- a2: T[(c,i),(w',r')]
-    for (int idx = tid; idx < m * n; idx += kThreads) {
-      const int rr2 = idx % r2, ww2 = (idx / r2) % w2, ii = (idx / n) % d, c = idx / (n * d);
-      Z acc{0.0, 0.0};
-      if (a.kind == TRUNCATE) {
-        for (int rr = 0; rr < r; ++rr) acc = zfma(G[(size_t)c * r + rr], X[((size_t)rr * dj + ii) * r2 + rr2], acc);
-      } else if (a.kind == HADAMARD) {
-        for (int ww = 0; ww < w; ++ww) {
-          const Z o = O[((size_t)ww * d + ii) * w2 + ww2];
-          Z s{0.0, 0.0};
-          for (int rr = 0; rr < r; ++rr) s = zfma(G[((size_t)c * w + ww) * r + rr], X[((size_t)rr * d + ii) * r2 + rr2], s);
-          acc = zfma(o, s, acc);
-        }
-      } else {
-        for (int ww = 0; ww < w; ++ww)
-          for (int jj = 0; jj < dj; ++jj) {
-            const Z o = O[(((size_t)ww * d + ii) * dj + jj) * w2 + ww2];
-            Z s{0.0, 0.0};
-            for (int rr = 0; rr < r; ++rr)
-              s = zfma(G[((size_t)c * w + ww) * r + rr], X[((size_t)rr * dj + jj) * r2 + rr2], s);
-            acc = zfma(o, s, acc);
-          }
-      }
-      T[idx] = acc;
-    }
+  int rows = 1;                                   // carry rows: chi (window 1) or chi d_pending (window 2)
+  int chi = 1;                                    // bond of the next output core
+  int s0 = 0;
+  if (win2) {                                     // the first site contracted exactly into the carry
+    contract<S>(a, 1, a.d[0], a.dj[0], orr[0], orr[1], xr[0], xr[1], G, Xo + a.xoff[0], Oo + a.ooff[0], T);
+    const int n0 = a.d[0] * orr[1] * xr[1];
+    for (int i = tid; i < n0; i += kThreads) G[i] = T[i];
+    rows = a.d[0];
+    s0 = 1;
     __syncthreads();
-    Z *Cq = a.Cq[q] + (size_t)b * a.Cq_bs[q];
+  }
+  tph = clock64();
+  for (int st = s0; st < L; ++st) {
+    // absorb site st; the split emits output core q (q = st for window 1, st - 1 for window 2)
+    const int q = win2 ? st - 1 : st;
+    const int d = a.d[st], dj = a.dj[st];
+    const int w = orr[st], w2 = orr[st + 1], r = xr[st], r2 = xr[st + 1];
+    contract<S>(a, rows, d, dj, w, w2, r, r2, G, Xo + a.xoff[st], Oo + a.ooff[st], T);
+    const int m = win2 ? rows : rows * d;         // split: rows (chi, i_q) ...
+    const int n = win2 ? d * w2 * r2 : w2 * r2;   // ... columns (window 2: i_{q+1}, w', r')
+    S *Cq = static_cast<S *>(a.Cq[q]) + (size_t)b * a.Cq_bs[q];
     if (tid == 0 && a.cycles) a.cycles[((size_t)b * L + q) * 4 + 0] = clock64() - tph;
     tph = clock64();
-    // ---- a7: last site
-    if (q == L - 1) {
-      double s = 0.0;
-      for (int i = tid; i < m * n; i += kThreads) { Cq[i] = T[i]; s += abs2(T[i]); }
-      s = block_sum(s, red);
+    // ---- a7: last site (window 1)
+    if (!win2 && q == L - 1) {
+      double sq = 0.0;
+      for (int i = tid; i < m * n; i += kThreads) { Cq[i] = T[i]; sq += abs2(T[i]); }
+      sq = block_sum(sq, red);
       if (tid == 0) {
-        a.norm2[b] = s;
+        a.norm2[b] = sq;
         a.delta2[(size_t)b * L + q] = 0.0;
         a.yr[(size_t)b * L1 + L] = 1;
         if (L == 1) a.yr[(size_t)b * L1] = 1;
         if (a.sweeps) a.sweeps[(size_t)b * L + q] = 0;
-        if (!isfinite(s)) atomicOr(a.status, 1);
+        if (!isfinite(sq)) atomicOr(a.status, 1);
       }
       return;
     }
     // ---- a3: A (m x p, column-major, ld m)
     int p;
-    Z *A = Q;                                     // reuse: Q is free between a1 and here
+    S *A = Q;                                     // reuse: Q is free between a1 and here
     if (m <= n) {
       p = m;
       for (int idx = tid; idx < m * n; idx += kThreads) H[idx] = conj(T[idx]);   // T^H column-major (n x m)
       __syncthreads();
-      house_qr(H, n, m, tau, red);
+      house_qr<S>(H, n, m, tau, red);
       for (int idx = tid; idx < m * m; idx += kThreads) {       // A = R^H: A[i, j] = conj(R[j, i]), i >= j
         const int j = idx / m, i = idx % m;
-        A[idx] = (i >= j) ? conj(H[j + (size_t)i * n]) : Z{0.0, 0.0};
+        A[idx] = (i >= j) ? conj(H[j + (size_t)i * n]) : mk<S>(0.0, 0.0);
       }
     } else {
       p = n;
@@ -438,14 +495,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup_c(Args a) {
     if (tid == 0 && a.cycles) a.cycles[((size_t)b * L + q) * 4 + 1] = clock64() - tph;
     tph = clock64();
     // ---- a4
-    const int sweeps = jacobi(A, m, p, a.eps > 1e-14 ? DBL_EPSILON * DBL_EPSILON : 0.0, red);
+    const int sweeps = jacobi<S>(A, m, p, a.eps > 1e-14 ? DBL_EPSILON * DBL_EPSILON : 0.0, red);
     for (int j = tid >> 5; j < p; j += kWarps) {
-      double s = 0.0;
-      for (int i = tid & 31; i < m; i += 32) s += abs2(A[(size_t)j * m + i]);
-      s = warp_sum(s);
+      double sq = 0.0;
+      for (int i = tid & 31; i < m; i += 32) sq += abs2(A[(size_t)j * m + i]);
+      sq = warp_sum(sq);
       if ((tid & 31) == 0) {
-        if (!isfinite(s)) { atomicOr(a.status, 1); s = 0.0; }
-        sg[j] = s;
+        if (!isfinite(sq)) { atomicOr(a.status, 1); sq = 0.0; }
+        sg[j] = sq;
       }
     }
     __syncthreads();
@@ -468,6 +525,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup_c(Args a) {
       for (int kk = 1; kk <= p; ++kk)
         if (tail[kk] <= thr) { k = kk; break; }
       if (a.max_rank > 0) k = min(k, a.max_rank);
+      if (win2) k = min(k, xr[q + 1] * orr[q + 1]);            // c-A35: exact rank at bond q+1
       if (tot == 0.0) k = 1;
       k = max(k, 1);
       s_sc[0] = (double)k;
@@ -481,8 +539,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup_c(Args a) {
       const int kk = idx / m, i = idx % m;
       const int j = perm[kk];
       const double s2 = sg[j];
-      Z *col = A + (size_t)j * m;
-      col[i] = (s2 > 0.0) ? scl(1.0 / sqrt(s2), col[i]) : Z{(i == kk) ? 1.0 : 0.0, 0.0};
+      S *col = A + (size_t)j * m;
+      col[i] = (s2 > 0.0) ? scl(1.0 / sqrt(s2), col[i]) : mk<S>((i == kk) ? 1.0 : 0.0, 0.0);
     }
     __syncthreads();
     for (int idx = tid; idx < m * k; idx += kThreads) {
@@ -499,25 +557,41 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup_c(Args a) {
       if (q == 0) a.yr[(size_t)b * L1] = 1;
       a.delta2[(size_t)b * L + q] = s_sc[1];
     }
-    // G[kk, col] = sum_i conj(U[i, kk]) T[i, col]   (k x n) -> (k, w', r')
+    // G[kk, col] = sum_i conj(U[i, kk]) T[i, col]   (k x n)
     for (int idx = tid; idx < k * n; idx += kThreads) {
       const int kk = idx / n, col = idx % n;
-      const Z *u = A + (size_t)perm[kk] * m;
-      Z acc{0.0, 0.0};
+      const S *u = A + (size_t)perm[kk] * m;
+      S acc = mk<S>(0.0, 0.0);
       for (int i = 0; i < m; ++i) acc = cfma(u[i], T[(size_t)i * n + col], acc);
       G[idx] = acc;
     }
+    __syncthreads();
+    if (win2 && st == L - 1) {                    // fully decomposed: C_{L-1} = diag(s) V^H (k, d, 1)
+      S *Cl = static_cast<S *>(a.Cq[L - 1]) + (size_t)b * a.Cq_bs[L - 1];
+      double sq = 0.0;
+      for (int i = tid; i < k * n; i += kThreads) { Cl[i] = G[i]; sq += abs2(G[i]); }
+      sq = block_sum(sq, red);
+      if (tid == 0) {
+        a.norm2[b] = sq;
+        a.delta2[(size_t)b * L + L - 1] = 0.0;
+        a.yr[(size_t)b * L1 + L] = 1;
+        if (a.sweeps) a.sweeps[(size_t)b * L + L - 1] = 0;
+        if (!isfinite(sq)) atomicOr(a.status, 1);
+      }
+      return;
+    }
     chi = k;
+    rows = win2 ? k * d : k;
     if (tid == 0 && a.cycles && q > 0) a.cycles[((size_t)b * L + q) * 4 + 3] = clock64() - tph;
     tph = clock64();
-    __syncthreads();
   }
+  (void)chi;
 }
 
 }  // namespace cplx
 
-static void complex_sizes(const Shape &S, long long &zmember, long long &imember, long long &xo, long long &oo,
-                          long long &gn, long long &tn, int &pmax) {
+static void member_sizes(const Shape &S, int window, long long &zmember, long long &imember, long long &xo,
+                         long long &oo, long long &gn, long long &tn, int &pmax) {
   xo = S.xoff[S.L];
   oo = std::max<long long>(1, S.ooff[S.L]);
   gn = S.g_elems;
@@ -531,7 +605,17 @@ static void complex_sizes(const Shape &S, long long &zmember, long long &imember
     const long long oc = (S.kind == MATVEC) ? (long long)S.orr[q] * S.d[q] * S.dj[q] * S.orr[q + 1]
                                             : (long long)S.orr[q] * S.d[q] * S.orr[q + 1];
     core_max = std::max(core_max, oc);
-    // a1 temporaries: prev-core product (rows <= core elems) lives behind Q
+  }
+  if (window == 2) {                    // super-core (chi d_q) x (d_{q+1} w' r') and its carry
+    for (int st = 1; st < S.L; ++st) {
+      const long long m = (long long)S.cap[st - 1] * S.d[st - 1];
+      const long long n = (long long)S.d[st] * S.orr[st + 1] * S.xr[st + 1];
+      tn = std::max(tn, m * n);
+      gn = std::max(gn, (long long)S.cap[st] * n);
+      pmax = (int)std::max<long long>(pmax, std::max(m, n));
+    }
+    gn = std::max(gn, (long long)S.d[0] * S.orr[1] * S.xr[1]);
+    tn = std::max(tn, (long long)S.d[0] * S.orr[1] * S.xr[1]);
   }
   tn = std::max(tn, core_max);
   // regions: Xo, Oo, G, T (tn), H (tn), Q (2 tn: Q / A and the a1 product), tau (pmax)
@@ -541,18 +625,19 @@ static void complex_sizes(const Shape &S, long long &zmember, long long &imember
   imember = (imember + 255) & ~255LL;
 }
 
-size_t complex_workspace_bytes(const Shape &S) {
+size_t member_workspace_bytes(const Shape &S, int elem_bytes, int window) {
   long long zm, im, xo, oo, gn, tn;
   int pmax;
-  complex_sizes(S, zm, im, xo, oo, gn, tn, pmax);
-  return (size_t)S.B * (size_t)zm * 16 + (size_t)S.B * (size_t)im + 256;
+  member_sizes(S, window, zm, im, xo, oo, gn, tn, pmax);
+  return (size_t)S.B * (size_t)zm * elem_bytes + (size_t)S.B * (size_t)im + 256;
 }
 
-qtt_status_t complex_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags,
-                           const LargeIO &io, void *workspace, size_t workspace_bytes, cudaStream_t s,
-                           long long *cycles) {
-  if (S.L > 64) { set_error("complex path: n_sites > 64"); return QTT_EUNSUPPORTED; }
-  const size_t need = complex_workspace_bytes(S);
+qtt_status_t member_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags,
+                          const LargeIO &io, void *workspace, size_t workspace_bytes, cudaStream_t s,
+                          long long *cycles, bool complex_dt, int window) {
+  if (S.L > 64) { set_error("per-member path: n_sites > 64"); return QTT_EUNSUPPORTED; }
+  const int elem = complex_dt ? 16 : 8;
+  const size_t need = member_workspace_bytes(S, elem, window);
   if (!workspace || workspace_bytes < need) {
     set_error("workspace %zu bytes < required %zu", workspace_bytes, need);
     return QTT_ECAPACITY;
@@ -562,13 +647,13 @@ qtt_status_t complex_zipup(const Shape &S, const qtt_trains_t *op, const qtt_tra
   a.L = S.L; a.B = S.B; a.kind = S.kind; a.op_batch = op ? op->batch : 1;
   for (int q = 0; q < S.L; ++q) {
     a.d[q] = S.d[q]; a.dj[q] = S.dj[q];
-    a.xsrc[q] = (const cplx::Z *)x->cores[q];
+    a.xsrc[q] = x->cores[q];
     a.x_bs[q] = (long long)x->ranks[q] * x->d_out[q] * x->ranks[q + 1];
     if (op) {
-      a.osrc[q] = (const cplx::Z *)op->cores[q];
+      a.osrc[q] = op->cores[q];
       a.o_bs[q] = (long long)op->ranks[q] * op->d_out[q] * (op->n_legs == 2 ? op->d_in[q] : 1) * op->ranks[q + 1];
     }
-    a.Cq[q] = (cplx::Z *)io.out->cores[q];
+    a.Cq[q] = io.out->cores[q];
     a.Cq_bs[q] = (long long)io.out->ranks[q] * S.d[q] * io.out->ranks[q + 1];
   }
   for (int q = 0; q <= S.L; ++q) {
@@ -577,11 +662,11 @@ qtt_status_t complex_zipup(const Shape &S, const qtt_trains_t *op, const qtt_tra
   }
   long long zm, im, xo, oo, gn, tn;
   int pmax;
-  complex_sizes(S, zm, im, xo, oo, gn, tn, pmax);
-  a.ws = (cplx::Z *)workspace;
+  member_sizes(S, window, zm, im, xo, oo, gn, tn, pmax);
+  a.ws = workspace;
   a.ws_member = zm;
   a.xo_n = xo; a.oo_n = oo; a.g_n = gn; a.t_n = tn;
-  a.iws = (char *)workspace + (size_t)S.B * zm * 16;
+  a.iws = (char *)workspace + (size_t)S.B * zm * elem;
   a.iws_member = im;
   a.pmax = pmax;
   a.yr = io.out_ranks; a.delta2 = io.delta2; a.norm2 = io.norm2; a.sigma = io.sigma;
@@ -589,17 +674,24 @@ qtt_status_t complex_zipup(const Shape &S, const qtt_trains_t *op, const qtt_tra
   a.eps = io.eps; a.max_rank = io.max_rank;
   a.orth_op = (flags & QTT_NO_OPERATOR_ORTH) ? 0 : 1;
   a.cycles = cycles;
+  a.window = window;
   QTT_CUDA_TRY(cudaMemsetAsync(io.status, 0, sizeof(int32_t), s));
-  const size_t smem = (size_t)(4 * tn + gn + std::max(pmax, 64)) * 16;
+  const size_t smem = (size_t)(4 * tn + gn + std::max(pmax, 64)) * elem;
   a.smem = smem <= 200 * 1024 ? 1 : 0;
-  if (a.smem) {
-    static bool attr = false;
-    if (!attr) {
-      QTT_CUDA_TRY(cudaFuncSetAttribute(cplx::k_zipup_c, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
+  static bool attr_c = false, attr_r = false;
+  if (complex_dt) {
+    if (a.smem && !attr_c) {
+      QTT_CUDA_TRY(cudaFuncSetAttribute(cplx::k_zipup<cplx::Z>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr_c = true;
     }
+    cplx::k_zipup<cplx::Z><<<S.B, kThreads, a.smem ? smem : 0, s>>>(a);
+  } else {
+    if (a.smem && !attr_r) {
+      QTT_CUDA_TRY(cudaFuncSetAttribute(cplx::k_zipup<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr_r = true;
+    }
+    cplx::k_zipup<double><<<S.B, kThreads, a.smem ? smem : 0, s>>>(a);
   }
-  cplx::k_zipup_c<<<S.B, kThreads, a.smem ? smem : 0, s>>>(a);
   QTT_CUDA_TRY(cudaGetLastError());
   return QTT_OK;
 }

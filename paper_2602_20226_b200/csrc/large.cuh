@@ -31,11 +31,12 @@ struct LargeIO {
 };
 
 size_t large_workspace_bytes(const Shape &S);
-// complex128 path (complex.cu): one CTA per member, every step
-size_t complex_workspace_bytes(const Shape &S);
-qtt_status_t complex_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags,
-                           const struct LargeIO &io, void *workspace, size_t workspace_bytes, cudaStream_t s,
-                           long long *cycles = nullptr);
+// per-member path (complex.cu): one CTA per member, every step; complex128 trains (f2) and
+// the window-2 zip-up (f4, real or complex)
+size_t member_workspace_bytes(const Shape &S, int elem_bytes, int window);
+qtt_status_t member_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags,
+                          const struct LargeIO &io, void *workspace, size_t workspace_bytes, cudaStream_t s,
+                          long long *cycles, bool complex_dt, int window);
 qtt_status_t large_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags,
                          const LargeIO &io, void *workspace, size_t workspace_bytes, cudaStream_t s);
 

@@ -994,7 +994,7 @@ extern "C" {
 
 const char *qtt_last_error(void) { return qtt::g_err; }
 const char *qtt_version(void) {
-  return "libqtt 0.3 (sm_100a; fp64 zip-up: small- and large-member paths; fp32 variant with 3xTF32 tcgen05 contractions; complex128 zip-up)";
+  return "libqtt 0.3 (sm_100a; fp64 zip-up: small- and large-member paths; fp32 variant with 3xTF32 tcgen05 contractions; complex128 and window-2 zip-ups)";
 }
 
 qtt_status_t qtt_zipup_capacity(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
@@ -1009,15 +1009,19 @@ qtt_status_t qtt_zipup_capacity(const char *subscripts, const qtt_trains_t *op, 
 
 size_t qtt_zipup_workspace_bytes(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
                                  const qtt_trains_t *out) {
-  {
-    const int dt = train_dtypes(op, x, out);
-    if (dt < 0) { set_error("mixed dtypes: x, op and out must share one of QTT_F64, QTT_F32, QTT_C128"); return 0; }
-    if (dt == 1) {                 // fp32 variant: fp64 staging of all three trains + the fp64 workspace
-      F32Stage F;
-      f32_stage(op, x, out, nullptr, F);
-      const size_t inner = qtt_zipup_workspace_bytes(subscripts, op ? &F.op64 : nullptr, &F.x64, out ? &F.out64 : nullptr);
-      return inner ? F.bytes + inner : 0;
-    }
+  return qtt_zipup_workspace_bytes_flags(subscripts, op, x, out, 0);
+}
+
+size_t qtt_zipup_workspace_bytes_flags(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                                       const qtt_trains_t *out, uint32_t flags) {
+  const int dt = train_dtypes(op, x, out);
+  if (dt < 0) { set_error("mixed dtypes: x, op and out must share one of QTT_F64, QTT_F32, QTT_C128"); return 0; }
+  if (dt == 1) {                   // fp32 variant: fp64 staging of all three trains + the fp64 workspace
+    F32Stage F;
+    f32_stage(op, x, out, nullptr, F);
+    const size_t inner =
+        qtt_zipup_workspace_bytes_flags(subscripts, op ? &F.op64 : nullptr, &F.x64, out ? &F.out64 : nullptr, flags);
+    return inner ? F.bytes + inner : 0;
   }
   // the output capacities the caller will pass bound the zip-up ranks (max_rank)
   int mr = 0;
@@ -1025,7 +1029,8 @@ size_t qtt_zipup_workspace_bytes(const char *subscripts, const qtt_trains_t *op,
     for (int q = 1; q < x->n_sites; ++q) mr = std::max(mr, (int)out->ranks[q]);
   Shape S;
   if (analyse(subscripts, op, x, mr, S) != QTT_OK) return 0;
-  if (train_dtypes(op, x, out) == 2) return complex_workspace_bytes(S);
+  const int window = (flags & QTT_WINDOW2) ? 2 : 1;
+  if (dt == 2 || window == 2) return member_workspace_bytes(S, dt == 2 ? 16 : 8, window);
   if (check_small_path(S) == QTT_OK) return layout(S).total;
   return large_workspace_bytes(S);
 }
@@ -1083,11 +1088,13 @@ qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt
   }
   if (sigma && sigma_stride < 1) { set_error("sigma_stride < 1"); return QTT_EINVAL; }
   cudaStream_t s = (cudaStream_t)stream;
-  if (train_dtypes(op, x, out) == 2) {     // complex128 (Fourier chain)
+  const bool cdt = train_dtypes(op, x, out) == 2;
+  if (cdt || (flags & QTT_WINDOW2)) {      // complex128 (Fourier chain, f2) / window 2 (f4)
     g_err[0] = 0;
     if (events) for (int i = 0; i < 3; ++i) QTT_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[i], s));
     LargeIO io{out, out_ranks, delta2, norm2, sigma, sigma_stride, sweeps, status, eps, max_rank};
-    qtt_status_t cst = complex_zipup(S, op, x, flags, io, workspace, workspace_bytes, s, cycles);
+    qtt_status_t cst = member_zipup(S, op, x, flags, io, workspace, workspace_bytes, s, cycles, cdt,
+                                    (flags & QTT_WINDOW2) ? 2 : 1);
     if (cst != QTT_OK) return cst;
     if (events) QTT_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[3], s));
     return QTT_OK;

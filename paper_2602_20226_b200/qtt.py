@@ -22,6 +22,7 @@ QTT_OK = 0
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ESHAPE", 3: "ECONFORM", 4: "ENUMERIC", 5: "ECAPACITY",
                 6: "EGUARD", 7: "ECUDA", 8: "EUNSUPPORTED"}
 NO_OPERATOR_ORTH = 1
+WINDOW2 = 2                  # QTT_WINDOW2: super-core of two sites
 
 
 class QttError(RuntimeError):
@@ -46,7 +47,8 @@ QTT_F64, QTT_F32, QTT_C128 = 0, 1, 2
 
 _lib = None
 
-SYMBOLS = ["qtt_zipup_capacity", "qtt_zipup_workspace_bytes", "qtt_zipup", "qtt_zipup_summary",
+SYMBOLS = ["qtt_zipup_capacity", "qtt_zipup_workspace_bytes", "qtt_zipup_workspace_bytes_flags", "qtt_zipup",
+           "qtt_zipup_summary",
            "qtt_round_capacity", "qtt_round_workspace_bytes", "qtt_round",
            "qtt_einsum_exact", "qtt_inner_workspace_bytes", "qtt_inner", "qtt_to_dense_workspace_bytes",
            "qtt_to_dense", "qtt_last_error", "qtt_version"]
@@ -66,6 +68,8 @@ def load_library(path: str = LIB_PATH):
     L.qtt_zipup_capacity.restype = i32
     L.qtt_zipup_workspace_bytes.argtypes = [ctypes.c_char_p, P, P, P]
     L.qtt_zipup_workspace_bytes.restype = sz
+    L.qtt_zipup_workspace_bytes_flags.argtypes = [ctypes.c_char_p, P, P, P, ctypes.c_uint32]
+    L.qtt_zipup_workspace_bytes_flags.restype = sz
     L.qtt_zipup.argtypes = [ctypes.c_char_p, P, P, f64, i32, ctypes.c_uint32, P, vp, vp, vp, vp,
                             ctypes.POINTER(_Diag), vp, sz, vp]
     L.qtt_zipup.restype = i32
@@ -250,8 +254,9 @@ class ZipupPlan:
         if op is not None:
             os_, ko = op.c_struct()
         outs, kout = self.out.c_struct()
-        nbytes = self.lib.qtt_zipup_workspace_bytes(subscripts.encode(), ctypes.byref(os_) if os_ is not None else None,
-                                                    ctypes.byref(xs), ctypes.byref(outs))
+        nbytes = self.lib.qtt_zipup_workspace_bytes_flags(subscripts.encode(),
+                                                          ctypes.byref(os_) if os_ is not None else None,
+                                                          ctypes.byref(xs), ctypes.byref(outs), self.flags)
         if nbytes == 0:
             raise QttError(2, self.lib.qtt_last_error().decode())
         self.workspace = torch.empty((nbytes + 255) // 256 * 256, dtype=torch.uint8, device=device)

@@ -14,7 +14,7 @@ import math
 import numpy as np
 
 from oracle import tt
-from oracle.zipup import zipup as oracle_zipup
+from oracle.zipup import zipup as oracle_zipup_w1, zipup_window
 
 U64 = 1.1e-16
 
@@ -39,8 +39,14 @@ def fragile(sig: np.ndarray, k: int, eps: float, max_rank: int, u: float = U64) 
 
 
 def compare(kind, op_cores, x_cores, eps, max_rank, gpu_cores, gpu_ranks, gpu_sigma, gpu_delta2, gpu_norm2,
-            rel_tol=1e-10, sig_tol=1e-12, dense=True, orth_operator=True, u=U64):
-    """Returns a dict of measured errors; raises AssertionError on a protocol violation."""
+            rel_tol=1e-10, sig_tol=1e-12, dense=True, orth_operator=True, u=U64, window=1):
+    """Returns a dict of measured errors; raises AssertionError on a protocol violation.
+    window: the zip-up super-core size the GPU ran with (1, or 2 for QTT_WINDOW2)."""
+    def oracle_zipup(*args, **kw):
+        if window == 1:
+            return oracle_zipup_w1(*args, **kw)
+        return zipup_window(*args, window=window, **kw)
+
     ref = oracle_zipup(kind, op_cores, x_cores, eps, max_rank, orth_operator=orth_operator)
     L = len(x_cores)
     if list(gpu_ranks) != ref["ranks"]:
