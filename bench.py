@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--cpu-members", type=int, default=8, help="oracle sample size (members) for cpu_baseline")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
                     help="f32: the fp32 variant (binary32 cores; large-path contractions as 3xTF32 on tcgen05)")
+    ap.add_argument("--window", type=int, default=1, choices=[1, 2],
+                    help="2: QTT_WINDOW2 super-cores of two sites (SURVEY.md §8(f) f4; per-member kernel)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -78,9 +80,40 @@ def build_workload(args, rank):
     return subs, p.kind, [p], xs, ops, cfg
 
 
-def site_flops(kind, ranks_y, xr, orr, d, dj, sweeps):
+def site_flops_w2(kind, ranks_y, xr, orr, d, dj, sweeps):
+    """site_flops for the window-2 zip-up: split q is (chi_q d_q) x (d_{q+1} w r) after
+    absorbing site q+1 into a carry of chi_q d_q rows (site 0 absorbed first, chi = 1)."""
+    L = len(d)
+    d, dj = [int(v) for v in d], [int(v) for v in dj]
+
+    def contract(rows, s):
+        w, w2 = (int(orr[s]), int(orr[s + 1])) if kind != "truncate" else (1, 1)
+        r, r2 = int(xr[s]), int(xr[s + 1])
+        if kind == "matvec":
+            return 2 * rows * w * r * dj[s] * r2 + 2 * rows * d[s] * w2 * r2 * w * dj[s]
+        if kind == "hadamard":
+            return 2 * rows * w * r * d[s] * r2 + 2 * rows * d[s] * r2 * w * w2
+        return 2 * rows * r * d[s] * r2
+
+    out = [(float(contract(1, 0)), 0.0, 0.0, 0.0)]
+    for q in range(L - 1):
+        s = q + 1
+        chi = int(ranks_y[q])
+        rows = chi * d[q]
+        w2 = int(orr[s + 1]) if kind != "truncate" else 1
+        m, n = rows, d[s] * w2 * int(xr[s + 1])
+        k = int(ranks_y[q + 1])
+        p = min(m, n)
+        fq = (2.0 * n * m * m - (2.0 / 3.0) * m ** 3) if m <= n else 0.0
+        out.append((float(contract(rows, s)), fq, 2.0 * k * m * n, float(sweeps[q]) * p * (p - 1) / 2 * 12 * m))
+    return out
+
+
+def site_flops(kind, ranks_y, xr, orr, d, dj, sweeps, window=1):
     """Per-site algorithmic flops for one member:
     contract / qr / carry / jacobi (executed sweeps x p(p-1)/2 pairs x 12 m)."""
+    if window == 2:
+        return site_flops_w2(kind, ranks_y, xr, orr, d, dj, sweeps)
     L = len(d)
     d, dj = [int(v) for v in d], [int(v) for v in dj]
     out = []
@@ -196,9 +229,10 @@ def dram_traffic(workload, members):
 
 # ----------------------------------------------------------------------------- CPU oracle leg
 
-def oracle_sample(kind, probs, n_members):
+def oracle_sample(kind, probs, n_members, window=1):
     """Time the oracle, as it stands, on the host cores over a bounded sample."""
-    from oracle.zipup import zipup as ozip
+    from oracle.zipup import zipup as ozip1, zipup_window
+    ozip = ozip1 if window == 1 else (lambda *a_: zipup_window(*a_, window=window))
     try:
         from threadpoolctl import threadpool_info
         cores = max([i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"] or [1])
@@ -243,12 +277,15 @@ def main():
     stream = torch.cuda.current_stream()
 
     subs, kind, probs, xs, ops, cfg = build_workload(args, rank)
+    if args.window == 2:
+        cfg = dict(cfg, window=2)
     mpo = kind == "matvec"
     npdt = np.float32 if args.dtype == "f32" else np.float64
     xd = qtt.to_device(xs, dtype=npdt)
     od = None if ops is None else qtt.to_device(ops, mpo=mpo, dtype=npdt)
     p0 = probs[0]
-    plan = qtt.ZipupPlan(subs, od, xd, p0.eps, p0.max_rank, sweeps=True, cycles=True)
+    wflags = qtt.WINDOW2 if args.window == 2 else 0
+    plan = qtt.ZipupPlan(subs, od, xd, p0.eps, p0.max_rank, flags=wflags, sweeps=True, cycles=True)
     L = xd.n_sites
     B = xd.batch
     summary = torch.zeros(4, dtype=torch.float64, device="cuda")
@@ -303,7 +340,8 @@ def main():
     dj = xd.d_out
     tot = np.zeros(4)
     for b in range(B):
-        f = site_flops(kind, list(ranks[b]), xd.ranks, od.ranks if od is not None else None, d, dj, sweeps[b])
+        f = site_flops(kind, list(ranks[b]), xd.ranks, od.ranks if od is not None else None, d, dj, sweeps[b],
+                       args.window)
         tot += np.sum(np.array(f), axis=0)
     flops_alg = tot[0] + tot[1] + tot[2]
     flops_all = flops_alg + tot[3]
@@ -311,6 +349,8 @@ def main():
     fp64_peak = max(peaks["dfma_tflops"], peaks["dmma_tflops"])
     achieved = flops_all / site_s / 1e12
     launches_per_step = 3 + (1 if kind != "truncate" else 0)   # a1 (x[, op]), k_sweep, summary
+    if args.window == 2:
+        launches_per_step = 2                                    # k_zipup<double>, summary
 
     units = world * B * L
     value = units / (ms_max * 1e-3)
@@ -323,7 +363,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         depth = 2
-        pipe = qtt.HostPipeline(subs, od, xd, p0.eps, p0.max_rank, depth=depth)
+        pipe = qtt.HostPipeline(subs, od, xd, p0.eps, p0.max_rank, depth=depth, flags=wflags)
         hx = [c.detach().cpu().pin_memory() for c in xd.cores]
         ho = [c.detach().cpu().pin_memory() for c in od.cores] if od is not None else None
         hsets = []
@@ -371,7 +411,7 @@ def main():
     cpu = None
     parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu, refs = oracle_sample(kind, probs, args.cpu_members)
+        cpu, refs = oracle_sample(kind, probs, args.cpu_members, args.window)
         from oracle import tt
         worst = 0.0
         for b, ref in enumerate(refs):
@@ -395,7 +435,9 @@ def main():
                 " (single zip-up; its per-site scratch exceeds L2 for cfg3/cfg4)")),
             "alg_tflops": round(world * flops_alg / (ms_max * 1e-3) / 1e12, 3),
             "alg_tflops_note": "contraction+QR+carry flops (SURVEY.md §8(d)); Jacobi excluded",
-            "roofline": {"kernel": "k_sweep (persistent a2-a7 over all sites and members; Jacobi-dominated)", "bound": "fp64",
+            "roofline": {"kernel": ("k_sweep (persistent a2-a7 over all sites and members; Jacobi-dominated)"
+                                    if args.window == 1 else "k_zipup<double> (window 2: one CTA per member, every step)"),
+                         "bound": "fp64",
                          "achieved": round(achieved, 3), "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": round(achieved / fp64_peak, 4), "traffic": traffic,
                          "peak_source": "measured in this run by csrc/probe/peak.cu (MEASURED_PEAKS.json has no FP64)",
