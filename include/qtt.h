@@ -175,6 +175,28 @@ qtt_status_t qtt_round(const qtt_trains_t *x, const int32_t *x_ranks, double eps
                        const qtt_trains_t *out, int32_t *out_ranks, double *delta2, double *norm2,
                        int32_t *status, void *workspace, size_t workspace_bytes, void *stream);
 
+/* ---------------------------------------------------------------------------------------
+ * qtt_variational -- variational refinement of a zip-up result (Eq.
+ * variational 294): minimise |C - op(x)| core by core, single-site,
+ * with C(i_q) = d<C|op(x)>/dC*(i_q) at the normalisation centre (reading c-A36).  The seed C
+ * is right-orthonormalised (centre at site 0), then `sweeps` times: update sites 0..L-1
+ * moving the centre right by QR, then L-1..0 moving it left by LQ.  Bond ranks are the
+ * seed's (a bond shrinks only where a core cannot be orthonormal).  QTT_F64 only.
+ *   subscripts, op, x : as for qtt_zipup (the operands are not modified, not normalised).
+ *   c          : in/out trains (capacity slots as qtt_zipup writes them); on return member b
+ *                holds C with the centre at site 0, packed at c_ranks.
+ *   c_ranks    : device int32 [B*(L+1)] in: the seed's ranks (qtt_zipup's out_ranks); out: final.
+ *   center_norm2 : device f64 [B * sweeps * 2L]: |C_q|^2 after every update, in update order;
+ *                |op(x) - C|^2 = |op(x)|^2 - |C_q|^2, so the sequence never decreases.
+ *   status     : device int32 [1]; bit 1 = non-finite value.
+ *   workspace  : >= qtt_variational_workspace_bytes(subscripts, op, x, c) bytes.
+ */
+size_t qtt_variational_workspace_bytes(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                                       const qtt_trains_t *c);
+qtt_status_t qtt_variational(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                             const qtt_trains_t *c, int32_t *c_ranks, int32_t sweeps, double *center_norm2,
+                             int32_t *status, void *workspace, size_t workspace_bytes, void *stream);
+
 /* qtt_zipup_summary -- the per-batch scalars that are all-reduced across GPUs
  * (SURVEY.md §8(a) a8): summary4 (device f64 [4]) = [sum_b sum_q delta2, sum_b norm2,
  * sum_b sum_q out_ranks[b][q+1] (q < L-1), B].  Deterministic fixed-order sums. */

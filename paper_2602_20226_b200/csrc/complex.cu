@@ -697,3 +697,325 @@ qtt_status_t member_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trai
 }
 
 }  // namespace qtt
+
+// ======================================================================= f3: variational
+// Single-site variational refinement seeded by a zip-up result (Eq.
+// variational 294; reading c-A36).  One CTA per member:
+//   C right-orthonormalised (centre at 0); right environments Re[q] (c, w, r);
+//   sweep: q = 0..L-1: C_q = sum Le[q] W_q x_q Re[q+1]; QR moves the centre right and Le[q+1]
+//   is built from the new left-orthonormal C_q; then q = L-1..0 with LQ / Re[q].
+//   |C_q|^2 after every update goes to center_norm2 (|O - C|^2 = |O|^2 - |C_q|^2).
+namespace qtt {
+namespace cplx {
+
+struct VarArgs {
+  int L, B, kind, op_batch, sweeps;
+  int d[64], dj[64], xr[65], orr[65], cap[65];
+  const double *x[64];
+  const double *op[64];
+  long long x_bs[64], o_bs[64];
+  double *c[64];
+  long long c_bs[64];
+  int *c_ranks;                       // device [B][L+1] (in: the seed's ranks; out: after the sweeps)
+  double *norms;                      // device [B][sweeps * 2L]
+  int *status;
+  double *ws;
+  long long ws_member;
+  long long coff[65], eoff[65];       // per-member offsets: C slots (capacity), environments
+  long long e_n, s_n;                 // environment region (each of Le, Re) and scratch sizes
+};
+
+// W[w, i, j, w'] of the operator (Hadamard: A[w, i, w'] on i == j; truncate: identity)
+__device__ __forceinline__ double opval(const VarArgs &a, const double *O, int q, int w, int i, int j, int w2,
+                                        int wr2) {
+  if (a.kind == MATVEC) return O[(((size_t)w * a.d[q] + i) * a.dj[q] + j) * wr2 + w2];
+  if (a.kind == HADAMARD) return (i == j) ? O[((size_t)w * a.d[q] + i) * wr2 + w2] : 0.0;
+  return (i == j) ? 1.0 : 0.0;
+}
+
+// X2[c, i, w', r'] = sum_{w, r, j} Le[c, w, r] W[w, i, j, w'] x[r, j, r']   (c < rc)
+__device__ void env_apply_left(const VarArgs &a, int q, int rc, const double *Le, const double *X,
+                               const double *O, double *X1, double *X2) {
+  const int tid = threadIdx.x;
+  const int d = a.d[q], dj = a.dj[q];
+  const int w = (a.kind == TRUNCATE) ? 1 : a.orr[q], w2 = (a.kind == TRUNCATE) ? 1 : a.orr[q + 1];
+  const int r = a.xr[q], r2 = a.xr[q + 1];
+  // X1[c, w, j, r'] = sum_r Le[c, w, r] x[r, j, r']
+  for (int idx = tid; idx < rc * w * dj * r2; idx += kThreads) {
+    const int rr2 = idx % r2, jj = (idx / r2) % dj, ww = (idx / (r2 * dj)) % w, c = idx / (r2 * dj * w);
+    double s = 0.0;
+    for (int rr = 0; rr < r; ++rr) s = fma(Le[((size_t)c * w + ww) * r + rr], X[((size_t)rr * dj + jj) * r2 + rr2], s);
+    X1[idx] = s;
+  }
+  __syncthreads();
+  // X2[c, i, w', r'] = sum_{w, j} X1[c, w, j, r'] W[w, i, j, w']
+  for (int idx = tid; idx < rc * d * w2 * r2; idx += kThreads) {
+    const int rr2 = idx % r2, ww2 = (idx / r2) % w2, ii = (idx / (r2 * w2)) % d, c = idx / (r2 * w2 * d);
+    double s = 0.0;
+    for (int ww = 0; ww < w; ++ww)
+      for (int jj = 0; jj < dj; ++jj) {
+        if (a.kind != MATVEC && jj != ii) continue;
+        s = fma(X1[(((size_t)c * w + ww) * dj + jj) * r2 + rr2], opval(a, O, q, ww, ii, jj, ww2, w2), s);
+      }
+    X2[idx] = s;
+  }
+  __syncthreads();
+}
+
+// Re_new[c, w, r] = sum C[c, i, c'] W[w, i, j, w'] x[r, j, r'] Re[c', w', r']
+__device__ void env_right(const VarArgs &a, int q, int rc, int rc2, const double *C, const double *Re,
+                          const double *X, const double *O, double *Y1, double *Y2, double *Rn) {
+  const int tid = threadIdx.x;
+  const int d = a.d[q], dj = a.dj[q];
+  const int w = (a.kind == TRUNCATE) ? 1 : a.orr[q], w2 = (a.kind == TRUNCATE) ? 1 : a.orr[q + 1];
+  const int r = a.xr[q], r2 = a.xr[q + 1];
+  // Y1[c, i, w', r'] = sum_{c'} C[c, i, c'] Re[c', w', r']
+  for (int idx = tid; idx < rc * d * w2 * r2; idx += kThreads) {
+    const int rr2 = idx % r2, ww2 = (idx / r2) % w2, ii = (idx / (r2 * w2)) % d, c = idx / (r2 * w2 * d);
+    double s = 0.0;
+    for (int a2 = 0; a2 < rc2; ++a2) s = fma(C[((size_t)c * d + ii) * rc2 + a2], Re[((size_t)a2 * w2 + ww2) * r2 + rr2], s);
+    Y1[idx] = s;
+  }
+  __syncthreads();
+  // Y2[c, w, j, r'] = sum_{i, w'} Y1[c, i, w', r'] W[w, i, j, w']
+  for (int idx = tid; idx < rc * w * dj * r2; idx += kThreads) {
+    const int rr2 = idx % r2, jj = (idx / r2) % dj, ww = (idx / (r2 * dj)) % w, c = idx / (r2 * dj * w);
+    double s = 0.0;
+    for (int ii = 0; ii < d; ++ii) {
+      if (a.kind != MATVEC && ii != jj) continue;
+      for (int ww2 = 0; ww2 < w2; ++ww2)
+        s = fma(Y1[(((size_t)c * d + ii) * w2 + ww2) * r2 + rr2], opval(a, O, q, ww, ii, jj, ww2, w2), s);
+    }
+    Y2[idx] = s;
+  }
+  __syncthreads();
+  // Rn[c, w, r] = sum_{j, r'} Y2[c, w, j, r'] x[r, j, r']
+  for (int idx = tid; idx < rc * w * r; idx += kThreads) {
+    const int rr = idx % r, ww = (idx / r) % w, c = idx / (r * w);
+    double s = 0.0;
+    for (int jj = 0; jj < dj; ++jj)
+      for (int rr2 = 0; rr2 < r2; ++rr2)
+        s = fma(Y2[(((size_t)c * w + ww) * dj + jj) * r2 + rr2], X[((size_t)rr * dj + jj) * r2 + rr2], s);
+    Rn[idx] = s;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_variational(VarArgs a) {
+  const int b = blockIdx.x, tid = threadIdx.x, L = a.L;
+  __shared__ double red[kWarps];
+  __shared__ int cr[65];
+  double *w0 = a.ws + (size_t)b * a.ws_member;
+  double *Cw = w0, *Le = Cw + a.coff[L], *Re = Le + a.e_n, *S1 = Re + a.e_n, *S2 = S1 + a.s_n, *S3 = S2 + a.s_n,
+         *tau = S3 + a.s_n;
+  const int ob = (a.op_batch == 1) ? 0 : b;
+  for (int q = tid; q <= L; q += kThreads) cr[q] = a.c_ranks[(size_t)b * (L + 1) + q];
+  __syncthreads();
+  // the seed into the workspace, packed at its ranks
+  for (int q = 0; q < L; ++q) {
+    const long long n = (long long)cr[q] * a.d[q] * cr[q + 1];
+    const double *src = a.c[q] + (size_t)b * a.c_bs[q];
+    for (long long i = tid; i < n; i += kThreads) Cw[a.coff[q] + i] = src[i];
+  }
+  __syncthreads();
+  auto Xq = [&](int q) { return a.x[q] + (size_t)b * a.x_bs[q]; };
+  auto Oq = [&](int q) { return a.op[q] ? a.op[q] + (size_t)ob * a.o_bs[q] : (const double *)nullptr; };
+  // centre from q to q-1: C_q^T = Q R (thin, k = min(r, c) -- the bond shrinks when the core
+  // cannot be row-orthonormal, as numpy's reduced QR in the oracle), C_q <- Q^T, C_{q-1} <- C_{q-1} R^T
+  auto move_left = [&](int q) {
+    const int r = cr[q], c = a.d[q] * cr[q + 1], k = min(r, c);
+    double *core = Cw + a.coff[q];
+    for (int idx = tid; idx < r * c; idx += kThreads) S1[idx] = core[idx];   // C_q^T, column-major (c x r)
+    __syncthreads();
+    house_qr<double>(S1, c, r, tau, red);
+    form_q<double>(S1, c, k, tau, S2);
+    for (int idx = tid; idx < k * c; idx += kThreads) core[idx] = S2[idx];
+    double *prev = Cw + a.coff[q - 1];
+    const int pr = cr[q - 1] * a.d[q - 1];
+    for (int idx = tid; idx < pr * k; idx += kThreads) {
+      const int row = idx / k, kk = idx % k;
+      double sacc = 0.0;
+      for (int j2 = kk; j2 < r; ++j2) sacc = fma(prev[(size_t)row * r + j2], S1[kk + (size_t)j2 * c], sacc);
+      S3[idx] = sacc;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < pr * k; idx += kThreads) prev[idx] = S3[idx];
+    if (tid == 0) cr[q] = k;
+    __syncthreads();
+  };
+  // centre from q to q+1: C_q = Q R (rows = cr[q] d_q), C_{q+1} <- R C_{q+1}
+  auto move_right = [&](int q) {
+    const int rows = cr[q] * a.d[q], kc = cr[q + 1], k = min(rows, kc);
+    double *C = Cw + a.coff[q];
+    for (int idx = tid; idx < rows * kc; idx += kThreads) S1[(idx % kc) * rows + idx / kc] = C[idx];
+    __syncthreads();
+    house_qr<double>(S1, rows, kc, tau, red);
+    form_q<double>(S1, rows, k, tau, S2);
+    for (int idx = tid; idx < rows * k; idx += kThreads) C[idx] = S2[(idx % k) * rows + idx / k];
+    double *Cn = Cw + a.coff[q + 1];
+    const int cols = a.d[q + 1] * cr[q + 2];
+    for (int idx = tid; idx < k * cols; idx += kThreads) {
+      const int i2 = idx / cols, j2 = idx % cols;
+      double sacc = 0.0;
+      for (int l = i2; l < kc; ++l) sacc = fma(S1[i2 + (size_t)l * rows], Cn[(size_t)l * cols + j2], sacc);
+      S3[idx] = sacc;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < k * cols; idx += kThreads) Cn[idx] = S3[idx];
+    if (tid == 0) cr[q + 1] = k;
+    __syncthreads();
+  };
+  for (int q = L - 1; q >= 1; --q) move_left(q);  // right-orthonormalise the seed: centre at site 0
+  // environments
+  if (tid == 0) { Le[a.eoff[0]] = 1.0; Re[a.eoff[L]] = 1.0; }
+  __syncthreads();
+  for (int q = L - 1; q >= 1; --q)
+    env_right(a, q, cr[q], cr[q + 1], Cw + a.coff[q], Re + a.eoff[q + 1], Xq(q), Oq(q), S1, S2, Re + a.eoff[q]);
+  int cnt = 0;
+  auto update = [&](int q) {                      // C_q = sum Le[q] W_q x_q Re[q+1]   (Eq. variational)
+    env_apply_left(a, q, cr[q], Le + a.eoff[q], Xq(q), Oq(q), S1, S2);
+    const int w2 = (a.kind == TRUNCATE) ? 1 : a.orr[q + 1], r2 = a.xr[q + 1], rc2 = cr[q + 1], d = a.d[q];
+    double *C = Cw + a.coff[q];
+    double sq = 0.0;
+    for (int idx = tid; idx < cr[q] * d * rc2; idx += kThreads) {
+      const int a2 = idx % rc2, ci = idx / rc2;
+      double sacc = 0.0;
+      for (int ww2 = 0; ww2 < w2; ++ww2)
+        for (int rr2 = 0; rr2 < r2; ++rr2)
+          sacc = fma(S2[((size_t)ci * w2 + ww2) * r2 + rr2], Re[a.eoff[q + 1] + ((size_t)a2 * w2 + ww2) * r2 + rr2], sacc);
+      C[idx] = sacc;
+      sq = fma(sacc, sacc, sq);
+    }
+    sq = block_sum(sq, red);
+    if (tid == 0) {
+      a.norms[(size_t)b * a.sweeps * 2 * L + cnt] = sq;
+      if (!isfinite(sq)) atomicOr(a.status, 1);
+    }
+    ++cnt;
+    __syncthreads();
+  };
+  for (int sw = 0; sw < a.sweeps; ++sw) {
+    for (int q = 0; q < L; ++q) {                 // to the right
+      update(q);
+      if (q == L - 1) break;
+      move_right(q);
+      // Le[q+1][c', w', r'] = sum_{c, i} C[c, i, c'] X2[c, i, w', r']   (X2 from Le[q])
+      env_apply_left(a, q, cr[q], Le + a.eoff[q], Xq(q), Oq(q), S1, S2);
+      const int w2 = (a.kind == TRUNCATE) ? 1 : a.orr[q + 1], r2 = a.xr[q + 1], k = cr[q + 1];
+      const int rows = cr[q] * a.d[q];
+      const double *C = Cw + a.coff[q];
+      for (int idx = tid; idx < k * w2 * r2; idx += kThreads) {
+        const int wr = idx % (w2 * r2), a2 = idx / (w2 * r2);
+        double sacc = 0.0;
+        for (int ci = 0; ci < rows; ++ci) sacc = fma(C[(size_t)ci * k + a2], S2[(size_t)ci * w2 * r2 + wr], sacc);
+        Le[a.eoff[q + 1] + idx] = sacc;
+      }
+      __syncthreads();
+    }
+    for (int q = L - 1; q >= 0; --q) {            // and back
+      update(q);
+      if (q == 0) break;
+      move_left(q);
+      env_right(a, q, cr[q], cr[q + 1], Cw + a.coff[q], Re + a.eoff[q + 1], Xq(q), Oq(q), S1, S2, Re + a.eoff[q]);
+    }
+  }
+  // write back (centre at site 0); bonds may have shrunk where a core could not be orthonormal
+  for (int q = tid; q <= L; q += kThreads) a.c_ranks[(size_t)b * (L + 1) + q] = cr[q];
+  for (int q = 0; q < L; ++q) {
+    const long long n = (long long)cr[q] * a.d[q] * cr[q + 1];
+    double *dst = a.c[q] + (size_t)b * a.c_bs[q];
+    for (long long i = tid; i < n; i += kThreads) dst[i] = Cw[a.coff[q] + i];
+  }
+}
+
+}  // namespace cplx
+
+static void var_sizes(const Shape &S, const qtt_trains_t *c, long long &member, long long *coff, long long *eoff,
+                      long long &e_n, long long &s_n, int &pmax) {
+  const int L = S.L;
+  coff[0] = 0;
+  eoff[0] = 0;
+  s_n = 1;
+  pmax = 64;
+  for (int q = 0; q < L; ++q) {
+    const long long cq = c->ranks[q], cq1 = c->ranks[q + 1];
+    const long long w = (S.kind == TRUNCATE) ? 1 : S.orr[q], w2 = (S.kind == TRUNCATE) ? 1 : S.orr[q + 1];
+    coff[q + 1] = coff[q] + cq * S.d[q] * cq1;
+    eoff[q + 1] = eoff[q] + cq * w * S.xr[q];
+    s_n = std::max(s_n, cq * w * S.dj[q] * S.xr[q + 1]);
+    s_n = std::max(s_n, cq * S.d[q] * w2 * S.xr[q + 1]);
+    s_n = std::max(s_n, cq * S.d[q] * cq1 * 2);
+    s_n = std::max(s_n, cq * w * S.xr[q]);
+    s_n = std::max(s_n, cq1 * S.d[q] * (q + 2 <= L ? (long long)c->ranks[std::min(q + 2, L)] : 1));
+    pmax = (int)std::max<long long>(pmax, std::max(cq * S.d[q], cq1 * S.d[q]));
+  }
+  e_n = eoff[L] + 1;
+  member = coff[L] + 2 * e_n + 3 * s_n + pmax;
+  member = (member + 31) & ~31LL;
+}
+
+}  // namespace qtt
+
+using namespace qtt;
+
+extern "C" {
+
+size_t qtt_variational_workspace_bytes(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                                       const qtt_trains_t *c) {
+  Shape S;
+  if (!c || qtt_zipup_analyse(subscripts, op, x, 0, S) != QTT_OK) return 0;
+  long long member, coff[65], eoff[65], e_n, s_n;
+  int pmax;
+  var_sizes(S, c, member, coff, eoff, e_n, s_n, pmax);
+  return (size_t)S.B * member * 8 + 256;
+}
+
+qtt_status_t qtt_variational(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                             const qtt_trains_t *c, int32_t *c_ranks, int32_t sweeps, double *center_norm2,
+                             int32_t *status, void *workspace, size_t workspace_bytes, void *stream) {
+  Shape S;
+  qtt_status_t st = qtt_zipup_analyse(subscripts, op, x, 0, S);
+  if (st != QTT_OK) return st;
+  if (!c || !c->cores || !c->ranks || !c_ranks || !center_norm2 || !status) { set_error("NULL argument"); return QTT_EINVAL; }
+  if ((x->dtype != QTT_F64) || (op && op->dtype != QTT_F64) || c->dtype != QTT_F64) {
+    set_error("qtt_variational: QTT_F64 trains only");
+    return QTT_EUNSUPPORTED;
+  }
+  if (c->n_sites != S.L || c->batch != S.B || c->n_legs != 1) { set_error("seed train shape mismatch"); return QTT_ESHAPE; }
+  for (int q = 0; q < S.L; ++q)
+    if (c->d_out[q] != S.d[q]) { set_error("seed digit size mismatch at core %d", q); return QTT_ESHAPE; }
+  if (sweeps < 1) { set_error("sweeps < 1"); return QTT_EINVAL; }
+  if (S.L > 64) { set_error("n_sites > 64"); return QTT_EUNSUPPORTED; }
+  cplx::VarArgs a;
+  memset(&a, 0, sizeof(a));
+  long long member;
+  int pmax;
+  var_sizes(S, c, member, a.coff, a.eoff, a.e_n, a.s_n, pmax);
+  if (!workspace || workspace_bytes < (size_t)S.B * member * 8 + 256) {
+    set_error("workspace %zu bytes < required %zu", workspace_bytes, (size_t)S.B * member * 8 + 256);
+    return QTT_ECAPACITY;
+  }
+  a.L = S.L; a.B = S.B; a.kind = S.kind; a.op_batch = op ? op->batch : 1; a.sweeps = sweeps;
+  for (int q = 0; q < S.L; ++q) {
+    a.d[q] = S.d[q]; a.dj[q] = S.dj[q];
+    a.x[q] = (const double *)x->cores[q];
+    a.x_bs[q] = (long long)x->ranks[q] * x->d_out[q] * x->ranks[q + 1];
+    if (op) {
+      a.op[q] = (const double *)op->cores[q];
+      a.o_bs[q] = (long long)op->ranks[q] * op->d_out[q] * (op->n_legs == 2 ? op->d_in[q] : 1) * op->ranks[q + 1];
+    }
+    a.c[q] = (double *)c->cores[q];
+    a.c_bs[q] = (long long)c->ranks[q] * S.d[q] * c->ranks[q + 1];
+  }
+  for (int q = 0; q <= S.L; ++q) { a.xr[q] = S.xr[q]; a.orr[q] = S.orr[q]; a.cap[q] = c->ranks[q]; }
+  a.c_ranks = c_ranks; a.norms = center_norm2; a.status = status;
+  a.ws = (double *)workspace;
+  a.ws_member = member;
+  cudaStream_t s = (cudaStream_t)stream;
+  QTT_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), s));
+  cplx::k_variational<<<S.B, kThreads, 0, s>>>(a);
+  QTT_CUDA_TRY(cudaGetLastError());
+  return QTT_OK;
+}
+
+}  // extern "C"

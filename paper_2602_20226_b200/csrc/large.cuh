@@ -31,6 +31,9 @@ struct LargeIO {
 };
 
 size_t large_workspace_bytes(const Shape &S);
+// shape analysis of qtt_zipup's operands (zipup.cu), shared with qtt_variational
+qtt_status_t qtt_zipup_analyse(const char *subs, const qtt_trains_t *op, const qtt_trains_t *x, int32_t max_rank,
+                               Shape &S);
 // per-member path (complex.cu): one CTA per member, every step; complex128 trains (f2) and
 // the window-2 zip-up (f4, real or complex)
 size_t member_workspace_bytes(const Shape &S, int elem_bytes, int window);

@@ -977,6 +977,11 @@ static int train_dtypes(const qtt_trains_t *op, const qtt_trains_t *x, const qtt
   return -1;
 }
 
+qtt_status_t qtt_zipup_analyse(const char *subs, const qtt_trains_t *op, const qtt_trains_t *x, int32_t max_rank,
+                               Shape &S) {
+  return analyse(subs, op, x, max_rank, S);
+}
+
 }  // namespace qtt
 
 using namespace qtt;

@@ -48,7 +48,7 @@ QTT_F64, QTT_F32, QTT_C128 = 0, 1, 2
 _lib = None
 
 SYMBOLS = ["qtt_zipup_capacity", "qtt_zipup_workspace_bytes", "qtt_zipup_workspace_bytes_flags", "qtt_zipup",
-           "qtt_zipup_summary",
+           "qtt_zipup_summary", "qtt_variational_workspace_bytes", "qtt_variational",
            "qtt_round_capacity", "qtt_round_workspace_bytes", "qtt_round",
            "qtt_einsum_exact", "qtt_inner_workspace_bytes", "qtt_inner", "qtt_to_dense_workspace_bytes",
            "qtt_to_dense", "qtt_last_error", "qtt_version"]
@@ -73,6 +73,10 @@ def load_library(path: str = LIB_PATH):
     L.qtt_zipup.argtypes = [ctypes.c_char_p, P, P, f64, i32, ctypes.c_uint32, P, vp, vp, vp, vp,
                             ctypes.POINTER(_Diag), vp, sz, vp]
     L.qtt_zipup.restype = i32
+    L.qtt_variational_workspace_bytes.argtypes = [ctypes.c_char_p, P, P, P]
+    L.qtt_variational_workspace_bytes.restype = sz
+    L.qtt_variational.argtypes = [ctypes.c_char_p, P, P, P, vp, i32, vp, vp, vp, sz, vp]
+    L.qtt_variational.restype = i32
     L.qtt_zipup_summary.argtypes = [i32, i32, vp, vp, vp, vp, vp]
     L.qtt_zipup_summary.restype = i32
     L.qtt_round_capacity.argtypes = [P, i32, ctypes.POINTER(i32)]
@@ -383,6 +387,41 @@ def round_train(x: DeviceTrains, x_ranks: Optional[torch.Tensor], eps: float, ma
                        int(max_rank), ctypes.byref(os_), ranks.data_ptr(), delta2.data_ptr(), norm2.data_ptr(),
                        status.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
     return ZipupResult(out, ranks, delta2, norm2, status, None, None, ws)
+
+
+@dataclass
+class VariationalResult:
+    out: DeviceTrains           # capacity-sized cores of C (centre at site 0)
+    ranks: torch.Tensor         # int32 (B, L+1)
+    center_norm2: torch.Tensor  # float64 (B, sweeps * 2L): |C_q|^2 after every update
+    status: torch.Tensor
+
+
+def variational(subscripts: str, op: Optional[DeviceTrains], x: DeviceTrains, seed: ZipupResult, sweeps: int,
+                stream=None) -> VariationalResult:
+    """qtt_variational (f3): refine a zip-up result variationally.  The
+    seed's cores and ranks are copied first (the zip-up result is left intact)."""
+    L = load_library()
+    c = DeviceTrains([t.clone() for t in seed.out.cores], list(seed.out.ranks), list(seed.out.d_out), None)
+    ranks = seed.ranks.clone()
+    xs, kx = x.c_struct()
+    os_ = None
+    if op is not None:
+        os_, ko = op.c_struct()
+    cs, kc = c.c_struct()
+    B, n = x.batch, x.n_sites
+    dev = x.cores[0].device
+    norms = torch.zeros((B, sweeps * 2 * n), dtype=torch.float64, device=dev)
+    status = torch.zeros((1,), dtype=torch.int32, device=dev)
+    nbytes = L.qtt_variational_workspace_bytes(subscripts.encode(), ctypes.byref(os_) if os_ is not None else None,
+                                               ctypes.byref(xs), ctypes.byref(cs))
+    if nbytes == 0:
+        raise QttError(2, L.qtt_last_error().decode())
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    _check(L.qtt_variational(subscripts.encode(), ctypes.byref(os_) if os_ is not None else None, ctypes.byref(xs),
+                             ctypes.byref(cs), ranks.data_ptr(), int(sweeps), norms.data_ptr(), status.data_ptr(),
+                             ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+    return VariationalResult(c, ranks, norms, status)
 
 
 def summary(res: ZipupResult, stream=None) -> torch.Tensor:
