@@ -40,9 +40,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "qft"],
+    ap.add_argument("--workload", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "qft", "variational"],
                     help="qft: the tensorized DFT of PAPER.md:533-566 (N = 2^13, max rank 16) as a chain of "
-                         "12 complex Hadamard zip-ups (SURVEY.md §8(f) f2)")
+                         "12 complex Hadamard zip-ups (SURVEY.md §8(f) f2); variational: one sweep of "
+                         "qtt_variational (f3) on cfg5 members seeded by a max-rank-16 zip-up")
     ap.add_argument("--members-per-gpu", type=int, default=512)
     ap.add_argument("--cpu-members", type=int, default=8, help="oracle sample size (members) for cpu_baseline")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
@@ -266,6 +267,8 @@ def main():
         return run_reference(args, rank, world)
     if args.workload == "qft":
         return run_qft(args, rank, world, local)
+    if args.workload == "variational":
+        return run_variational(args, rank, world, local)
 
     import torch
     import torch.distributed as dist
@@ -581,6 +584,78 @@ def run_qft(args, rank, world, local):
                 "e2e": {"value": units / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ems, 3)},
                 "gpu_launches": (n - 1) * args.steps, "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_variational(args, rank, world, local):
+    """--workload variational (f3): cfg5 members (this rank's shard) seeded by a max-rank-16
+    zip-up (untimed); one step = one qtt_variational sweep (right and back) over every member.
+    Unit: site updates per second (2 L per member per sweep)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2602_20226_b200 import qtt
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    M = args.members_per_gpu
+    lo, hi = qdist.member_range(rank, max(world, 1), M)
+    probs, xs, ops = gen.cfg5_batch_arrays(list(range(lo, hi)))
+    xd, od = qtt.to_device(xs), qtt.to_device(ops, mpo=True)
+    seed = qtt.ZipupPlan("ij,j->i", od, xd, 1e-10, 16).run(od, xd)
+    L, B = xd.n_sites, xd.batch
+    for _ in range(max(args.warmup, 3)):
+        v = qtt.variational("ij,j->i", od, xd, seed, 1)
+    torch.cuda.synchronize()
+    assert int(v.status.item()) == 0
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    clocks.start()
+    time.sleep(0.25)
+    t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        v = qtt.variational("ij,j->i", od, xd, seed, 1)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = qdist.max_over_ranks(t0.elapsed_time(t1) / args.steps, "cuda", dist)
+    units = max(world, 1) * B * 2 * L
+    value = units / (ms * 1e-3)
+    cpu = None
+    gain = None
+    if rank == 0 and world == 1:
+        from oracle import tt
+        from oracle.variational import variational as ovar
+        b = 0
+        sd = qtt.member_cores(seed.out, seed.ranks[b].cpu().tolist(), b)
+        got = qtt.member_cores(v.out, v.ranks[b].cpu().tolist(), b)
+        ex = tt.exact_matvec(probs[b].op.cores, probs[b].x.cores)
+        gain = {"member": b, "dist_seed": tt.diff_norm(sd, ex), "dist_after_1_sweep": tt.diff_norm(got, ex)}
+        if not args.no_cpu_baseline:
+            c0 = time.perf_counter()
+            ref = ovar("matvec", probs[b].op.cores, probs[b].x.cores, sd, 1)
+            cdt = time.perf_counter() - c0
+            gain["parity_vs_oracle"] = tt.diff_norm(got, ref["cores"]) / tt.qr_norm(ref["cores"])
+            cpu = {"value": 2 * L / cdt, "unit": "site-updates/s", "cores": os.cpu_count(), "kind": "oracle",
+                   "sample": f"one member, one sweep, NumPy einsum + LAPACK QR, {cdt:.2f} s wall"}
+    if rank == 0:
+        line = {"metric": "variational site updates/sec (f3)", "value": round(value, 3), "unit": "site-updates/s",
+                "n_gpus": max(world, 1), "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (cfg5 members, seeded generators)",
+                "config": {"workload": "f3: one single-site variational sweep (PAPER.md:277-301) on cfg5 members "
+                                       "seeded by a max-rank-16 zip-up", "members_per_gpu": M,
+                           "global_batch": M * max(world, 1), "L": L, "seed_max_rank": 16,
+                           "parallelism": f"dp{max(world, 1)} (members sharded)"},
+                "roofline": {"kernel": "k_variational (one CTA per member, environments in global memory)",
+                             "bound": "alu", "achieved": None, "peak": None, "unit": "TFLOP/s", "frac": None,
+                             "traffic": None, "note": "first plain version; no flop model yet"},
+                "distance": gain, "cpu_baseline": cpu, "e2e": None,
+                "gpu_launches": args.steps, "clocks": clk}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
