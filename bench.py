@@ -263,6 +263,8 @@ def main():
 
     if args.impl == "reference" and args.workload == "qft":
         return run_qft_reference(args, rank)
+    if args.impl == "reference" and args.workload == "variational":
+        return run_variational_reference(args, rank)
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if args.workload == "qft":
@@ -661,6 +663,35 @@ def run_variational(args, rank, world, local):
         dist.destroy_process_group()
 
 
+def run_variational_reference(args, rank):
+    """--impl reference for --workload variational: the oracle's sweep on one member (bounded
+    sample) with the GPU arm's config and unit."""
+    if rank != 0:
+        return
+    from oracle.zipup import zipup as ozip
+    from oracle.variational import variational as ovar
+    probs, xs, ops = gen.cfg5_batch_arrays([0])
+    p = probs[0]
+    seed = ozip("matvec", p.op.cores, p.x.cores, 1e-10, 16)["cores"]
+    L = len(p.x.cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ovar("matvec", p.op.cores, p.x.cores, seed, 1)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = 2 * L / dt
+    line = {"metric": "variational site updates/sec (f3)", "value": round(value, 3), "unit": "site-updates/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": 0, "ms_per_step": round(dt * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+            "data": "synthetic (cfg5 members, seeded generators)",
+            "config": {"workload": "f3: one single-site variational sweep (PAPER.md:277-301) on cfg5 members "
+                                   "seeded by a max-rank-16 zip-up", "members_per_gpu": args.members_per_gpu,
+                       "global_batch": args.members_per_gpu, "L": L, "seed_max_rank": 16, "parallelism": "dp1"},
+            "cpu_baseline": {"value": round(value, 3), "unit": "site-updates/s", "cores": os.cpu_count(),
+                             "kind": "oracle", "sample": "each step: one member, one sweep (oracle)"},
+            "e2e": {"value": round(value, 3), "unit": "site-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
 def run_qft_reference(args, rank):
     if rank != 0:
         return
@@ -696,13 +727,15 @@ def run_reference(args, rank, world):
     if args.workload == "cfg5":
         cfg = dict(cfg, members_per_gpu=full_members, global_batch=full_members * max(world, 1),
                    parallelism=f"dp{max(world, 1)} (members sharded, 1 all-reduce/step)")
+    if args.window == 2:
+        cfg = dict(cfg, window=2)
     for _ in range(args.warmup):
-        oracle_sample(kind, probs, 1)
+        oracle_sample(kind, probs, 1, args.window)
     vals = []
     t0 = time.perf_counter()
     info = None
     for _ in range(args.steps):
-        info, _ = oracle_sample(kind, probs, len(probs))
+        info, _ = oracle_sample(kind, probs, len(probs), args.window)
         vals.append(info["value"])
     dt = time.perf_counter() - t0
     value = statistics.median(vals)
