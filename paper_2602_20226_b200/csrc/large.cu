@@ -174,7 +174,11 @@ __global__ void k_copy_T(const SiteDims *dims, const double *T, double *Tw, doub
 
 // ------------------------------------------------------------------ a3: cooperative QR
 
-constexpr int kNb = 16;              // panel width
+#ifndef QTT_QR_NB
+#define QTT_QR_NB 16
+#endif
+constexpr int kNb = QTT_QR_NB;       // panel width (32 measured: cfg3 equal, cfg2 +10% -- the
+                                     // column-step grid barriers, not the trailing passes, bound it)
 constexpr int kQrRowsMax = 512;      // max T^H rows per CTA held in shared memory (panel)
 
 struct QrArgs {
@@ -199,8 +203,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_qr_coop(QrArgs a) {
   const int m = D.m, n = D.n, g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r0 = g * a.RB, r1 = min(n, r0 + a.RB), nr = max(0, r1 - r0);
   double *P = smq;                              // [kNb][RB] panel (my rows)
-  double *Y = P + kNb * a.RB;                   // [kNb][RB] reflectors (unit diagonal explicit)
-  double *red = Y + kNb * a.RB;                 // [kThreads/32]
+  double *Y = P;                                // the same storage holds the reflectors (unit
+                                                // diagonal explicit) once the panel is written back
+  double *red = P + kNb * a.RB;                 // [kThreads/32]
   double *tw = red + 32;                        // [kNb*kNb] T_wy ; [kNb] tau ; [kNb] dots
   double *tau = tw + kNb * kNb;
   double *dots = tau + kNb;
@@ -268,8 +273,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_qr_coop(QrArgs a) {
     // write the factored panel back (R entries and reflectors), build Y
     for (int idx = tid; idx < nb * nr; idx += kThreads) {
       const int cc = idx / nr, i = idx % nr, r = r0 + i, j = j0 + cc;
-      a.Tw[(size_t)j * n + r] = P[cc * a.RB + i];
-      Y[cc * a.RB + i] = (r > j) ? P[cc * a.RB + i] : (r == j ? 1.0 : 0.0);
+      const double pv = P[cc * a.RB + i];
+      a.Tw[(size_t)j * n + r] = pv;
+      Y[cc * a.RB + i] = (r > j) ? pv : (r == j ? 1.0 : 0.0);
     }
     for (int idx = tid; idx < kNb * a.RB; idx += kThreads)
       if (idx / a.RB >= nb) Y[idx] = 0.0;
@@ -918,7 +924,7 @@ static qtt_status_t plan_sweep(int L, const std::vector<int> &d, const std::vect
   P.RB = (int)((P.ncap + P.Gqr - 1) / P.Gqr);
   P.RB = ((P.RB + 31) / 32) * 32;
   while (P.RB > kQrRowsMax) { set_error("large path: n = %lld too large", P.ncap); return QTT_EUNSUPPORTED; }
-  P.qr_smem = sizeof(double) * ((size_t)2 * kNb * P.RB + 32 + kNb * kNb + 2 * kNb + kNb * 64);
+  P.qr_smem = sizeof(double) * ((size_t)kNb * P.RB + 32 + kNb * kNb + 2 * kNb + kNb * 64);
   // Jacobi: blocks of WB = kWarps columns -- every warp has a pair in each cross round, and a
   // block round (dataflow wait + block copies) is amortised over WB rounds (measured: cfg2
   // 134 -> 101 ms against ~64 blocks of 4; cfg3 already had WB = 8), capped by smem
