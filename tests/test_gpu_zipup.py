@@ -251,3 +251,25 @@ def test_extreme_magnitudes(lib, scale):
     x[0] = x[0] * scale
     op = gen.random_mpo(dims, 3, np.random.default_rng(32), 0.5).cores
     check(lib, "matvec", op, x, 1e-10, 24)
+
+
+@pytest.mark.parametrize("R", [64, 65])
+def test_small_large_path_boundary(lib, R):
+    """m = chi d = 128 runs on the small-member path, 130 on the large one: both agree with the
+    oracle at the boundary (SURVEY.md §8(a) a3/a4 size split)."""
+    x = gen.random_mps([2] * 14, R, np.random.default_rng(100 + R)).cores      # bonds up to R
+    assert max(c.shape[0] for c in x) == R
+    op = gen.random_mpo([2] * 14, 2, np.random.default_rng(200 + R), 0.5).cores
+    check(lib, "truncate", None, x, 1e-10, 0, dense=True)                       # m = 2 R
+    check(lib, "matvec", op, x, 1e-10, 64, dense=True)
+
+
+def test_maximum_sites_and_refusal(lib):
+    """L = 64 sites (kMaxSites) works; L = 65 is refused with QTT_EUNSUPPORTED, not run."""
+    x = gen.random_mps([2] * 64, 6, np.random.default_rng(7)).cores
+    check(lib, "truncate", None, x, 1e-8, 5, dense=False)
+    x65 = gen.random_mps([2] * 65, 2, np.random.default_rng(8)).cores
+    xd = lib.to_device(x65)
+    with pytest.raises(lib.QttError) as e:
+        lib.ZipupPlan("i->i", None, xd, 1e-8, 4)
+    assert e.value.status == 8
