@@ -575,7 +575,7 @@ def run_qft(args, rank, world, local):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
                 "scaling": "replicas", "vs_baseline": None, "dtype": "c128",
                 "data": "the paper's closed-form DFT factor trains (gen.qft_trains)", "config": _qft_cfg(world),
-                "roofline": {"kernel": "k_zipup_c (one CTA per member: the chain has one member)", "bound": "alu",
+                "roofline": {"kernel": "k_zipup<complex> (one CTA per member: the chain has one member)", "bound": "alu",
                              "achieved": round(achieved, 6), "peak": round(per_sm, 4), "unit": "TFLOP/s",
                              "frac": round(achieved / per_sm, 5), "traffic": None,
                              "peak_source": "measured FP64 peak / SM count (one CTA runs the member)"},
