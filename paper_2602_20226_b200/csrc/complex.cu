@@ -214,7 +214,7 @@ __device__ int jacobi(S *A, int rows, int p, double noise_eps, double *red) {
   const int half = lane >> 4, hl = lane & 15;
   const unsigned hmask = 0xffffu << (16 * half);
   const double tol = (double)max(rows, 1) * DBL_EPSILON;
-  __shared__ int s_rot;
+  __shared__ int s_rot, s_big, s_fail;
   double tot = 0.0;
   for (int i = tid; i < rows * p; i += kThreads) tot += abs2(A[i]);
   tot = block_sum(tot, red);
@@ -234,9 +234,9 @@ __device__ int jacobi(S *A, int rows, int p, double noise_eps, double *red) {
   const int n = p + (p & 1);
   int sweep = 0;
   for (; sweep < kMaxSweeps; ++sweep) {
-    if (tid == 0) s_rot = 0;
+    if (tid == 0) { s_rot = 0; s_big = 0; }
     __syncthreads();
-    int rot = 0;
+    int rot = 0, big = 0;
     for (int r = 0; r < n - 1; ++r) {
       // one pair per half-warp (16 lanes): 16 pairs of a round in flight across the 8 warps
       for (int pr = 2 * warp + half; pr < n / 2; pr += 2 * kWarps) {
@@ -271,6 +271,7 @@ __device__ int jacobi(S *A, int rows, int p, double noise_eps, double *red) {
           g = shx(g, hmask, o);
         }
         const double ag2 = abs2(g);
+        if (al > noise && be > noise && ag2 >= 1e-12 * (al * be)) big = 1;
         if (al > noise && be > noise && ag2 > tol * tol * al * be) {
           // division-free (as the fp64 path): with d = b - a, y = 1/sqrt(d^2 + 4|g|^2),
           // c^2 = (1 + |d| y)/2, z = 1/c: c = c^2 z and s e^{i phi} = sign(d) y z g
@@ -298,10 +299,44 @@ __device__ int jacobi(S *A, int rows, int p, double noise_eps, double *red) {
       __syncthreads();
     }
     if (rot) s_rot = 1;
+    if (big) s_big = 1;
     __syncthreads();
-    const int any = s_rot;
+    const int any = s_rot, anybig = s_big;
     __syncthreads();
     if (!any) { ++sweep; break; }
+    // every pair of this sweep started within |cos| < 1e-6: by the quadratic convergence of
+    // cyclic Jacobi the next sweep is almost always the verification sweep that rotates nothing
+    // -- check that on all pairs at once (no rounds, one barrier) with the sweep's own test
+    if (!anybig) {
+      if (tid == 0) s_fail = 0;
+      __syncthreads();
+      int fail = 0;
+      for (int e = 2 * warp + half; e < p * p; e += 2 * kWarps) {
+        const int ci = e / p, cj = e % p;
+        if (cj <= ci) continue;
+        const S *ai = A + (size_t)ci * rows, *aj = A + (size_t)cj * rows;
+        double al = 0.0, be = 0.0;
+        S g = mk<S>(0.0, 0.0);
+        for (int i = hl; i < rows; i += 16) {
+          const S x = ai[i], y = aj[i];
+          al += abs2(x);
+          be += abs2(y);
+          g = cfma(x, y, g);
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          al = shx(al, hmask, o);
+          be = shx(be, hmask, o);
+          g = shx(g, hmask, o);
+        }
+        if (al > noise && be > noise && abs2(g) > tol * tol * al * be) fail = 1;
+      }
+      if (fail) s_fail = 1;
+      __syncthreads();
+      const int f = s_fail;
+      __syncthreads();
+      if (!f) { ++sweep; break; }
+    }
   }
   if (scale != 1.0) {
     const double inv = 1.0 / scale;
