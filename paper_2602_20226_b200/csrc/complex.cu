@@ -770,17 +770,17 @@ __device__ __forceinline__ double opval(const VarArgs &a, const double *O, int q
 
 // X2[c, i, w', r'] = sum_{w, r, j} Le[c, w, r] W[w, i, j, w'] x[r, j, r']   (c < rc)
 __device__ void env_apply_left(const VarArgs &a, int q, int rc, const double *Le, const double *X,
-                               const double *O, double *X1, double *X2) {
+                               const double *O, double *X1, double *X2, double *gsm) {
   const int tid = threadIdx.x;
   const int d = a.d[q], dj = a.dj[q];
   const int w = (a.kind == TRUNCATE) ? 1 : a.orr[q], w2 = (a.kind == TRUNCATE) ? 1 : a.orr[q + 1];
   const int r = a.xr[q], r2 = a.xr[q + 1];
-  // X1[c, w, j, r'] = sum_r Le[c, w, r] x[r, j, r']
-  for (int idx = tid; idx < rc * w * dj * r2; idx += kThreads) {
-    const int rr2 = idx % r2, jj = (idx / r2) % dj, ww = (idx / (r2 * dj)) % w, c = idx / (r2 * dj * w);
-    double s = 0.0;
-    for (int rr = 0; rr < r; ++rr) s = fma(Le[((size_t)c * w + ww) * r + rr], X[((size_t)rr * dj + jj) * r2 + rr2], s);
-    X1[idx] = s;
+  // X1[(c, w), (j, r')] = sum_r Le[(c, w), r] x[r, (j, r')]   (CTA GEMM, smem-staged tiles)
+  {
+    const int N = dj * r2;
+    cta_gemm<kThreads>(rc * w, N, r, [&](int i, int k) { return Le[(size_t)i * r + k]; },
+                       [&](int k, int j) { return X[(size_t)k * N + j]; },
+                       [&](int i, int j, double v) { X1[(size_t)i * N + j] = v; }, gsm);
   }
   __syncthreads();
   // X2[c, i, w', r'] = sum_{w, j} X1[c, w, j, r'] W[w, i, j, w']
@@ -799,17 +799,17 @@ __device__ void env_apply_left(const VarArgs &a, int q, int rc, const double *Le
 
 // Re_new[c, w, r] = sum C[c, i, c'] W[w, i, j, w'] x[r, j, r'] Re[c', w', r']
 __device__ void env_right(const VarArgs &a, int q, int rc, int rc2, const double *C, const double *Re,
-                          const double *X, const double *O, double *Y1, double *Y2, double *Rn) {
+                          const double *X, const double *O, double *Y1, double *Y2, double *Rn, double *gsm) {
   const int tid = threadIdx.x;
   const int d = a.d[q], dj = a.dj[q];
   const int w = (a.kind == TRUNCATE) ? 1 : a.orr[q], w2 = (a.kind == TRUNCATE) ? 1 : a.orr[q + 1];
   const int r = a.xr[q], r2 = a.xr[q + 1];
-  // Y1[c, i, w', r'] = sum_{c'} C[c, i, c'] Re[c', w', r']
-  for (int idx = tid; idx < rc * d * w2 * r2; idx += kThreads) {
-    const int rr2 = idx % r2, ww2 = (idx / r2) % w2, ii = (idx / (r2 * w2)) % d, c = idx / (r2 * w2 * d);
-    double s = 0.0;
-    for (int a2 = 0; a2 < rc2; ++a2) s = fma(C[((size_t)c * d + ii) * rc2 + a2], Re[((size_t)a2 * w2 + ww2) * r2 + rr2], s);
-    Y1[idx] = s;
+  // Y1[(c, i), (w', r')] = sum_{c'} C[(c, i), c'] Re[c', (w', r')]
+  {
+    const int N = w2 * r2;
+    cta_gemm<kThreads>(rc * d, N, rc2, [&](int i, int k) { return C[(size_t)i * rc2 + k]; },
+                       [&](int k, int j) { return Re[(size_t)k * N + j]; },
+                       [&](int i, int j, double v) { Y1[(size_t)i * N + j] = v; }, gsm);
   }
   __syncthreads();
   // Y2[c, w, j, r'] = sum_{i, w'} Y1[c, i, w', r'] W[w, i, j, w']
@@ -824,14 +824,12 @@ __device__ void env_right(const VarArgs &a, int q, int rc, int rc2, const double
     Y2[idx] = s;
   }
   __syncthreads();
-  // Rn[c, w, r] = sum_{j, r'} Y2[c, w, j, r'] x[r, j, r']
-  for (int idx = tid; idx < rc * w * r; idx += kThreads) {
-    const int rr = idx % r, ww = (idx / r) % w, c = idx / (r * w);
-    double s = 0.0;
-    for (int jj = 0; jj < dj; ++jj)
-      for (int rr2 = 0; rr2 < r2; ++rr2)
-        s = fma(Y2[(((size_t)c * w + ww) * dj + jj) * r2 + rr2], X[((size_t)rr * dj + jj) * r2 + rr2], s);
-    Rn[idx] = s;
+  // Rn[(c, w), r] = sum_{(j, r')} Y2[(c, w), (j, r')] x[r, (j, r')]
+  {
+    const int K = dj * r2;
+    cta_gemm<kThreads>(rc * w, r, K, [&](int i, int k) { return Y2[(size_t)i * K + k]; },
+                       [&](int k, int j) { return X[(size_t)j * K + k]; },
+                       [&](int i, int j, double v) { Rn[(size_t)i * r + j] = v; }, gsm);
   }
   __syncthreads();
 }
@@ -839,6 +837,7 @@ __device__ void env_right(const VarArgs &a, int q, int rc, int rc2, const double
 __global__ void __launch_bounds__(kThreads, 1) k_variational(VarArgs a) {
   const int b = blockIdx.x, tid = threadIdx.x, L = a.L;
   __shared__ double red[kWarps];
+  __shared__ double gsm[2 * 16 * 64];            // cta_gemm staging
   __shared__ int cr[65];
   double *w0 = a.ws + (size_t)b * a.ws_member;
   double *Cw = w0, *Le = Cw + a.coff[L], *Re = Le + a.e_n, *S1 = Re + a.e_n, *S2 = S1 + a.s_n, *S3 = S2 + a.s_n,
@@ -905,22 +904,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_variational(VarArgs a) {
   if (tid == 0) { Le[a.eoff[0]] = 1.0; Re[a.eoff[L]] = 1.0; }
   __syncthreads();
   for (int q = L - 1; q >= 1; --q)
-    env_right(a, q, cr[q], cr[q + 1], Cw + a.coff[q], Re + a.eoff[q + 1], Xq(q), Oq(q), S1, S2, Re + a.eoff[q]);
+    env_right(a, q, cr[q], cr[q + 1], Cw + a.coff[q], Re + a.eoff[q + 1], Xq(q), Oq(q), S1, S2, Re + a.eoff[q], gsm);
   int cnt = 0;
   auto update = [&](int q) {                      // C_q = sum Le[q] W_q x_q Re[q+1]   (Eq. variational)
-    env_apply_left(a, q, cr[q], Le + a.eoff[q], Xq(q), Oq(q), S1, S2);
+    env_apply_left(a, q, cr[q], Le + a.eoff[q], Xq(q), Oq(q), S1, S2, gsm);
     const int w2 = (a.kind == TRUNCATE) ? 1 : a.orr[q + 1], r2 = a.xr[q + 1], rc2 = cr[q + 1], d = a.d[q];
     double *C = Cw + a.coff[q];
-    double sq = 0.0;
-    for (int idx = tid; idx < cr[q] * d * rc2; idx += kThreads) {
-      const int a2 = idx % rc2, ci = idx / rc2;
-      double sacc = 0.0;
-      for (int ww2 = 0; ww2 < w2; ++ww2)
-        for (int rr2 = 0; rr2 < r2; ++rr2)
-          sacc = fma(S2[((size_t)ci * w2 + ww2) * r2 + rr2], Re[a.eoff[q + 1] + ((size_t)a2 * w2 + ww2) * r2 + rr2], sacc);
-      C[idx] = sacc;
-      sq = fma(sacc, sacc, sq);
+    {  // C[(c, i), c'] = sum_{(w', r')} X2[(c, i), (w', r')] Re[c', (w', r')]
+      const int K = w2 * r2;
+      const double *R1 = Re + a.eoff[q + 1];
+      cta_gemm<kThreads>(cr[q] * d, rc2, K, [&](int i, int k) { return S2[(size_t)i * K + k]; },
+                         [&](int k, int j) { return R1[(size_t)j * K + k]; },
+                         [&](int i, int j, double v) { C[(size_t)i * rc2 + j] = v; }, gsm);
     }
+    __syncthreads();
+    double sq = 0.0;
+    for (int idx = tid; idx < cr[q] * d * rc2; idx += kThreads) sq = fma(C[idx], C[idx], sq);
     sq = block_sum(sq, red);
     if (tid == 0) {
       a.norms[(size_t)b * a.sweeps * 2 * L + cnt] = sq;
@@ -935,23 +934,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_variational(VarArgs a) {
       if (q == L - 1) break;
       move_right(q);
       // Le[q+1][c', w', r'] = sum_{c, i} C[c, i, c'] X2[c, i, w', r']   (X2 from Le[q])
-      env_apply_left(a, q, cr[q], Le + a.eoff[q], Xq(q), Oq(q), S1, S2);
+      env_apply_left(a, q, cr[q], Le + a.eoff[q], Xq(q), Oq(q), S1, S2, gsm);
       const int w2 = (a.kind == TRUNCATE) ? 1 : a.orr[q + 1], r2 = a.xr[q + 1], k = cr[q + 1];
       const int rows = cr[q] * a.d[q];
       const double *C = Cw + a.coff[q];
-      for (int idx = tid; idx < k * w2 * r2; idx += kThreads) {
-        const int wr = idx % (w2 * r2), a2 = idx / (w2 * r2);
-        double sacc = 0.0;
-        for (int ci = 0; ci < rows; ++ci) sacc = fma(C[(size_t)ci * k + a2], S2[(size_t)ci * w2 * r2 + wr], sacc);
-        Le[a.eoff[q + 1] + idx] = sacc;
-      }
+      double *L1 = Le + a.eoff[q + 1];
+      const int N = w2 * r2;
+      cta_gemm<kThreads>(k, N, rows, [&](int i, int kk) { return C[(size_t)kk * k + i]; },
+                         [&](int kk, int j) { return S2[(size_t)kk * N + j]; },
+                         [&](int i, int j, double v) { L1[(size_t)i * N + j] = v; }, gsm);
       __syncthreads();
     }
     for (int q = L - 1; q >= 0; --q) {            // and back
       update(q);
       if (q == 0) break;
       move_left(q);
-      env_right(a, q, cr[q], cr[q + 1], Cw + a.coff[q], Re + a.eoff[q + 1], Xq(q), Oq(q), S1, S2, Re + a.eoff[q]);
+      env_right(a, q, cr[q], cr[q + 1], Cw + a.coff[q], Re + a.eoff[q + 1], Xq(q), Oq(q), S1, S2, Re + a.eoff[q], gsm);
     }
   }
   // write back (centre at site 0); bonds may have shrunk where a core could not be orthonormal
