@@ -397,8 +397,32 @@ __device__ void orth_operand(const Args &a, const void *const *src, const long l
 // rows c (for window 2 the rows are (chi, pending digit), so the same formula applies)
 template <typename S>
 __device__ void contract(const Args &a, int rows, int d, int dj, int w, int w2, int r, int r2, const S *G, const S *X,
-                         const S *O, S *T) {
+                         const S *O, S *T, S *X1, double *gsm) {
   const int n = w2 * r2;
+  if constexpr (sizeof(S) == sizeof(double)) {    // real: X1 = G x as a CTA GEMM, then the operator core
+    if (a.kind != TRUNCATE) {
+      const int N = dj * r2;                      // X1[(c, w), (j, r')] = sum_r G[(c, w), r] x[r, (j, r')]
+      cta_gemm<kThreads>(rows * w, N, r, [&](int i, int k) { return G[(size_t)i * r + k]; },
+                         [&](int k, int j) { return X[(size_t)k * N + j]; },
+                         [&](int i, int j, double v) { X1[(size_t)i * N + j] = v; }, gsm);
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < rows * d * n; idx += kThreads) {
+        const int rr2 = idx % r2, ww2 = (idx / r2) % w2, ii = (idx / n) % d, c = idx / (n * d);
+        double acc = 0.0;
+        for (int ww = 0; ww < w; ++ww) {
+          if (a.kind == HADAMARD) {
+            acc = fma(O[((size_t)ww * d + ii) * w2 + ww2], X1[(((size_t)c * w + ww) * dj + ii) * r2 + rr2], acc);
+          } else {
+            for (int jj = 0; jj < dj; ++jj)
+              acc = fma(O[(((size_t)ww * d + ii) * dj + jj) * w2 + ww2], X1[(((size_t)c * w + ww) * dj + jj) * r2 + rr2], acc);
+          }
+        }
+        T[idx] = acc;
+      }
+      __syncthreads();
+      return;
+    }
+  }
   for (int idx = threadIdx.x; idx < rows * d * n; idx += kThreads) {
     const int rr2 = idx % r2, ww2 = (idx / r2) % w2, ii = (idx / n) % d, c = idx / (n * d);
     S acc = mk<S>(0.0, 0.0);
@@ -436,6 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup(Args a) {
   const int b = blockIdx.x, tid = threadIdx.x, L = a.L, L1 = L + 1;
   __shared__ double red[kWarps];
   __shared__ double s_sc[4];
+  __shared__ double gsm[sizeof(S) == sizeof(double) ? 2 * 16 * 64 : 1];   // cta_gemm staging (real)
   extern __shared__ __align__(16) unsigned char zsm_raw[];
   S *zsm = reinterpret_cast<S *>(zsm_raw);
   S *w0 = static_cast<S *>(a.ws) + (size_t)b * a.ws_member;
@@ -473,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup(Args a) {
   int chi = 1;                                    // bond of the next output core
   int s0 = 0;
   if (win2) {                                     // the first site contracted exactly into the carry
-    contract<S>(a, 1, a.d[0], a.dj[0], orr[0], orr[1], xr[0], xr[1], G, Xo + a.xoff[0], Oo + a.ooff[0], T);
+    contract<S>(a, 1, a.d[0], a.dj[0], orr[0], orr[1], xr[0], xr[1], G, Xo + a.xoff[0], Oo + a.ooff[0], T, H, gsm);
     const int n0 = a.d[0] * orr[1] * xr[1];
     for (int i = tid; i < n0; i += kThreads) G[i] = T[i];
     rows = a.d[0];
@@ -486,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup(Args a) {
     const int q = win2 ? st - 1 : st;
     const int d = a.d[st], dj = a.dj[st];
     const int w = orr[st], w2 = orr[st + 1], r = xr[st], r2 = xr[st + 1];
-    contract<S>(a, rows, d, dj, w, w2, r, r2, G, Xo + a.xoff[st], Oo + a.ooff[st], T);
+    contract<S>(a, rows, d, dj, w, w2, r, r2, G, Xo + a.xoff[st], Oo + a.ooff[st], T, H, gsm);
     const int m = win2 ? rows : rows * d;         // split: rows (chi, i_q) ...
     const int n = win2 ? d * w2 * r2 : w2 * r2;   // ... columns (window 2: i_{q+1}, w', r')
     S *Cq = static_cast<S *>(a.Cq[q]) + (size_t)b * a.Cq_bs[q];
@@ -593,12 +618,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup(Args a) {
       a.delta2[(size_t)b * L + q] = s_sc[1];
     }
     // G[kk, col] = sum_i conj(U[i, kk]) T[i, col]   (k x n)
-    for (int idx = tid; idx < k * n; idx += kThreads) {
-      const int kk = idx / n, col = idx % n;
-      const S *u = A + (size_t)perm[kk] * m;
-      S acc = mk<S>(0.0, 0.0);
-      for (int i = 0; i < m; ++i) acc = cfma(u[i], T[(size_t)i * n + col], acc);
-      G[idx] = acc;
+    if constexpr (sizeof(S) == sizeof(double)) {
+      cta_gemm<kThreads>(k, n, m, [&](int kk, int i) { return (double)A[(size_t)perm[kk] * m + i]; },
+                         [&](int i, int col) { return (double)T[(size_t)i * n + col]; },
+                         [&](int kk, int col, double v) { G[(size_t)kk * n + col] = v; }, gsm);
+    } else {
+      for (int idx = tid; idx < k * n; idx += kThreads) {
+        const int kk = idx / n, col = idx % n;
+        const S *u = A + (size_t)perm[kk] * m;
+        S acc = mk<S>(0.0, 0.0);
+        for (int i = 0; i < m; ++i) acc = cfma(u[i], T[(size_t)i * n + col], acc);
+        G[idx] = acc;
+      }
     }
     __syncthreads();
     if (win2 && st == L - 1) {                    // fully decomposed: C_{L-1} = diag(s) V^H (k, d, 1)
@@ -640,6 +671,11 @@ static void member_sizes(const Shape &S, int window, long long &zmember, long lo
     const long long oc = (S.kind == MATVEC) ? (long long)S.orr[q] * S.d[q] * S.dj[q] * S.orr[q + 1]
                                             : (long long)S.orr[q] * S.d[q] * S.orr[q + 1];
     core_max = std::max(core_max, oc);
+  }
+  for (int q = 0; q < S.L; ++q) {        // X1 = G x staged in the H region during the contraction
+    const long long rows = (window == 2 && q > 0) ? (long long)S.cap[q - 1] * S.d[q - 1] : (long long)S.cap[q];
+    const long long w = (S.kind == TRUNCATE) ? 1 : S.orr[q];
+    tn = std::max(tn, std::max(rows, 1LL) * w * S.dj[q] * S.xr[q + 1]);
   }
   if (window == 2) {                    // super-core (chi d_q) x (d_{q+1} w' r') and its carry
     for (int st = 1; st < S.L; ++st) {
