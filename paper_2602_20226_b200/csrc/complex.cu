@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "jacobi.cuh"
 #include "large.cuh"
 
 namespace qtt {
@@ -112,6 +113,8 @@ struct Args {
   int smem;                            // 1: G, T, H, Q/A, tau in dynamic shared memory
   long long *cycles;                   // optional [B][L][4]: a2, a3, a4, a5-a6 clocks (a1 in [q=0][3])
   int window;                          // 1, or 2 (f4)
+  int jreg;                            // real: register-blocked Jacobi (jacobi.cuh) in smem at jsm_off
+  long long jsm_off;                   // byte offset of that region in dynamic shared memory
 };
 
 // In-place Householder QR of the column-major rows x cols matrix H (ld = rows), K =
@@ -555,7 +558,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup(Args a) {
     if (tid == 0 && a.cycles) a.cycles[((size_t)b * L + q) * 4 + 1] = clock64() - tph;
     tph = clock64();
     // ---- a4
-    const int sweeps = jacobi<S>(A, m, p, a.eps > 1e-14 ? DBL_EPSILON * DBL_EPSILON : 0.0, red);
+    int sweeps = -1;
+    if constexpr (sizeof(S) == sizeof(double)) {
+      if (a.jreg && m <= 128 && p <= 128) {      // the fp64 path's register-blocked Jacobi
+        double *Js = reinterpret_cast<double *>(zsm_raw + a.jsm_off);
+        double *jscr = Js + 128 * kLdA;
+        int *jflag = reinterpret_cast<int *>(jscr + 1024);
+        const int mp = (m <= 32) ? 32 : (m <= 64) ? 64 : 128;
+        const int pp = 2 * kWarps * ((p <= 2 * kWarps) ? 1 : (p <= 4 * kWarps) ? 2 : (p <= 8 * kWarps) ? 4 : 8);
+        for (int idx = tid; idx < pp * mp; idx += kThreads) {   // zero-padded, ld kLdA
+          const int j = idx / mp, row = idx % mp;
+          Js[(size_t)j * kLdA + row] = (row < m && j < p) ? (double)A[(size_t)j * m + row] : 0.0;
+        }
+        __syncthreads();
+        sweeps = jacobi_dispatch<kWarps>(Js, m, p, jflag, jscr, a.eps > 1e-14);
+        for (int idx = tid; idx < p * m; idx += kThreads) {
+          const int j = idx / m, row = idx % m;
+          A[idx] = Js[(size_t)j * kLdA + row];
+        }
+        __syncthreads();
+      }
+    }
+    if (sweeps < 0) sweeps = jacobi<S>(A, m, p, a.eps > 1e-14 ? DBL_EPSILON * DBL_EPSILON : 0.0, red);
     for (int j = tid >> 5; j < p; j += kWarps) {
       double sq = 0.0;
       for (int i = tid & 31; i < m; i += 32) sq += abs2(A[(size_t)j * m + i]);
@@ -747,21 +771,25 @@ qtt_status_t member_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trai
   a.cycles = cycles;
   a.window = window;
   QTT_CUDA_TRY(cudaMemsetAsync(io.status, 0, sizeof(int32_t), s));
-  const size_t smem = (size_t)(4 * tn + gn + std::max(pmax, 64)) * elem;
-  a.smem = smem <= 200 * 1024 ? 1 : 0;
+  size_t smem = (size_t)(4 * tn + gn + std::max(pmax, 64)) * elem;
+  const size_t jbytes = complex_dt ? 0 : (size_t)(128 * kLdA + 1024 + 8) * sizeof(double);
+  a.jreg = complex_dt ? 0 : 1;
+  a.smem = (smem + jbytes <= 200 * 1024) ? 1 : 0;     // + ~17 KB static (cta_gemm staging)
+  a.jsm_off = a.smem ? (long long)((smem + 15) & ~size_t(15)) : 0;
+  smem = (a.smem ? (size_t)a.jsm_off : 0) + jbytes;
   static bool attr_c = false, attr_r = false;
   if (complex_dt) {
     if (a.smem && !attr_c) {
       QTT_CUDA_TRY(cudaFuncSetAttribute(cplx::k_zipup<cplx::Z>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr_c = true;
     }
-    cplx::k_zipup<cplx::Z><<<S.B, kThreads, a.smem ? smem : 0, s>>>(a);
+    cplx::k_zipup<cplx::Z><<<S.B, kThreads, smem, s>>>(a);
   } else {
-    if (a.smem && !attr_r) {
+    if (!attr_r) {
       QTT_CUDA_TRY(cudaFuncSetAttribute(cplx::k_zipup<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr_r = true;
     }
-    cplx::k_zipup<double><<<S.B, kThreads, a.smem ? smem : 0, s>>>(a);
+    cplx::k_zipup<double><<<S.B, kThreads, smem, s>>>(a);
   }
   QTT_CUDA_TRY(cudaGetLastError());
   return QTT_OK;
