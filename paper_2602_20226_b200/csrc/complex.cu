@@ -29,6 +29,7 @@
 
 #include "common.cuh"
 #include "jacobi.cuh"
+#include "qr_small.cuh"
 #include "large.cuh"
 
 namespace qtt {
@@ -463,8 +464,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup(Args a) {
   const int b = blockIdx.x, tid = threadIdx.x, L = a.L, L1 = L + 1;
   __shared__ double red[kWarps];
   __shared__ double s_sc[4];
-  __shared__ double gsm[sizeof(S) == sizeof(double) ? 2 * 16 * 64 : 1];   // cta_gemm staging (real)
   extern __shared__ __align__(16) unsigned char zsm_raw[];
+  // real scalars (a.jreg): dynamic shared memory = [Rp (packed R; also the cta_gemm staging and
+  // the Jacobi scratch, never live at the same time)] [Bk / Jacobi matrix, 128 x kLdA] [Ysm] [tau]
+  double *Rp = reinterpret_cast<double *>(zsm_raw + a.jsm_off);
+  double *Bk = Rp + kRpDoubles, *Ysm = Bk + kSmall * kLdA, *tauq = Ysm + 16 * kYld;
+  double *gsm = Rp;
   S *zsm = reinterpret_cast<S *>(zsm_raw);
   S *w0 = static_cast<S *>(a.ws) + (size_t)b * a.ws_member;
   S *Xo = w0, *Oo = Xo + a.xo_n, *G = Oo + a.oo_n, *T = G + a.g_n, *H = T + a.t_n, *Q = H + a.t_n,
@@ -538,7 +543,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup(Args a) {
     // ---- a3: A (m x p, column-major, ld m)
     int p;
     S *A = Q;                                     // reuse: Q is free between a1 and here
-    if (m <= n) {
+    bool in_js = false;                           // real: A = R^T already in the Jacobi matrix Bk
+    if constexpr (sizeof(S) == sizeof(double)) {
+      if (a.jreg && m <= n && m <= kSmall) {      // the fp64 path's blocked QR (qr_small.cuh)
+        p = m;
+        qr_of_TH(reinterpret_cast<const double *>(T), m, n, Rp, Bk, tauq, Ysm);
+        __syncthreads();
+        const int mp = (m <= 32) ? 32 : (m <= 64) ? 64 : 128;
+        const int pp = 2 * kWarps * ((p <= 2 * kWarps) ? 1 : (p <= 4 * kWarps) ? 2 : (p <= 8 * kWarps) ? 4 : 8);
+        for (int idx = tid; idx < pp * mp; idx += kThreads) {   // A = R^T, zero-padded, ld kLdA
+          const int j = idx / mp, row = idx % mp;
+          Bk[(size_t)j * kLdA + row] = (row < m && j < p && row >= j) ? Rp[rp_idx(j, row, m)] : 0.0;
+        }
+        in_js = true;
+      }
+    }
+    if (in_js) {
+    } else if (m <= n) {
       p = m;
       for (int idx = tid; idx < m * n; idx += kThreads) H[idx] = conj(T[idx]);   // T^H column-major (n x m)
       __syncthreads();
@@ -561,14 +582,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup(Args a) {
     int sweeps = -1;
     if constexpr (sizeof(S) == sizeof(double)) {
       if (a.jreg && m <= 128 && p <= 128) {      // the fp64 path's register-blocked Jacobi
-        double *Js = reinterpret_cast<double *>(zsm_raw + a.jsm_off);
-        double *jscr = Js + 128 * kLdA;
+        double *Js = Bk;
+        double *jscr = Rp;                       // Rp is free once A = R^T sits in Bk
         int *jflag = reinterpret_cast<int *>(jscr + 1024);
-        const int mp = (m <= 32) ? 32 : (m <= 64) ? 64 : 128;
-        const int pp = 2 * kWarps * ((p <= 2 * kWarps) ? 1 : (p <= 4 * kWarps) ? 2 : (p <= 8 * kWarps) ? 4 : 8);
-        for (int idx = tid; idx < pp * mp; idx += kThreads) {   // zero-padded, ld kLdA
-          const int j = idx / mp, row = idx % mp;
-          Js[(size_t)j * kLdA + row] = (row < m && j < p) ? (double)A[(size_t)j * m + row] : 0.0;
+        if (!in_js) {
+          const int mp = (m <= 32) ? 32 : (m <= 64) ? 64 : 128;
+          const int pp = 2 * kWarps * ((p <= 2 * kWarps) ? 1 : (p <= 4 * kWarps) ? 2 : (p <= 8 * kWarps) ? 4 : 8);
+          for (int idx = tid; idx < pp * mp; idx += kThreads) {   // zero-padded, ld kLdA
+            const int j = idx / mp, row = idx % mp;
+            Js[(size_t)j * kLdA + row] = (row < m && j < p) ? (double)A[(size_t)j * m + row] : 0.0;
+          }
         }
         __syncthreads();
         sweeps = jacobi_dispatch<kWarps>(Js, m, p, jflag, jscr, a.eps > 1e-14);
@@ -772,11 +795,17 @@ qtt_status_t member_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trai
   a.window = window;
   QTT_CUDA_TRY(cudaMemsetAsync(io.status, 0, sizeof(int32_t), s));
   size_t smem = (size_t)(4 * tn + gn + std::max(pmax, 64)) * elem;
-  const size_t jbytes = complex_dt ? 0 : (size_t)(128 * kLdA + 1024 + 8) * sizeof(double);
-  a.jreg = complex_dt ? 0 : 1;
-  a.smem = (smem + jbytes <= 200 * 1024) ? 1 : 0;     // + ~17 KB static (cta_gemm staging)
-  a.jsm_off = a.smem ? (long long)((smem + 15) & ~size_t(15)) : 0;
-  smem = (a.smem ? (size_t)a.jsm_off : 0) + jbytes;
+  if (complex_dt) {                     // the member's matrices on chip when they fit
+    a.jreg = 0;
+    a.smem = smem <= 200 * 1024 ? 1 : 0;
+    a.jsm_off = 0;
+    if (!a.smem) smem = 0;
+  } else {                              // real: blocked QR + register Jacobi working set on chip
+    a.jreg = 1;
+    a.smem = 0;
+    a.jsm_off = 0;
+    smem = (size_t)(kRpDoubles + kSmall * kLdA + 16 * kYld + kSmall) * sizeof(double);
+  }
   static bool attr_c = false, attr_r = false;
   if (complex_dt) {
     if (a.smem && !attr_c) {
@@ -786,7 +815,7 @@ qtt_status_t member_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trai
     cplx::k_zipup<cplx::Z><<<S.B, kThreads, smem, s>>>(a);
   } else {
     if (!attr_r) {
-      QTT_CUDA_TRY(cudaFuncSetAttribute(cplx::k_zipup<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      QTT_CUDA_TRY(cudaFuncSetAttribute(cplx::k_zipup<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr_r = true;
     }
     cplx::k_zipup<double><<<S.B, kThreads, smem, s>>>(a);

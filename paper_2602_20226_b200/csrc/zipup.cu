@@ -18,10 +18,9 @@
 #include "jacobi.cuh"
 #include "large.cuh"
 #include "orth.cuh"
+#include "qr_small.cuh"
 
-#ifndef QTT_QR_PANEL
-#define QTT_QR_PANEL 8
-#endif
+
 
 namespace qtt {
 
@@ -41,8 +40,6 @@ qtt_status_t cuda_status(cudaError_t e, const char *what) {
 
 
 constexpr int kMaxSites = 64;
-constexpr int kSmall = 128;            // max rows m (and p) of a site matrix on this path
-constexpr int kRpDoubles = kSmall * (kSmall + 1) / 2;  // packed R / GEMM staging / scratch (8256)
 constexpr int kBkDoubles = kRpDoubles;                  // staged MPO core limit
 constexpr int kSiteSmemDoubles = kRpDoubles + kSmall * kLdA + kSmall + 16 + 8 + kSmall + 16 * 136;
 constexpr size_t kSiteSmemBytes = kSiteSmemDoubles * sizeof(double) + (kSmall + 8) * sizeof(int);
@@ -197,16 +194,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_orth(OrthArgs a) {
 
 // ======================================================================= a2..a7: site step
 
-// Threads per k_sweep CTA (one CTA per SM).  256 (8 warps, <= 255 registers, one block pair
-// of 2 x 8 columns per warp in the Jacobi) measured faster than 512 (16 warps, <= 128
-// registers, 2 x 4 columns): 90.2k vs 102.2k site-steps/s on cfg5 -- the Jacobi round is
-// bound by FP64 and MIO issue, not by latency that more warps could hide.
-#ifndef QTT_SWEEP_THREADS
-#define QTT_SWEEP_THREADS 256
-#endif
-constexpr int kST = QTT_SWEEP_THREADS;
-constexpr int kSW = kST / 32;
-
 struct SweepArgs {
   int L, B, kind, shared_op;
   int d[kMaxSites], dj[kMaxSites];       // output / contracted digit size per site
@@ -230,207 +217,6 @@ struct SweepArgs {
   double eps;
   int max_rank;
 };
-
-// a3: R (m x m upper triangular, packed row-major in Rp) of T^H, T row-major m x n, m <= n.
-// Incremental Householder over row blocks of T^H (kSmall = 128 columns of T per block):
-// QR([R; block]); the reflector of column j touches R[j][j] and the block column only.
-// Blocked by panels of 16 columns: warp 0 factors a panel with the 16 columns x 128 rows in
-// registers (4 rows per lane, warp-wide reductions, no CTA barrier inside the panel); then
-// every thread pair applies the 16 reflectors to one trailing column held in registers.
-// Two CTA barriers per panel; 2 blocks for n = 256.
-constexpr int kPanel = QTT_QR_PANEL;
-constexpr int kPanelSh = 5 - ilog2<kPanel>();   // halve<kPanel>: lane l holds index l >> kPanelSh
-
-__device__ __forceinline__ int rp_idx(int j, int c, int m) { return j * m - (j * (j - 1)) / 2 + (c - j); }
-
-__device__ __forceinline__ void qr_panel(double *Rp, double *Bk, double *tau, int m, int j0) {
-  const int lane = threadIdx.x & 31;
-  double P[kPanel][4];
-#pragma unroll
-  for (int cc = 0; cc < kPanel; ++cc)
-#pragma unroll
-    for (int t = 0; t < 4; ++t) P[cc][t] = (j0 + cc < m) ? Bk[(lane + 32 * t) * kLdA + j0 + cc] : 0.0;
-#pragma unroll
-  for (int jj = 0; jj < kPanel; ++jj) {
-    const int j = j0 + jj;
-    if (j < m) {
-      // one reduce-scatter gives both ||x_j||^2 (index jj) and x_j . x_c for the remaining panel
-      // columns (v_j = scale * x_j below the unit entry, so v_j . x_c = scale * x_j . x_c):
-      // the norm and the dot products share one latency chain
-      double v[kPanel];
-#pragma unroll
-      for (int cc = 0; cc < kPanel; ++cc) {
-        double d = 0.0;
-        if (cc >= jj) {
-#pragma unroll
-          for (int t = 0; t < 4; ++t) d = fma(P[jj][t], P[cc][t], d);
-        }
-        v[cc] = d;
-      }
-      halve<kPanel, 16, kPanel>(v, lane);
-      const double s = __shfl_sync(0xffffffffu, v[0], jj << kPanelSh);
-      double tj, beta, scale;
-      householder_fast(Rp[rp_idx(j, j, m)], s, tj, beta, scale);
-#pragma unroll
-      for (int t = 0; t < 4; ++t) P[jj][t] *= scale;
-      if (lane == 0) { Rp[rp_idx(j, j, m)] = beta; tau[j] = tj; }
-      if (tj != 0.0) {
-#pragma unroll
-        for (int cc = jj + 1; cc < kPanel; ++cc) {
-          const int c = j0 + cc;
-          const double dot = __shfl_sync(0xffffffffu, v[0], cc << kPanelSh);
-          if (c < m) {
-            const double rjc = Rp[rp_idx(j, c, m)];
-            const double w = tj * fma(scale, dot, rjc);
-#pragma unroll
-            for (int t = 0; t < 4; ++t) P[cc][t] = fma(-w, P[jj][t], P[cc][t]);
-            if (lane == 0) Rp[rp_idx(j, c, m)] = rjc - w;
-          }
-        }
-      }
-      __syncwarp();
-    }
-  }
-#pragma unroll
-  for (int cc = 0; cc < kPanel; ++cc)
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-      if (j0 + cc < m) Bk[(lane + 32 * t) * kLdA + j0 + cc] = P[cc][t];
-}
-
-// Trailing update of the panel j0..jn-1 (reflectors v_jj = [e_(j0+jj) on R's row; V_B[:, jj]],
-// V_B = Bk columns j0..jn-1) on the columns c in [jn, m) of [R; B], in compact-WY form without
-// forming T (LAPACK dlarft):  Y = V^T C (DMMA, with G = V_B^T V_B in the same GEMM),
-// Z = tau-forward substitution Z_jj = tau_jj (Y_jj - sum_{i<jj} G_{i,jj} Z_i) (the sequential
-// reflector recurrence, exactly), then R_p -= Z, B -= V_B Z (DMMA).  Equivalent to applying
-// H_(j0) ... H_(jn-1) one after another.
-constexpr int kYld = 136;            // Y/Z row stride (== 8 mod 16: conflict-free fragment loads)
-
-__device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-      : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
-}
-
-// Barrier over the warps [wbeg, wbeg + nw) taking part in a trailing update: the whole CTA,
-// or named barrier 1 when warp 0 is busy factoring the next panel (lookahead).
-__device__ __forceinline__ void wy_sync(int nw) {
-  if (nw == kSW) __syncthreads();
-  else asm volatile("bar.sync 1, %0;" ::"r"(nw * 32) : "memory");
-}
-
-// Update columns [cbeg, cend) of [R; B] with the panel j0..jn-1 (see above).  gram: compute
-// the Gram of the panel (Y columns j0..jn-1) in the same GEMM; otherwise it is already in
-// Ysm from an earlier call for this panel.  Run by warps [wbeg, wbeg + nw) only.
-__device__ void qr_trailing_wy(double *Rp, double *Bk, const double *tau, double *Ysm, int m, int j0, int jn,
-                               int cbeg, int cend, bool gram, int wbeg, int nw) {
-  const int tid = threadIdx.x - wbeg * 32, lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) - wbeg;
-  const int np = jn - j0;                         // reflectors in the panel (<= kPanel)
-  const int gr = lane >> 2, gc = lane & 3;        // mma fragment coordinates
-  // (1) Y (kPanel x cols) = V_B^T Bk[:, cols], cols = [j0, jn) (Gram, if asked) + [cbeg, cend)
-  {
-    const int col0 = gram ? j0 : cbeg;
-    const int ntile = (cend - col0 + 7) >> 3;
-    for (int nt = warp; nt < ntile; nt += nw) {
-      double c[kPanel / 8][2];
-#pragma unroll
-      for (int mt = 0; mt < kPanel / 8; ++mt) c[mt][0] = c[mt][1] = 0.0;
-      const int bcol = col0 + nt * 8 + gr;        // B fragment: column gr, row gc
-      const bool bok = bcol < cend && (bcol < jn || bcol >= cbeg);
-#pragma unroll 4
-      for (int k0 = 0; k0 < kSmall; k0 += 4) {
-        const double *rowp = Bk + (size_t)(k0 + gc) * kLdA;
-        const double b = bok ? rowp[bcol] : 0.0;
-#pragma unroll
-        for (int mt = 0; mt < kPanel / 8; ++mt) {
-          const int ar = mt * 8 + gr;             // A fragment: row gr (reflector), col gc (k)
-          const double av = (ar < np) ? rowp[j0 + ar] : 0.0;
-          dmma884(c[mt][0], c[mt][1], av, b);
-        }
-      }
-#pragma unroll
-      for (int mt = 0; mt < kPanel / 8; ++mt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = col0 + nt * 8 + 2 * gc + e;
-          if (col < cend && (col < jn || col >= cbeg)) Ysm[(mt * 8 + gr) * kYld + col] = c[mt][e];
-        }
-    }
-  }
-  wy_sync(nw);
-  // (2) per updated column: Z = forward substitution; R rows j0..jn-1 updated
-  for (int c = cbeg + tid; c < cend; c += nw * 32) {
-    double z[kPanel];
-#pragma unroll
-    for (int jj = 0; jj < kPanel; ++jj) {
-      z[jj] = 0.0;
-      if (jj < np) {
-        const int j = j0 + jj;
-        double y = Ysm[jj * kYld + c] + Rp[rp_idx(j, c, m)];
-#pragma unroll
-        for (int i = 0; i < jj; ++i) y = fma(-Ysm[i * kYld + j0 + jj], z[i], y);
-        z[jj] = tau[j] * y;
-        Rp[rp_idx(j, c, m)] -= z[jj];
-        Ysm[jj * kYld + c] = z[jj];
-      }
-    }
-  }
-  wy_sync(nw);
-  // (3) B[:, cbeg:cend] -= V_B Z      (tiles of 8 rows x 8 columns, K = np <= kPanel)
-  {
-    const int nct = (cend - cbeg + 7) >> 3;
-    for (int rt = warp; rt < kSmall / 8; rt += nw) {
-      double af[kPanel / 4];                        // -V_B fragments for this row tile
-#pragma unroll
-      for (int ks = 0; ks < kPanel / 4; ++ks) {
-        const int kk = ks * 4 + gc;
-        af[ks] = (kk < np) ? -Bk[(size_t)(rt * 8 + gr) * kLdA + j0 + kk] : 0.0;
-      }
-      for (int ct = 0; ct < nct; ++ct) {
-        const int cb = cbeg + ct * 8;
-        double *crow = Bk + (size_t)(rt * 8 + gr) * kLdA;
-        const int cc0 = cb + 2 * gc;
-        double c0 = (cc0 < cend) ? crow[cc0] : 0.0, c1 = (cc0 + 1 < cend) ? crow[cc0 + 1] : 0.0;
-        const int zc = cb + gr;
-#pragma unroll
-        for (int ks = 0; ks < kPanel / 4; ++ks) {
-          const int kk = ks * 4 + gc;
-          const double zb = (kk < np && zc < cend) ? Ysm[kk * kYld + zc] : 0.0;
-          dmma884(c0, c1, af[ks], zb);
-        }
-        if (cc0 < cend) crow[cc0] = c0;
-        if (cc0 + 1 < cend) crow[cc0 + 1] = c1;
-      }
-    }
-  }
-  wy_sync(nw);
-}
-
-__device__ __noinline__ void qr_of_TH(const double *T, int m, int n, double *Rp, double *Bk, double *tau, double *Ysm) {
-  const int tid = threadIdx.x, warp = tid >> 5;
-  for (int i = tid; i < kRpDoubles; i += kST) Rp[i] = 0.0;
-  for (int c0 = 0; c0 < n; c0 += kSmall) {
-    const int nb = min(kSmall, n - c0);
-    __syncthreads();
-    for (int idx = tid; idx < kSmall * m; idx += kST) {
-      const int j = idx / kSmall, i = idx % kSmall;    // coalesced along i (columns of T)
-      Bk[i * kLdA + j] = (i < nb) ? T[(size_t)j * n + c0 + i] : 0.0;
-    }
-    __syncthreads();
-    // one-panel lookahead: the next panel's columns are updated first (all warps), then
-    // warp 0 factors it while warps 1.. update the remaining columns (named barrier 1)
-    if (warp == 0) qr_panel(Rp, Bk, tau, m, 0);
-    __syncthreads();
-    for (int j0 = 0; j0 < m; j0 += kPanel) {
-      const int jn = min(j0 + kPanel, m);
-      if (jn >= m) break;
-      const int jn2 = min(jn + kPanel, m);
-      qr_trailing_wy(Rp, Bk, tau, Ysm, m, j0, jn, jn, jn2, true, 0, kSW);
-      if (warp == 0) qr_panel(Rp, Bk, tau, m, jn);
-      else if (jn2 < m) qr_trailing_wy(Rp, Bk, tau, Ysm, m, j0, jn, jn2, m, false, 1, kSW - 1);
-      __syncthreads();
-    }
-  }
-}
 
 // a2 for "ij,j->i" on DMMA, fused with the MPO epilogue (no X round trip through global):
 //   X[(c,w),(j,r')] = sum_r G[(c,w),r] x_q[r,(j,r')]     (M = chi*w, K = r, N = dj*r2)
