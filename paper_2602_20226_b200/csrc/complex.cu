@@ -116,6 +116,7 @@ struct Args {
   int window;                          // 1, or 2 (f4)
   int jreg;                            // real: register-blocked Jacobi (jacobi.cuh) in smem at jsm_off
   long long jsm_off;                   // byte offset of that region in dynamic shared memory
+  const int *xr_pre, *orr_pre;         // real: a1 done by k_orth into the member slots ([B][L+1] ranks)
 };
 
 // In-place Householder QR of the column-major rows x cols matrix H (ld = rows), K =
@@ -487,7 +488,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup(Args a) {
 
   // ---- a1
   long long tph = clock64();
-  {
+  if (a.xr_pre) {                                 // done by the fp64 path's k_orth (real scalars)
+    for (int q = tid; q <= L; q += kThreads) {
+      xr[q] = a.xr_pre[(size_t)b * L1 + q];
+      orr[q] = (a.kind == TRUNCATE) ? 1 : a.orr_pre[(size_t)b * L1 + q];
+    }
+    if (a.op_batch == 1 && a.B > 1) Oo = static_cast<S *>(a.ws) + a.xo_n;   // shared operator: member 0's slot
+    __syncthreads();
+  } else {
     int legs[64];
     for (int q = 0; q < L; ++q) legs[q] = a.dj[q];
     orth_operand<S>(a, a.xsrc, a.x_bs, b, legs, a.xr0, a.xoff, Xo, xr, true, H, Q, tau, red);
@@ -747,7 +755,9 @@ size_t member_workspace_bytes(const Shape &S, int elem_bytes, int window) {
   long long zm, im, xo, oo, gn, tn;
   int pmax;
   member_sizes(S, window, zm, im, xo, oo, gn, tn, pmax);
-  return (size_t)S.B * (size_t)zm * elem_bytes + (size_t)S.B * (size_t)im + 256;
+  // + the a1 ranks of the real path's k_orth pre-pass ([B][L+1] for x and for the operator)
+  return (size_t)S.B * (size_t)zm * elem_bytes + (size_t)S.B * (size_t)im + 256 +
+         (elem_bytes == 8 ? 2 * (size_t)S.B * (S.L + 1) * sizeof(int) + 256 : 0);
 }
 
 qtt_status_t member_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags,
@@ -793,6 +803,14 @@ qtt_status_t member_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trai
   a.orth_op = (flags & QTT_NO_OPERATOR_ORTH) ? 0 : 1;
   a.cycles = cycles;
   a.window = window;
+  if (!complex_dt) {                    // a1 by the fp64 path's register-resident k_orth
+    int *ranks_pre = (int *)((char *)workspace + (size_t)S.B * zm * elem + (size_t)S.B * im + 256);
+    a.xr_pre = ranks_pre;
+    a.orr_pre = ranks_pre + (size_t)S.B * (S.L + 1);
+    qtt_status_t st = orth_prepass(S, op, x, flags, (double *)workspace, (double *)workspace + xo, zm,
+                                   (int *)a.xr_pre, (int *)a.orr_pre, s);
+    if (st != QTT_OK) return st;
+  }
   QTT_CUDA_TRY(cudaMemsetAsync(io.status, 0, sizeof(int32_t), s));
   size_t smem = (size_t)(4 * tn + gn + std::max(pmax, 64)) * elem;
   if (complex_dt) {                     // the member's matrices on chip when they fit

@@ -31,6 +31,9 @@ struct LargeIO {
 };
 
 size_t large_workspace_bytes(const Shape &S);
+// the fp64 a1 pre-pass (zipup.cu k_orth) into caller-given member slots (per-member kernel)
+qtt_status_t orth_prepass(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags, double *xdst,
+                          double *odst, long long dst_bs, int *xr_out, int *orr_out, cudaStream_t s);
 // shape analysis of qtt_zipup's operands (zipup.cu), shared with qtt_variational
 qtt_status_t qtt_zipup_analyse(const char *subs, const qtt_trains_t *op, const qtt_trains_t *x, int32_t max_rank,
                                Shape &S);

@@ -763,6 +763,46 @@ static int train_dtypes(const qtt_trains_t *op, const qtt_trains_t *x, const qtt
   return -1;
 }
 
+// a1 of the fp64 path (k_orth, register-resident Householder) for the per-member kernel:
+// member b's orthonormalised x cores go to xdst + b * dst_bs (+ S.xoff[q]), the operator's to
+// odst + b * dst_bs (+ S.ooff[q]; a shared operator only to member 0's slot), ranks to
+// xr_out / orr_out [B][L+1] (a shared operator's ranks are broadcast).
+qtt_status_t orth_prepass(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags, double *xdst,
+                          double *odst, long long dst_bs, int *xr_out, int *orr_out, cudaStream_t s) {
+  QTT_CUDA_TRY(cudaFuncSetAttribute(k_orth, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(kOrthSmemDoubles * sizeof(double))));
+  {
+    OrthArgs oa;
+    memset(&oa, 0, sizeof(oa));
+    oa.L = S.L; oa.orth = 1; oa.shared = 0;
+    for (int q = 0; q < S.L; ++q) { oa.legs[q] = S.dj[q]; oa.src[q] = (const double *)x->cores[q]; oa.off[q] = S.xoff[q]; }
+    for (int q = 0; q <= S.L; ++q) oa.r0[q] = S.xr[q];
+    oa.dst = xdst; oa.dst_bs = dst_bs; oa.rk = xr_out;
+    k_orth<<<S.B, kThreads, kOrthSmemDoubles * sizeof(double), s>>>(oa);
+    QTT_CUDA_TRY(cudaGetLastError());
+  }
+  if (S.kind != TRUNCATE) {
+    OrthArgs oa;
+    memset(&oa, 0, sizeof(oa));
+    oa.L = S.L; oa.orth = (flags & QTT_NO_OPERATOR_ORTH) ? 0 : 1; oa.shared = S.shared_op;
+    for (int q = 0; q < S.L; ++q) {
+      oa.legs[q] = (S.kind == MATVEC) ? S.d[q] * S.dj[q] : S.d[q];
+      oa.src[q] = (const double *)op->cores[q];
+      oa.off[q] = S.ooff[q];
+    }
+    for (int q = 0; q <= S.L; ++q) oa.r0[q] = S.orr[q];
+    oa.dst = odst; oa.dst_bs = dst_bs; oa.rk = orr_out;
+    const int nb = S.shared_op ? 1 : S.B;
+    k_orth<<<nb, kThreads, kOrthSmemDoubles * sizeof(double), s>>>(oa);
+    QTT_CUDA_TRY(cudaGetLastError());
+    if (S.shared_op)
+      for (int b = 1; b < S.B; ++b)
+        QTT_CUDA_TRY(cudaMemcpyAsync(orr_out + (size_t)b * (S.L + 1), orr_out, sizeof(int) * (S.L + 1),
+                                     cudaMemcpyDeviceToDevice, s));
+  }
+  return QTT_OK;
+}
+
 qtt_status_t qtt_zipup_analyse(const char *subs, const qtt_trains_t *op, const qtt_trains_t *x, int32_t max_rank,
                                Shape &S) {
   return analyse(subs, op, x, max_rank, S);
