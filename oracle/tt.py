@@ -74,15 +74,18 @@ def evaluate(cores, digits: np.ndarray) -> np.ndarray:
 
 # ------------------------------------------------------------------------ exact ops
 
-def inner(a, b) -> float:
-    """<a, b> by a left-to-right environment sweep, real case."""
+def inner(a, b):
+    """<a, b> = sum_i conj(a_i) b_i by a left-to-right environment sweep,
+    conjugate-linear in the first argument.  Returns a float for real trains
+    and a complex for complex ones."""
     E = np.ones((1, 1))
     for x, y in zip(a, b):
         rx, ry = x.shape[0], y.shape[0]
-        X = x.reshape(rx, -1, x.shape[-1])
+        X = np.conj(x.reshape(rx, -1, x.shape[-1]))
         Y = y.reshape(ry, -1, y.shape[-1])
         E = np.einsum("ab,aic,bid->cd", E, X, Y)
-    return float(E[0, 0])
+    v = E[0, 0]
+    return complex(v) if np.iscomplexobj(E) else float(v)
 
 
 def add(a, b) -> List[np.ndarray]:
@@ -99,14 +102,15 @@ def add(a, b) -> List[np.ndarray]:
         elif q == L - 1:
             out.append(np.concatenate([A, B], axis=0))
         else:
-            C = np.zeros((A.shape[0] + B.shape[0],) + _legs(A) + (A.shape[-1] + B.shape[-1],))
+            C = np.zeros((A.shape[0] + B.shape[0],) + _legs(A) + (A.shape[-1] + B.shape[-1],),
+                         dtype=np.result_type(A, B))
             C[: A.shape[0], ..., : A.shape[-1]] = A
             C[A.shape[0]:, ..., A.shape[-1]:] = B
             out.append(C)
     return out
 
 
-def scale(a, s: float) -> List[np.ndarray]:
+def scale(a, s) -> List[np.ndarray]:
     out = [c.copy() for c in a]
     out[0] = out[0] * s
     return out

@@ -155,3 +155,112 @@ def test_hadamard_closed_forms_after_rounding():
     c = gen.cos_train(b, 0, h, 3.0, 0).cores
     cc = tt.round_train(tt.exact_hadamard(c, c), 1e-12, 0)
     assert tt.ranks_of(cc)[1:-1] == [min(3, 2 ** q, 2 ** (10 - q)) for q in range(1, 10)]
+
+
+# ---------------------------------------------------------------- multi-dimension digit order
+# to_tensor is row-major over the original dimensions (dimension 0 slowest),
+# the digits of each dimension most significant first.  These pins build trains whose dense
+# value is known in closed form per dimension, so a swapped dimension order, a reversed digit
+# order or a transposed operator fails them.
+
+def _kron_digits(factors):
+    """Dense vector of prod_q f_q(digit_q), digits big-endian: kron(f_0, f_1, ...)."""
+    v = np.ones(1)
+    for f in factors:
+        v = np.kron(v, f)
+    return v
+
+
+def _rank1(vecs):
+    return [np.asarray(f, dtype=float).reshape(1, -1, 1) for f in vecs]
+
+
+def test_dim_order_separable_interleaved_2d():
+    """f(x) g(y) on the alternating layout x1,y1,x2,y2,... (configs[1], c-A19) equals
+    np.outer(f, g).ravel(); f and g are general rank-2/3 trains, the other dimension's bond
+    passing through each core (Kronecker bonds)."""
+    rng = np.random.default_rng(11)
+    Lx = 3
+    F = gen.random_mps([2] * Lx, 2, rng).cores
+    G = gen.random_mps([2] * Lx, 3, rng).cores
+    f, g = tt.to_dense_vector(F), tt.to_dense_vector(G)
+    cores, leg_dim = [], []
+    for q in range(Lx):
+        # x-site: C[(a,b), i, (a',b)] = F_q[a,i,a'] with g's bond b (left bond of G_q) carried
+        rb = G[q].shape[0]
+        cores.append(np.einsum("aic,bd->abicd", F[q], np.eye(rb)).reshape(
+            F[q].shape[0] * rb, 2, F[q].shape[2] * rb))
+        leg_dim.append(0)
+        ra = F[q].shape[2]
+        cores.append(np.einsum("ac,bid->abicd", np.eye(ra), G[q]).reshape(
+            ra * G[q].shape[0], 2, ra * G[q].shape[2]))
+        leg_dim.append(1)
+    got = tt.to_dense_vector(cores, leg_dim)
+    np.testing.assert_allclose(got, np.outer(f, g).ravel(), rtol=1e-13, atol=1e-14)
+    # the swapped order is a different vector (the pin discriminates)
+    assert np.abs(got - np.outer(g, f).ravel()).max() > 1e-3
+
+
+def test_dim_order_three_dims_mixed_radix():
+    """Three dimensions with mixed digit sizes, sites in the order z0, x0, y0, x1, z1
+    (leg_dim = [2, 0, 1, 0, 2]): dense = f(x) (x) g(y) (x) h(z), row-major x slowest."""
+    rng = np.random.default_rng(12)
+    fx = [rng.standard_normal(3), rng.standard_normal(2)]
+    gy = [rng.standard_normal(5)]
+    hz = [rng.standard_normal(2), rng.standard_normal(3)]
+    sites = [hz[0], fx[0], gy[0], fx[1], hz[1]]
+    leg_dim = [2, 0, 1, 0, 2]
+    got = tt.to_dense_vector(_rank1(sites), leg_dim)
+    want = np.kron(np.kron(_kron_digits(fx), _kron_digits(gy)), _kron_digits(hz))
+    np.testing.assert_allclose(got, want, rtol=1e-14, atol=0)
+    # default order (site order) is the plain kron of the sites
+    np.testing.assert_allclose(tt.to_dense_vector(_rank1(sites)), _kron_digits(sites), rtol=1e-14)
+
+
+def test_dim_order_operator_kron():
+    """A separable MPO A(x) (x) B(y) on the alternating layout densifies to np.kron(A, B)
+    (rows: out indices, row-major x slowest; columns likewise)."""
+    rng = np.random.default_rng(13)
+    Ax = [rng.standard_normal((2, 2)) for _ in range(2)]
+    By = [rng.standard_normal((3, 3)) for _ in range(2)]
+    cores = [Ax[0], By[0], Ax[1], By[1]]
+    mpo = [c.reshape(1, *c.shape, 1) for c in cores]
+    A = np.kron(Ax[0], Ax[1])
+    B = np.kron(By[0], By[1])
+    np.testing.assert_allclose(tt.to_dense_matrix(mpo, [0, 1, 0, 1]), np.kron(A, B), rtol=1e-14)
+    np.testing.assert_allclose(tt.to_dense_matrix(mpo), np.kron(np.kron(Ax[0], By[0]),
+                                                                np.kron(Ax[1], By[1])), rtol=1e-14)
+
+
+# ---------------------------------------------------------------- complex trains
+# The oracle takes complex128 since f2 (PAPER.md:533-566); addition (PAPER.md:196-209) and the
+# inner product (SPEC.md:241-249, conjugate-linear in the first argument, SPEC.md:244) must
+# keep imaginary parts.
+
+def _crnd(dims, R, seed):
+    rng = np.random.default_rng(seed)
+    re = gen.random_mps(dims, R, rng).cores
+    im = gen.random_mps(dims, R, rng).cores
+    return [a + 1j * b for a, b in zip(re, im)]
+
+
+def test_complex_add_inner_diff_norm():
+    a, b = _crnd([2, 3, 2, 2, 3], 3, 21), _crnd([2, 3, 2, 2, 3], 2, 22)
+    va, vb = tt.to_dense_vector(a), tt.to_dense_vector(b)
+    s = tt.add(a, b)
+    assert all(np.iscomplexobj(c) for c in s)
+    np.testing.assert_allclose(tt.to_dense_vector(s), va + vb, rtol=1e-13, atol=1e-13)
+    ip = tt.inner(a, b)
+    assert isinstance(ip, complex)
+    assert abs(ip - np.vdot(va, vb)) <= 1e-12 * np.linalg.norm(va) * np.linalg.norm(vb)
+    # conjugate-linear in the first argument: <i a, b> = -i <a, b>
+    ia = tt.scale(a, 1j)
+    assert abs(tt.inner(ia, b) - (-1j) * ip) <= 1e-12 * abs(ip)
+    assert abs(tt.inner(a, a).imag) <= 1e-12 * abs(tt.inner(a, a))
+    dn = tt.diff_norm(a, b)
+    assert abs(dn - np.linalg.norm(va - vb)) <= 1e-12 * np.linalg.norm(va - vb)
+    # a train differing from a only by an imaginary perturbation is at that distance
+    c = [x.copy() for x in a]
+    c[2] = c[2] + 1e-3j * np.ones_like(c[2])
+    vc = tt.to_dense_vector(c)
+    assert abs(tt.diff_norm(a, c) - np.linalg.norm(va - vc)) <= 1e-10 * np.linalg.norm(va - vc)
