@@ -762,7 +762,7 @@ size_t member_workspace_bytes(const Shape &S, int elem_bytes, int window) {
 
 qtt_status_t member_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags,
                           const LargeIO &io, void *workspace, size_t workspace_bytes, cudaStream_t s,
-                          long long *cycles, bool complex_dt, int window) {
+                          long long *cycles, bool complex_dt, int window, void *const *events) {
   if (S.L > 64) { set_error("per-member path: n_sites > 64"); return QTT_EUNSUPPORTED; }
   const int elem = complex_dt ? 16 : 8;
   const size_t need = member_workspace_bytes(S, elem, window);
@@ -803,7 +803,10 @@ qtt_status_t member_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trai
   a.orth_op = (flags & QTT_NO_OPERATOR_ORTH) ? 0 : 1;
   a.cycles = cycles;
   a.window = window;
-  if (!complex_dt) {                    // a1 by the fp64 path's register-resident k_orth
+  // a1 by the fp64 path's register-resident k_orth when every core fits its shared-memory
+  // staging budget; otherwise (bonds wider than k_orth stages) the kernel's own global-memory
+  // orth_operand runs (xr_pre stays NULL)
+  if (!complex_dt && a1_fits(S, false)) {
     int *ranks_pre = (int *)((char *)workspace + (size_t)S.B * zm * elem + (size_t)S.B * im + 256);
     a.xr_pre = ranks_pre;
     a.orr_pre = ranks_pre + (size_t)S.B * (S.L + 1);
@@ -811,7 +814,10 @@ qtt_status_t member_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trai
                                    (int *)a.xr_pre, (int *)a.orr_pre, s);
     if (st != QTT_OK) return st;
   }
+  // diag events: [0] before a1 (caller), [1] after the a1 pre-pass, [2] before k_zipup, [3] after (caller)
+  if (events) QTT_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[1], s));
   QTT_CUDA_TRY(cudaMemsetAsync(io.status, 0, sizeof(int32_t), s));
+  if (events) QTT_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[2], s));
   size_t smem = (size_t)(4 * tn + gn + std::max(pmax, 64)) * elem;
   if (complex_dt) {                     // the member's matrices on chip when they fit
     a.jreg = 0;
@@ -824,18 +830,12 @@ qtt_status_t member_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trai
     a.jsm_off = 0;
     smem = (size_t)(kRpDoubles + kSmall * kLdA + 16 * kYld + kSmall) * sizeof(double);
   }
-  static bool attr_c = false, attr_r = false;
-  if (complex_dt) {
-    if (a.smem && !attr_c) {
+  if (complex_dt) {       // dynamic-smem opt-in every call (per-device attribute; thread-safe)
+    if (a.smem)
       QTT_CUDA_TRY(cudaFuncSetAttribute(cplx::k_zipup<cplx::Z>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr_c = true;
-    }
     cplx::k_zipup<cplx::Z><<<S.B, kThreads, smem, s>>>(a);
   } else {
-    if (!attr_r) {
-      QTT_CUDA_TRY(cudaFuncSetAttribute(cplx::k_zipup<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_r = true;
-    }
+    QTT_CUDA_TRY(cudaFuncSetAttribute(cplx::k_zipup<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cplx::k_zipup<double><<<S.B, kThreads, smem, s>>>(a);
   }
   QTT_CUDA_TRY(cudaGetLastError());

@@ -999,8 +999,7 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
   Bf.ver = (int *)(ws + P.off_ver);
   Bf.sweeps_scratch = (int *)(ws + P.off_sw); Bf.bar = (GridBar *)(ws + P.off_bar);
   Bf.dims = (SiteDims *)(ws + P.off_dims); Bf.spec = (GemmSpec *)(ws + P.off_spec);
-  static bool attr = false;
-  if (!attr) {
+  {  // dynamic-smem opt-in on the current device, every call (per-device setting; cheap, thread-safe)
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_qr_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_jacobi_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1011,7 +1010,6 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
                                       (int)tf32g::SMEM_BYTES));
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_tf32<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)tf32g::SMEM_BYTES));
-    attr = true;
   }
   QTT_CUDA_TRY(cudaMemsetAsync(Bf.bar, 0, sizeof(GridBar) * 2, s));
   k_site0_init<<<1, 32, 0, s>>>(Bf.G, io.yr);

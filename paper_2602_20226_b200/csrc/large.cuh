@@ -40,9 +40,10 @@ qtt_status_t qtt_zipup_analyse(const char *subs, const qtt_trains_t *op, const q
 // per-member path (complex.cu): one CTA per member, every step; complex128 trains (f2) and
 // the window-2 zip-up (f4, real or complex)
 size_t member_workspace_bytes(const Shape &S, int elem_bytes, int window);
+bool a1_fits(const Shape &S, bool report);
 qtt_status_t member_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags,
                           const struct LargeIO &io, void *workspace, size_t workspace_bytes, cudaStream_t s,
-                          long long *cycles, bool complex_dt, int window);
+                          long long *cycles, bool complex_dt, int window, void *const *events);
 qtt_status_t large_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags,
                          const LargeIO &io, void *workspace, size_t workspace_bytes, cudaStream_t s);
 

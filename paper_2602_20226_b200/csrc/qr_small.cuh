@@ -24,6 +24,9 @@ constexpr int kRpDoubles = kSmall * (kSmall + 1) / 2;  // packed R / GEMM stagin
 #endif
 constexpr int kST = QTT_SWEEP_THREADS;
 constexpr int kSW = kST / 32;
+// qr_of_TH strides by kST and waits on named barriers sized for kST threads: every kernel that
+// calls it must run kST threads (k_sweep, and k_zipup<double> with kThreads)
+static_assert(kST == kThreads, "qr_small.cuh assumes QTT_SWEEP_THREADS == kThreads");
 
 // a3: R (m x m upper triangular, packed row-major in Rp) of T^H, T row-major m x n, m <= n.
 // Incremental Householder over row blocks of T^H (kSmall = 128 columns of T per block):

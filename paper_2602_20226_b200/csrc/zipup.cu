@@ -117,6 +117,12 @@ __device__ void smem_org2r(double *Ms, int c, int k, const double *tau) {
   }
 }
 
+// a shared operator's ranks (row 0 of a [B][n] int array) broadcast to every member's row
+__global__ void k_bcast_row(int *rows, int n, int B) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n && i < n * B) rows[i] = rows[i % n];
+}
+
 __global__ void __launch_bounds__(kThreads, 1) k_orth(OrthArgs a) {
   extern __shared__ double smem[];
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -641,6 +647,7 @@ static qtt_status_t analyse(const char *subs, const qtt_trains_t *op, const qtt_
 }
 
 static qtt_status_t check_small_path(const Shape &S) {
+  auto a1_ok = [&](void) { return a1_fits(S, true) ? QTT_OK : QTT_EUNSUPPORTED; };
   for (int q = 0; q < S.L; ++q) {
     const long long m = (long long)S.cap[q] * S.d[q];
     if (m > kSmall) {
@@ -652,7 +659,13 @@ static qtt_status_t check_small_path(const Shape &S) {
       return QTT_EUNSUPPORTED;
     }
   }
-  // a1 staging budget for both operands
+  return a1_ok();
+}
+
+// a1 staging budget of k_orth's shared-memory QR for both operands (x, and the operator unless
+// truncating): false when some core's (c x r) block + R + the previous core exceed
+// kOrthSmemDoubles or r > 2 kSmall.  report: set the thread-local error message.
+bool a1_fits(const Shape &S, bool report) {
   for (int pass = 0; pass < 2; ++pass) {
     const std::vector<int> &rk = pass == 0 ? S.xr : S.orr;
     if (pass == 1 && S.kind == TRUNCATE) break;
@@ -663,13 +676,14 @@ static qtt_status_t check_small_path(const Shape &S) {
       const long long c = (long long)legs * rr, r = rk[q], k = std::min<long long>(c, r);
       const long long need = 2 * kSmall + 16 + c * r + k * r + (long long)rk[q - 1] * legsp * r;
       if (need > kOrthSmemDoubles || r > 2 * kSmall) {
-        set_error("a1: core %d of operand %d too large for the shared-memory QR (%lld doubles)", q, pass, need);
-        return QTT_EUNSUPPORTED;
+        if (report)
+          set_error("a1: core %d of operand %d too large for the shared-memory QR (%lld doubles)", q, pass, need);
+        return false;
       }
       rr = (int)k;
     }
   }
-  return QTT_OK;
+  return true;
 }
 
 struct WsLayout {
@@ -795,10 +809,10 @@ qtt_status_t orth_prepass(const Shape &S, const qtt_trains_t *op, const qtt_trai
     const int nb = S.shared_op ? 1 : S.B;
     k_orth<<<nb, kThreads, kOrthSmemDoubles * sizeof(double), s>>>(oa);
     QTT_CUDA_TRY(cudaGetLastError());
-    if (S.shared_op)
-      for (int b = 1; b < S.B; ++b)
-        QTT_CUDA_TRY(cudaMemcpyAsync(orr_out + (size_t)b * (S.L + 1), orr_out, sizeof(int) * (S.L + 1),
-                                     cudaMemcpyDeviceToDevice, s));
+    if (S.shared_op && S.B > 1) {
+      k_bcast_row<<<(S.B * (S.L + 1) + 255) / 256, 256, 0, s>>>(orr_out, S.L + 1, S.B);
+      QTT_CUDA_TRY(cudaGetLastError());
+    }
   }
   return QTT_OK;
 }
@@ -922,10 +936,10 @@ qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt
   const bool cdt = train_dtypes(op, x, out) == 2;
   if (cdt || (flags & QTT_WINDOW2)) {      // complex128 (Fourier chain, f2) / window 2 (f4)
     g_err[0] = 0;
-    if (events) for (int i = 0; i < 3; ++i) QTT_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[i], s));
+    if (events) QTT_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[0], s));
     LargeIO io{out, out_ranks, delta2, norm2, sigma, sigma_stride, sweeps, status, eps, max_rank};
     qtt_status_t cst = member_zipup(S, op, x, flags, io, workspace, workspace_bytes, s, cycles, cdt,
-                                    (flags & QTT_WINDOW2) ? 2 : 1);
+                                    (flags & QTT_WINDOW2) ? 2 : 1, events);
     if (cst != QTT_OK) return cst;
     if (events) QTT_CUDA_TRY(cudaEventRecord((cudaEvent_t)events[3], s));
     return QTT_OK;
@@ -953,13 +967,11 @@ qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt
   double *T = (double *)(ws + W.t), *Xb = (double *)(ws + W.x);
   int *xr = (int *)(ws + W.xr), *orr = (int *)(ws + W.orr);
 
-  static bool attr_done = false;
-  if (!attr_done) {
-    QTT_CUDA_TRY(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSiteSmemBytes));
-    QTT_CUDA_TRY(cudaFuncSetAttribute(k_orth, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(kOrthSmemDoubles * sizeof(double))));
-    attr_done = true;
-  }
+  // dynamic-smem opt-in on the current device, every call: the attribute is per device and the
+  // call is cheap and thread-safe (qtt.h promises reentrant calls from any thread / device)
+  QTT_CUDA_TRY(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSiteSmemBytes));
+  QTT_CUDA_TRY(cudaFuncSetAttribute(k_orth, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(kOrthSmemDoubles * sizeof(double))));
   QTT_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), s));
 
   auto record = [&](int i) -> cudaError_t {
@@ -992,10 +1004,9 @@ qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt
     const int nb = S.shared_op ? 1 : S.B;
     k_orth<<<nb, kThreads, kOrthSmemDoubles * sizeof(double), s>>>(oa);
     QTT_CUDA_TRY(cudaGetLastError());
-    if (S.shared_op) {
-      for (int b = 1; b < S.B; ++b)
-        QTT_CUDA_TRY(cudaMemcpyAsync(orr + (size_t)b * (S.L + 1), orr, sizeof(int) * (S.L + 1),
-                                     cudaMemcpyDeviceToDevice, s));
+    if (S.shared_op && S.B > 1) {
+      k_bcast_row<<<(S.B * (S.L + 1) + 255) / 256, 256, 0, s>>>(orr, S.L + 1, S.B);
+      QTT_CUDA_TRY(cudaGetLastError());
     }
   } else {
     QTT_CUDA_TRY(cudaMemsetAsync(orr, 0, sizeof(int) * (S.L + 1) * S.B, s));

@@ -78,3 +78,13 @@ def test_window2_cfg5_members_and_accuracy(lib):
         ex = tt.exact_matvec(p.op.cores, p.x.cores)
         e2, e1 = tt.diff_norm(y2, ex), tt.diff_norm(y1, ex)
         assert e2 <= 1.05 * e1 + 1e-12 * tt.qr_norm(ex), (e2, e1)
+
+
+def test_window2_wide_bonds(lib):
+    """Bonds of 128 (x) exceed k_orth's shared-memory staging budget: the real window-2 path must
+    fall back to its global-memory a1 instead of overrunning shared memory."""
+    x = gen.random_mps([2] * 14, 128, np.random.default_rng(71), 1 / math.sqrt(128)).cores
+    op = gen.random_mpo([2] * 14, 3, np.random.default_rng(72), 0.5).cores
+    assert max(c.shape[0] for c in x) == 128
+    check_w2(lib, "matvec", op, x, 1e-8, 40, dense=False)
+    check_w2(lib, "truncate", None, x, 1e-3, 24, dense=False)
