@@ -45,7 +45,14 @@ def parse():
                          "12 complex Hadamard zip-ups (SURVEY.md §8(f) f2); variational: one sweep of "
                          "qtt_variational (f3) on cfg5 members seeded by a max-rank-16 zip-up")
     ap.add_argument("--members-per-gpu", type=int, default=512)
-    ap.add_argument("--cpu-members", type=int, default=8, help="oracle sample size (members) for cpu_baseline")
+    ap.add_argument("--strong", action="store_true",
+                    help="cfg5 strong scaling: --global-members (4096) split over the N ranks (dist.strong_range) "
+                         "instead of --members-per-gpu per rank (weak scaling, the default)")
+    ap.add_argument("--global-members", type=int, default=4096)
+    ap.add_argument("--cpu-members", type=int, default=64,
+                    help="cfg5 oracle sample size (members b = stride*t of this rank's shard) for cpu_baseline")
+    ap.add_argument("--cpu-budget-s", type=float, default=30.0,
+                    help="cfg1-4 cpu_baseline: stop the oracle zip-up after this many seconds (bounded sample)")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
                     help="f32: the fp32 variant (binary32 cores; large-path contractions as 3xTF32 on tcgen05)")
     ap.add_argument("--window", type=int, default=1, choices=[1, 2],
@@ -60,15 +67,20 @@ def parse():
 def build_workload(args, rank):
     """Returns (subscripts, kind, problems (list of gen.Problem for this rank), x_stack, op_stack, cfg dict)."""
     if args.workload == "cfg5":
-        M = args.members_per_gpu
-        lo, hi = qdist.member_range(rank, args.gpus, M)
+        if args.strong:
+            lo, hi = qdist.strong_range(rank, args.gpus, args.global_members)
+            gb = args.global_members
+        else:
+            lo, hi = qdist.member_range(rank, args.gpus, args.members_per_gpu)
+            gb = args.members_per_gpu * args.gpus
         members = list(range(lo, hi))
         probs, xs, ops = gen.cfg5_batch_arrays(members)
-        p0 = probs[0]
         cfg = {"workload": "configs[4] cfg5: batch of independent zip-ups, L=40 d=2, state rank 64 N(0,1/64), "
                            "random rank-4 MPO N(0,1/4), max rank 64, eps 1e-10",
-               "members_per_gpu": M, "global_batch": M * args.gpus, "L": 40, "rank": 64, "mpo_rank": 4,
-               "max_rank": 64, "eps": 1e-10, "parallelism": f"dp{args.gpus} (members sharded, 1 all-reduce/step)"}
+               "members_per_gpu": hi - lo, "global_batch": gb, "L": 40, "rank": 64, "mpo_rank": 4,
+               "max_rank": 64, "eps": 1e-10,
+               "parallelism": f"dp{args.gpus} (members sharded, 1 all-reduce/step, "
+                              f"{'strong: fixed global batch' if args.strong else 'weak: fixed members per GPU'})"}
         return "ij,j->i", "matvec", probs, xs, ops, cfg
     mk = {"cfg1": lambda: gen.cfg1(), "cfg2": lambda: gen.cfg2(), "cfg3": lambda: gen.cfg3(),
           "cfg4": lambda: gen.cfg4()}[args.workload]
@@ -230,33 +242,133 @@ def dram_traffic(workload, members):
 
 # ----------------------------------------------------------------------------- CPU oracle leg
 
-def oracle_sample(kind, probs, n_members, window=1):
-    """Time the oracle, as it stands, on the host cores over a bounded sample."""
-    from oracle.zipup import zipup as ozip1, zipup_window
-    ozip = ozip1 if window == 1 else (lambda *a_: zipup_window(*a_, window=window))
+def _blas_threads():
     try:
         from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"] or [1])
+        return max([i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"] or [1])
     except Exception:
-        cores = os.cpu_count()
-    n = min(n_members, len(probs))
+        return None
+
+
+def _cpu_member(job):
+    """Pool worker (spawned, BLAS threads = 1): regenerate cfg5 member b from its seed and run
+    the oracle zip-up on it, as it stands.  Returns (b, ranks, cores, seconds)."""
+    b, window = job
+    from oracle.zipup import zipup as ozip1, zipup_window
+    p = gen.cfg5_member(b)
     t0 = time.perf_counter()
-    results = []
-    for p in probs[:n]:
-        results.append(ozip(kind, None if p.op is None else p.op.cores, p.x.cores, p.eps, p.max_rank))
+    if window == 1:
+        r = ozip1(p.kind, p.op.cores, p.x.cores, p.eps, p.max_rank)
+    else:
+        r = zipup_window(p.kind, p.op.cores, p.x.cores, p.eps, p.max_rank, window=window)
+    return b, r["ranks"], r["cores"], time.perf_counter() - t0
+
+
+def _pool_init():
+    pass
+
+
+def cpu_baseline_cfg5(members, n_sample, window=1):
+    """SURVEY.md §8(d) (line 666): the oracle, as it stands, over a deterministic member sample
+    b = stride*t of this rank's shard, run by a multiprocessing pool of cpu_count workers with
+    BLAS threads = 1 (one member per worker at a time).  The rate (site-steps/s) of the sample
+    is the baseline; the full workload's oracle time is that rate's extrapolation (stated)."""
+    import multiprocessing as mp
+    n = max(1, min(n_sample, len(members)))
+    stride = max(1, len(members) // n)
+    sample = [members[stride * t] for t in range(n)]
+    ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    keys = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS", "BLIS_NUM_THREADS")
+    saved = {k: os.environ.get(k) for k in keys}
+    for k in keys:
+        os.environ[k] = "1"                      # inherited by the spawned workers only
+    try:
+        ctx = mp.get_context("spawn")
+        with ctx.Pool(ncores, initializer=_pool_init) as pool:
+            pool.map(abs, range(ncores))         # start every worker before the clock
+            t0 = time.perf_counter()
+            out = pool.map(_cpu_member, [(b, window) for b in sample], chunksize=1)
+            dt = time.perf_counter() - t0
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    L = len(out[0][2])
+    steps = n * L
+    cpu_s = sum(o[3] for o in out)
+    full = len(members) * L / (steps / dt)
+    info = {"value": round(steps / dt, 3), "unit": UNIT, "cores": ncores, "kind": "oracle",
+            "sample": f"{n} members b = {stride}*t (t < {n}) of the workload's {len(members)}, x {L} sites; "
+                      f"multiprocessing pool of {ncores} workers, BLAS threads 1 (SURVEY.md §8(d)); "
+                      f"{dt:.1f} s wall, {cpu_s:.1f} core-s; NumPy fp64 + LAPACK gesdd; "
+                      f"extrapolated oracle time for all {len(members)} members: {full:.0f} s"}
+    return info, {b: (rk, cores) for b, rk, cores, _ in out}
+
+
+class _Budget(Exception):
+    pass
+
+
+def cpu_baseline_single(p, budget_s, window=1):
+    """cfg1-4: one oracle zip-up with BLAS threads = host cores, stopped after
+    budget_s seconds at a site boundary (bounded sample).  Returns (info, result or None)."""
+    from oracle.zipup import zipup as ozip1, zipup_window
+    L = len(p.x.cores)
+    done = [0]
+    t0 = time.perf_counter()
+
+    def on_site(q):
+        done[0] = q + 1
+        if time.perf_counter() - t0 > budget_s:
+            raise _Budget()
+
+    res = None
+    try:
+        if window == 1:
+            res = ozip1(p.kind, None if p.op is None else p.op.cores, p.x.cores, p.eps, p.max_rank, on_site=on_site)
+            done[0] = L
+        else:
+            res = zipup_window(p.kind, None if p.op is None else p.op.cores, p.x.cores, p.eps, p.max_rank,
+                               window=window)
+            done[0] = L
+    except _Budget:
+        res = None
     dt = time.perf_counter() - t0
-    steps = sum(len(p.x.cores) for p in probs[:n])
-    return {"value": steps / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{n} members x {len(probs[0].x.cores)} sites of this rank's workload, {dt:.1f} s wall, "
-                      f"NumPy fp64 + LAPACK gesdd (host {os.cpu_count()} cores)"}, results
+    whole = done[0] == L
+    info = {"value": round(done[0] / dt, 4), "unit": UNIT, "cores": _blas_threads() or os.cpu_count(),
+            "kind": "oracle",
+            "sample": (f"one full zip-up ({L} sites), {dt:.1f} s wall" if whole else
+                       f"sites 0..{done[0] - 1} of {L} (stopped at the {budget_s:.0f} s budget; the early sites are "
+                       f"the small ones, so this rate is an upper bound on the oracle's), {dt:.1f} s wall")
+                      + f"; one process, NumPy fp64 + LAPACK gesdd, BLAS threads {_blas_threads()}"}
+    return info, res
 
 
 # ----------------------------------------------------------------------------- main
 
+def self_launch(args):
+    """`bench.py --gpus N` outside torchrun: re-exec this command under torch.distributed.run with
+    N ranks (one process per GPU, rendezvous on 127.0.0.1), so the line measures N GPUs."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    print("bench.py: launching " + " ".join(cmd), file=sys.stderr, flush=True)
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1:
+    if world != args.gpus:
+        if args.gpus != 1:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
         args.gpus = world
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -348,14 +460,24 @@ def main():
         f = site_flops(kind, list(ranks[b]), xd.ranks, od.ranks if od is not None else None, d, dj, sweeps[b],
                        args.window)
         tot += np.sum(np.array(f), axis=0)
-    flops_alg = tot[0] + tot[1] + tot[2]
-    flops_all = flops_alg + tot[3]
+    flops_alg = tot[0] + tot[1] + tot[2]          # contract + QR + carry, Jacobi excluded
     site_s = site_ms * 1e-3 / args.steps
     fp64_peak = max(peaks["dfma_tflops"], peaks["dmma_tflops"])
-    achieved = flops_all / site_s / 1e12
+    achieved = flops_alg / site_s / 1e12
+    jac_share = phase_share["a4_jacobi"] if phase_share else None
+    jacobi = {"flops_executed_per_step": tot[3], "sweeps_mean": float(sweeps[:, :-1].mean()),
+              "sweeps_max": int(sweeps.max()),
+              "note": "sweep-dependent work, excluded from the algorithmic rate (SURVEY.md §8(d))"}
+    if jac_share:
+        jt = site_s * jac_share
+        jacobi.update({"time_share_of_kernel": jac_share, "ms_per_step": round(jt * 1e3, 3),
+                       "fp64_tflops_executed": round(tot[3] / jt / 1e12, 3),
+                       "fp64_frac_executed": round(tot[3] / jt / 1e12 / fp64_peak, 4)})
     launches_per_step = 3 + (1 if kind != "truncate" else 0)   # a1 (x[, op]), k_sweep, summary
     if args.window == 2:
-        launches_per_step = 2                                    # k_zipup<double>, summary
+        launches_per_step = 3 + (1 if kind != "truncate" else 0)   # a1 (x[, op]), k_zipup<double>, summary
+    if od is not None and getattr(od, "batch", B) == 1 and B > 1:
+        launches_per_step += 1                                    # shared operator: rank broadcast
 
     units = world * B * L
     value = units / (ms_max * 1e-3)
@@ -416,42 +538,62 @@ def main():
     cpu = None
     parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu, refs = oracle_sample(kind, probs, args.cpu_members, args.window)
         from oracle import tt
-        worst = 0.0
-        for b, ref in enumerate(refs):
-            rk = [int(v) for v in ranks[b]]
-            if rk != ref["ranks"]:
-                worst = float("inf")
-                break
-            yg = qtt.member_cores(plan.out, rk, b)
-            worst = max(worst, tt.diff_norm(yg, ref["cores"]) / tt.qr_norm(ref["cores"]))
-        parity = {"members": len(refs), "max_rel_fro": worst, "ranks_equal": worst != float("inf")}
+        worst, n_cmp, ranks_equal = 0.0, 0, True
+        if args.workload == "cfg5":
+            members = [int(pp.meta["member"]) for pp in probs]
+            cpu, refs = cpu_baseline_cfg5(members, args.cpu_members, args.window)
+            for b, (rk_ref, cores_ref) in refs.items():
+                i = members.index(b)
+                rk = [int(v) for v in ranks[i]]
+                if rk != rk_ref:
+                    ranks_equal = False
+                    continue
+                yg = qtt.member_cores(plan.out, rk, i)
+                worst = max(worst, tt.diff_norm(yg, cores_ref) / tt.qr_norm(cores_ref))
+                n_cmp += 1
+        else:
+            cpu, ref = cpu_baseline_single(probs[0], args.cpu_budget_s, args.window)
+            if ref is not None:
+                rk = [int(v) for v in ranks[0]]
+                ranks_equal = rk == ref["ranks"]
+                if ranks_equal:
+                    yg = qtt.member_cores(plan.out, rk, 0)
+                    worst = tt.diff_norm(yg, ref["cores"]) / tt.qr_norm(ref["cores"])
+                    n_cmp = 1
+        parity = {"members": n_cmp, "max_rel_fro": worst, "ranks_equal": ranks_equal,
+                  "how": "QR-sweep norm of the exact difference train / QR-sweep norm of the oracle's (c-A29)"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": round(ms_max, 3), "higher_is_better": True,
-            "scaling": "weak" if args.workload == "cfg5" else "replicas", "vs_baseline": None, "dtype": args.dtype,
+            "scaling": ("strong" if args.strong else "weak") if args.workload == "cfg5" else "replicas",
+            "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (seeded generators, BASELINE.json configs)",
             "config": dict(cfg, l2="inputs %.2f GB/GPU%s" % (
                 sum(c.numel() * c.element_size() for c in xd.cores) / 1e9,
                 " > 126 MB L2: no flush needed" if args.workload == "cfg5" else
                 " (single zip-up; its per-site scratch exceeds L2 for cfg3/cfg4)")),
             "alg_tflops": round(world * flops_alg / (ms_max * 1e-3) / 1e12, 3),
-            "alg_tflops_note": "contraction+QR+carry flops (SURVEY.md §8(d)); Jacobi excluded",
-            "roofline": {"kernel": ("k_sweep (persistent a2-a7 over all sites and members; Jacobi-dominated)"
+            "alg_tflops_note": "whole step: contraction+QR+carry flops (SURVEY.md §8(d)) / ms_per_step; Jacobi excluded",
+            "roofline": {"kernel": (("k_sweep (persistent a2-a7 over all sites and members)" if B * L > 0 and
+                                     args.workload in ("cfg1", "cfg5") else
+                                     "large-member path (per site: k_gemm_dmma, k_qr_coop, k_jacobi_coop, k_finish)")
                                     if args.window == 1 else "k_zipup<double> (window 2: one CTA per member, every step)"),
                          "bound": "fp64",
-                         "achieved": round(achieved, 3), "peak": fp64_peak, "unit": "TFLOP/s",
+                         "achieved": round(achieved, 4), "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": round(achieved / fp64_peak, 4), "traffic": traffic,
-                         "peak_source": "measured in this run by csrc/probe/peak.cu (MEASURED_PEAKS.json has no FP64)",
-                         "flops_per_step": flops_all, "kernel_ms_per_step": round(site_ms / args.steps, 3),
+                         "achieved_def": "SURVEY.md §8(d) algorithmic flops of the launch (sum over sites and members "
+                                         "of F_contract + F_qr + F_carry; Jacobi excluded) / the launch's CUDA-event time",
+                         "peak_source": "FP64 (DMMA/DFMA) measured in this run by csrc/probe/peak.cu "
+                                        "(MEASURED_PEAKS.json has no FP64 entry)",
+                         "alg_flops_per_step": flops_alg, "kernel_ms_per_step": round(site_ms / args.steps, 3),
                          "share_of_step": round(site_ms / args.steps / ms, 4),
-                         "flop_split": {"contract": tot[0], "qr": tot[1], "carry": tot[2], "jacobi": tot[3]},
+                         "flop_split": {"contract": tot[0], "qr": tot[1], "carry": tot[2]},
                          "prepass_ms_per_step": round(orth_ms / args.steps, 3)},
+            "jacobi": jacobi,
             "fp64_peaks": peaks, "site_kernel_phase_share": phase_share,
-            "jacobi_sweeps": {"mean": float(sweeps[:, :-1].mean()), "max": int(sweeps.max())},
             "cpu_baseline": cpu, "parity_sample": parity, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "clocks": clk,
             "summary": qdist.summary_dict(summary.cpu().tolist()),
@@ -716,38 +858,40 @@ def run_qft_reference(args, rank):
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle (as it stands) on the host cores, same workload/metric."""
+    """--impl reference: the CPU oracle (as it stands) on the host cores, on this arm's config,
+    metric and unit.  Each step is a bounded sample of the workload: cfg5 -- one member per host
+    core (members b = stride*t of rank 0's shard), a spawned pool with BLAS threads 1 (SURVEY.md
+    §8(d)); cfg1-4 -- one oracle zip-up stopped at a per-step time budget.  Rank 0 only."""
     if rank != 0:
         return
-    # the line carries the GPU arm's config (full workload); each step times a bounded sample
-    # of it (the first members of rank 0's shard), described in cpu_baseline.sample
-    full_members = args.members_per_gpu
-    args.members_per_gpu = max(1, args.cpu_members // 4) if args.workload == "cfg5" else 1
     subs, kind, probs, xs, ops, cfg = build_workload(args, 0)
-    if args.workload == "cfg5":
-        cfg = dict(cfg, members_per_gpu=full_members, global_batch=full_members * max(world, 1),
-                   parallelism=f"dp{max(world, 1)} (members sharded, 1 all-reduce/step)")
     if args.window == 2:
         cfg = dict(cfg, window=2)
-    for _ in range(args.warmup):
-        oracle_sample(kind, probs, 1, args.window)
-    vals = []
-    t0 = time.perf_counter()
-    info = None
-    for _ in range(args.steps):
-        info, _ = oracle_sample(kind, probs, len(probs), args.window)
-        vals.append(info["value"])
+    ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    vals, info = [], None
+    budget = max(2.0, min(args.cpu_budget_s, 150.0 / max(1, args.steps + args.warmup)))
+    t0 = None
+    for it in range(args.warmup + args.steps):
+        if it == args.warmup:
+            t0 = time.perf_counter()
+        if args.workload == "cfg5":
+            members = [int(pp.meta["member"]) for pp in probs]
+            info, _ = cpu_baseline_cfg5(members, ncores, args.window)
+        else:
+            info, _ = cpu_baseline_single(probs[0], budget, args.window)
+        if it >= args.warmup:
+            vals.append(info["value"])
     dt = time.perf_counter() - t0
     value = statistics.median(vals)
-    L = len(probs[0].x.cores)
-    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
-            "scaling": "weak" if args.workload == "cfg5" else "replicas", "vs_baseline": None, "dtype": "f64",
+            "scaling": ("strong" if args.strong else "weak") if args.workload == "cfg5" else "replicas",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, BASELINE.json configs)", "impl": "reference",
             "config": cfg,
-            "cpu_baseline": dict(info, value=round(value, 3),
-                                 sample=f"each step: {len(probs)} members x {L} sites of the workload (oracle)"),
-            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": dict(info, value=round(value, 4),
+                                 sample="each step: " + info["sample"] + f"; median of {args.steps} steps"),
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 

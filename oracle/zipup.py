@@ -48,8 +48,11 @@ def site_matrix(kind: str, G: np.ndarray, Xq: np.ndarray, Oq: Optional[np.ndarra
 
 
 def zipup(kind: str, op: Optional[Sequence[np.ndarray]], x: Sequence[np.ndarray], eps: float,
-          max_rank: int, orth_operator: bool = True, force_ranks: Optional[Sequence[int]] = None):
-    """Returns a dict with
+          max_rank: int, orth_operator: bool = True, force_ranks: Optional[Sequence[int]] = None,
+          on_site=None):
+    """on_site(q): optional progress hook called after site q is finished (instrumentation
+    only -- bench.py's bounded CPU baseline stops a long run by raising from it).
+    Returns a dict with
       cores   : output cores C_q (chi_q, d_q, chi_{q+1})
       ranks   : [1, chi_1, ..., chi_{L-1}, 1]
       delta2  : discarded sum of squares per split (L-1 values)
@@ -97,6 +100,8 @@ def zipup(kind: str, op: Optional[Sequence[np.ndarray]], x: Sequence[np.ndarray]
         cores.append(U[:, :k].reshape(chi, d, k))                                 # step 4
         G = (sig[:k, None] * Vh[:k]).reshape(k, v, s)
         ranks.append(k)
+        if on_site is not None:
+            on_site(q)
     norm = float(np.linalg.norm(cores[-1]))
     return {"cores": cores, "ranks": ranks, "delta2": delta2, "sigmas": sigmas, "norm": norm}
 

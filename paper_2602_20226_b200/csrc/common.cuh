@@ -12,6 +12,13 @@ namespace qtt {
 
 constexpr int kThreads = 256;     // CTA size of every per-member kernel (8 warps)
 constexpr int kWarps = kThreads / 32;
+// c-A31: Jacobi may leave columns of squared norm <= eps_mach^2 ||A||_F^2 unrotated
+// only when the truncation discards them for certain: their total mass p eps_mach^2 ||A||_F^2
+// must stay below the rule's budget eps^2 ||A||_F^2, i.e. eps^2 > p eps_mach^2 (and eps > 1e-14,
+// the threshold the rule was measured with).  p: the matrix's column count (or an upper bound).
+__host__ __device__ __forceinline__ bool noise_ok(double eps, int p) {
+  return eps > 1e-14 && eps * eps > (double)p * (DBL_EPSILON * DBL_EPSILON);
+}
 constexpr int kLdA = 129;         // leading dim of the shared R / Jacobi matrix (odd: no bank conflicts)
 
 void set_error(const char *fmt, ...);

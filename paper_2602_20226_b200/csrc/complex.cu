@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup(Args a) {
           }
         }
         __syncthreads();
-        sweeps = jacobi_dispatch<kWarps>(Js, m, p, jflag, jscr, a.eps > 1e-14);
+        sweeps = jacobi_dispatch<kWarps>(Js, m, p, jflag, jscr, noise_ok(a.eps, p));
         for (int idx = tid; idx < p * m; idx += kThreads) {
           const int j = idx / m, row = idx % m;
           A[idx] = Js[(size_t)j * kLdA + row];
@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup(Args a) {
         __syncthreads();
       }
     }
-    if (sweeps < 0) sweeps = jacobi<S>(A, m, p, a.eps > 1e-14 ? DBL_EPSILON * DBL_EPSILON : 0.0, red);
+    if (sweeps < 0) sweeps = jacobi<S>(A, m, p, noise_ok(a.eps, p) ? DBL_EPSILON * DBL_EPSILON : 0.0, red);
     for (int j = tid >> 5; j < p; j += kWarps) {
       double sq = 0.0;
       for (int i = tid & 31; i < m; i += 32) sq += abs2(A[(size_t)j * m + i]);

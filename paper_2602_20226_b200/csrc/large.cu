@@ -1059,7 +1059,7 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
     {
       JacArgs ja;
       ja.dims = Bf.dims; ja.A = Bf.A; ja.bar = Bf.bar + 1; ja.flags = Bf.flags; ja.ver = Bf.ver; ja.part = Bf.part; ja.nrm = Bf.s2; ja.G = P.Gjac; ja.WB = P.WB;
-      ja.noise_ok = io.eps > 1e-14;
+      ja.noise_ok = noise_ok(io.eps, P.pcap);
       ja.sweeps_out = io.sweeps ? io.sweeps + q : Bf.sweeps_scratch; ja.status = io.status;
       QTT_CUDA_TRY(cudaMemsetAsync(Bf.flags, 0, sizeof(int) * 3, s));
       QTT_CUDA_TRY(cudaMemsetAsync(Bf.ver, 0, sizeof(int) * (P.pcap + 2), s));

@@ -446,7 +446,7 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
     }
     __syncthreads();
   }
-  const int sweeps = jacobi_dispatch<kSW>(Rs, m, p, iflag, Bk, a.eps > 1e-14);   // Bk: per-warp norm scratch
+  const int sweeps = jacobi_dispatch<kSW>(Rs, m, p, iflag, Bk, noise_ok(a.eps, p));   // Bk: per-warp norm scratch
   if (tid == 0 && a.cycles) a.cycles[((size_t)b * L + q) * 4 + 2] = clock64() - t_phase;
   t_phase = clock64();
   const int lane = tid & 31, warp = tid >> 5;
