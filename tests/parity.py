@@ -5,7 +5,8 @@ Gauge-invariant comparisons only (SVD signs are arbitrary, c-A8):
      is re-run with the GPU ranks forced;
   2. per-site singular values |s_G - s_O| <= stol * s_1 for j <= min(p, k+4);
   3. discarded mass delta2_q and ||y|| agree relative to ||T_q||^2 and ||y||;
-  4. rel_fro(Y_G, Y_O) <= 1e-10 + eps (fp64), dense when small, else QR-sweep distance.
+  4. rel_fro(Y_G, Y_O) <= 1e-10 + eps (fp64), dense when small, else QR-sweep distance;
+  5. four seeded rank-8 probe trains Z: |<Z,Y_G> - <Z,Y_O>| <= tol ||Z|| ||Y_O||.
 """
 from __future__ import annotations
 
@@ -38,16 +39,26 @@ def fragile(sig: np.ndarray, k: int, eps: float, max_rank: int, u: float = U64) 
     return False
 
 
+def probe_trains(x_cores, n=4, rank=8, seed=2602):
+    """Protocol item 5: seeded rank-8 probe trains Z on the digit sizes of the result."""
+    from paper_2602_20226_b200 import gen
+    dims = [int(c.shape[1]) for c in x_cores]
+    return [gen.random_mps(dims, rank, np.random.default_rng([seed, i])).cores for i in range(n)]
+
+
 def compare(kind, op_cores, x_cores, eps, max_rank, gpu_cores, gpu_ranks, gpu_sigma, gpu_delta2, gpu_norm2,
-            rel_tol=1e-10, sig_tol=1e-12, dense=True, orth_operator=True, u=U64, window=1):
+            rel_tol=1e-10, sig_tol=1e-12, dense=True, orth_operator=True, u=U64, window=1, ref=None,
+            probes=True):
     """Returns a dict of measured errors; raises AssertionError on a protocol violation.
-    window: the zip-up super-core size the GPU ran with (1, or 2 for QTT_WINDOW2)."""
+    window: the zip-up super-core size the GPU ran with (1, or 2 for QTT_WINDOW2).
+    ref: the oracle's result for these inputs when already computed (tests/oracle_cache.py)."""
     def oracle_zipup(*args, **kw):
         if window == 1:
             return oracle_zipup_w1(*args, **kw)
         return zipup_window(*args, window=window, **kw)
 
-    ref = oracle_zipup(kind, op_cores, x_cores, eps, max_rank, orth_operator=orth_operator)
+    if ref is None:
+        ref = oracle_zipup(kind, op_cores, x_cores, eps, max_rank, orth_operator=orth_operator)
     L = len(x_cores)
     if list(gpu_ranks) != ref["ranks"]:
         for q in range(L - 1):
@@ -91,5 +102,14 @@ def compare(kind, op_cores, x_cores, eps, max_rank, gpu_cores, gpu_ranks, gpu_si
         rel = tt.diff_norm(gpu_cores, ref["cores"]) / max(tt.qr_norm(ref["cores"]), 1e-300)
     assert rel <= rel_tol + eps, f"rel_fro {rel:.3e} > {rel_tol + eps:.1e}"
     out["rel_fro"] = rel
+    # 5. seeded probe inner products |<Z, Y_G> - <Z, Y_O>| <= tol ||Z|| ||Y_O||
+    if probes:
+        worst_p = 0.0
+        for Z in probe_trains(ref["cores"]):
+            zn = tt.qr_norm(Z)
+            dv = abs(tt.inner(Z, gpu_cores) - tt.inner(Z, ref["cores"])) / max(zn * ny, 1e-300)
+            worst_p = max(worst_p, dv)
+        assert worst_p <= rel_tol + eps, f"probe inner products differ by {worst_p:.3e}"
+        out["probe_err"] = worst_p
     out["ref"] = ref
     return out

@@ -82,3 +82,22 @@ def test_f32_cfg3_full_shape_known_answer(lib):
     dig = np.random.default_rng(9).integers(0, 2, size=(4096, L))
     ya, yy = tt.evaluate(a, dig), tt.evaluate(y, dig)
     assert np.sqrt(np.mean((ya - yy) ** 2) / np.mean(ya ** 2)) <= 1e-4
+
+
+@pytest.mark.slow
+def test_f32_cfg3_full_oracle_parity(lib):
+    """configs[2] fp32 variant at full size: binary32 inputs (the fp64 draws rounded), against the
+    fp64 oracle on the same rounded inputs at rel_fro <= 1e-4 + eps, sigma within 1e-5 s_1,
+    fragility with the fp32 unit roundoff (c-A32).  Oracle result from
+    tests/golden/cache/cfg3_f32.npz (scripts/make_oracle_golden.py) or computed."""
+    from oracle_cache import oracle_result
+    p = gen.cfg3()
+    op, x = f32(p.op.cores), f32(p.x.cores)
+    ref = oracle_result("cfg3_f32", "hadamard", op, x, p.eps, p.max_rank)
+    res = run32(lib, "hadamard", op, x, p.eps, p.max_rank)
+    ranks = res.ranks[0].cpu().tolist()
+    cores = lib.member_cores(res.out, ranks, 0)
+    out = compare("hadamard", op, x, p.eps, p.max_rank, cores, ranks, res.sigma[0].cpu().numpy(),
+                  res.delta2[0].cpu().numpy(), float(res.norm2[0].item()), rel_tol=1e-4, sig_tol=1e-5,
+                  dense=False, u=U32, ref=ref)
+    print("cfg3 fp32 full:", {k: v for k, v in out.items() if k != "ref"})

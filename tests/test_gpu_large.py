@@ -122,3 +122,22 @@ def test_large_extreme_magnitudes(lib, scale):
     x = list(p.x.cores)
     x[0] = x[0] * scale
     check(lib, "matvec", p.op.cores, x, p.eps, p.max_rank)
+
+
+@pytest.mark.slow
+def test_cfg3_full_oracle_parity(lib):
+    """configs[2] at full size against the oracle by the whole §8(c) protocol (ranks, sigma to
+    1e-12 s_1 for j <= k+4, delta^2, QR-sweep rel_fro <= 1e-10 + eps, probe inner products):
+    two random rank-256 trains, L = 30, T of 512 x 65536 at the middle sites, p = 512 in
+    k_jacobi_coop, heavy truncation (every bond cut from 65536 columns to 256).  The oracle's
+    result (about 5-10 CPU minutes) comes from tests/golden/cache/cfg3_f64.npz when
+    scripts/make_oracle_golden.py has written it for these exact inputs, else it is computed."""
+    from oracle_cache import oracle_result
+    p = gen.cfg3()
+    ref = oracle_result("cfg3_f64", "hadamard", p.op.cores, p.x.cores, p.eps, p.max_rank)
+    res = run_gpu(lib, "hadamard", p.op.cores, p.x.cores, p.eps, p.max_rank, sigma_stride=512)
+    cores, ranks, sig, d2, n2 = member(lib, res)
+    out = compare("hadamard", p.op.cores, p.x.cores, p.eps, p.max_rank, cores, ranks, sig, d2, n2,
+                  dense=False, ref=ref)
+    assert max(ranks) == 256
+    print("cfg3 full:", {k: v for k, v in out.items() if k != "ref"})

@@ -12,12 +12,12 @@ from parity import compare
 pytestmark = pytest.mark.gpu
 
 
-def run_gpu(lib, kind, op, x, eps, max_rank, mpo_op=True, flags=0):
+def run_gpu(lib, kind, op, x, eps, max_rank, mpo_op=True, flags=0, sigma_stride=256):
     import torch
     subs = {"matvec": "ij,j->i", "hadamard": "i,i->i", "truncate": "i->i"}[kind]
     xd = lib.to_device(x)
     od = None if op is None else lib.to_device(op, mpo=(kind == "matvec"))
-    plan = lib.ZipupPlan(subs, od, xd, eps, max_rank, flags=flags, sigma_stride=256)
+    plan = lib.ZipupPlan(subs, od, xd, eps, max_rank, flags=flags, sigma_stride=sigma_stride)
     res = plan.run(od, xd)
     torch.cuda.synchronize()
     assert int(res.status.item()) == 0, f"device status {int(res.status.item())}"
