@@ -197,6 +197,35 @@ qtt_status_t qtt_variational(const char *subscripts, const qtt_trains_t *op, con
                              const qtt_trains_t *c, int32_t *c_ranks, int32_t sweeps, double *center_norm2,
                              int32_t *status, void *workspace, size_t workspace_bytes, void *stream);
 
+/* qtt_variational_ex -- the same refinement with multi-core super-cores (PAPER.md:300:
+ * "By fusing multiple adjacent C(i_q) into a super-core ... it is possible to realize multi-core
+ * strategies, which normally leads to better convergence and an efficient way of controlling
+ * the ranks"; the paper's call variational(max_rank=8, cutoff=0.0, ncores=2, nsweeps=2),
+ * PAPER.md:794; reading c-A37).
+ *   seed, seed_ranks : the starting train (device int32 [B*(L+1)] ranks); read completely
+ *                before anything is written, so it may alias c / c_ranks.
+ *   c, c_ranks : output slots (capacities c->ranks >= seed->ranks; with ncores = 2 the bond
+ *                ranks adapt up to min(max_rank, capacity)), final ranks written to c_ranks;
+ *                on return the centre is at site 0 (cores 1..L-1 right-orthonormal).
+ *   ncores     : 1 (as qtt_variational) or 2: the super-core of sites (q, q+1),
+ *                S = Le[q] W_q x_q W_{q+1} x_{q+1} Re[q+2], is split by Householder QR + one-sided
+ *                Jacobi and truncated by the zip-up's rule (SPEC.md:299 with eps = cutoff,
+ *                k <= max_rank (<= 0: unbounded), k <= capacity); a sweep updates the pairs
+ *                q = 0..L-2 (centre moving right) then L-2..0 (an LQ moves it left).
+ *   center_norm2 : device f64 [B * sweeps * 2L]; ncores = 2 writes 2(L-1) values per sweep,
+ *                the kept |S_k|^2 = sum_{j<=k} s_j^2 of each split.
+ *   workspace  : >= qtt_variational_workspace_bytes_ex(subscripts, op, x, c, ncores) bytes.
+ * Errors: QTT_ECAPACITY (capacity below the seed's ranks or workspace), QTT_ESHAPE, QTT_EINVAL
+ * (eps outside [0,1), sweeps < 1, ncores = 2 with one site), QTT_EUNSUPPORTED (ncores not 1/2,
+ * non-f64 trains).  status bit 1 = non-finite value, bit 2 = Jacobi did not converge. */
+size_t qtt_variational_workspace_bytes_ex(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                                          const qtt_trains_t *c, int32_t ncores);
+qtt_status_t qtt_variational_ex(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                                const qtt_trains_t *seed, const int32_t *seed_ranks, const qtt_trains_t *c,
+                                int32_t *c_ranks, int32_t sweeps, int32_t ncores, double eps, int32_t max_rank,
+                                double *center_norm2, int32_t *status, void *workspace, size_t workspace_bytes,
+                                void *stream);
+
 /* qtt_zipup_summary -- the per-batch scalars that are all-reduced across GPUs
  * (SURVEY.md §8(a) a8): summary4 (device f64 [4]) = [sum_b sum_q delta2, sum_b norm2,
  * sum_b sum_q out_ranks[b][q+1] (q < L-1), B].  Deterministic fixed-order sums. */

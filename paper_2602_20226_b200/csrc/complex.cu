@@ -856,19 +856,25 @@ namespace cplx {
 
 struct VarArgs {
   int L, B, kind, op_batch, sweeps;
+  int ncores, max_rank;               // 1: single-site; 2: two-site super-cores (reading c-A37)
+  double eps;                         // two-site split truncation (SPEC.md:299 rule, eps = cutoff)
   int d[64], dj[64], xr[65], orr[65], cap[65];
   const double *x[64];
   const double *op[64];
   long long x_bs[64], o_bs[64];
+  const double *sd[64];               // seed slots (may alias c)
+  long long sd_bs[64];
+  const int *sd_ranks;                // device [B][L+1] the seed's ranks
   double *c[64];
   long long c_bs[64];
-  int *c_ranks;                       // device [B][L+1] (in: the seed's ranks; out: after the sweeps)
+  int *c_ranks;                       // device [B][L+1] out: ranks after the sweeps
   double *norms;                      // device [B][sweeps * 2L]
   int *status;
   double *ws;
   long long ws_member;
   long long coff[65], eoff[65];       // per-member offsets: C slots (capacity), environments
   long long e_n, s_n;                 // environment region (each of Le, Re) and scratch sizes
+  int pmax;                           // >= every split's min(m, n) and row count
 };
 
 // W[w, i, j, w'] of the operator (Hadamard: A[w, i, w'] on i == j; truncate: identity)
@@ -950,16 +956,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_variational(VarArgs a) {
   __shared__ double red[kWarps];
   __shared__ double gsm[2 * 16 * 64];            // cta_gemm staging
   __shared__ int cr[65];
+  __shared__ double s_k[2];
   double *w0 = a.ws + (size_t)b * a.ws_member;
   double *Cw = w0, *Le = Cw + a.coff[L], *Re = Le + a.e_n, *S1 = Re + a.e_n, *S2 = S1 + a.s_n, *S3 = S2 + a.s_n,
-         *tau = S3 + a.s_n;
+         *S4 = S3 + a.s_n, *S5 = S4 + a.s_n, *tau = S5 + a.s_n, *sg = tau + a.pmax;
+  int *perm = reinterpret_cast<int *>(sg + a.pmax);
   const int ob = (a.op_batch == 1) ? 0 : b;
-  for (int q = tid; q <= L; q += kThreads) cr[q] = a.c_ranks[(size_t)b * (L + 1) + q];
+  for (int q = tid; q <= L; q += kThreads) cr[q] = a.sd_ranks[(size_t)b * (L + 1) + q];
   __syncthreads();
-  // the seed into the workspace, packed at its ranks
+  // the seed into the workspace, packed at its ranks (read completely before c is written:
+  // the seed may alias the output slots)
   for (int q = 0; q < L; ++q) {
     const long long n = (long long)cr[q] * a.d[q] * cr[q + 1];
-    const double *src = a.c[q] + (size_t)b * a.c_bs[q];
+    const double *src = a.sd[q] + (size_t)b * a.sd_bs[q];
     for (long long i = tid; i < n; i += kThreads) Cw[a.coff[q] + i] = src[i];
   }
   __syncthreads();
@@ -1039,7 +1048,136 @@ __global__ void __launch_bounds__(kThreads, 1) k_variational(VarArgs a) {
     ++cnt;
     __syncthreads();
   };
-  for (int sw = 0; sw < a.sweeps; ++sw) {
+  // ---- two-site super-cores (ncores = 2, reading c-A37)
+  // split(q): S[(c, i), (i', a)] = Le[q] W_q x_q W_{q+1} x_{q+1} Re[q+2] (into S1, row-major
+  // m x n), SVD by Householder QR + one-sided Jacobi (as the zip-up's a3/a4), truncation by the
+  // SPEC.md:299 rule (eps, max_rank, output capacity); C_q <- U_k, C_{q+1} <- U_k^T S =
+  // diag(s_k) V_k^T (the centre sits at q+1).  Records |S_k|^2 = sum_{j<=k} s_j^2.
+  auto split = [&](int q) {
+    // X2[(c, i), (w', r')] from Le[q]  (S2; S1 scratch)
+    env_apply_left(a, q, cr[q], Le + a.eoff[q], Xq(q), Oq(q), S1, S2, gsm);
+    // Z[(c, i), i', (w'', r'')] = site q+1 absorbed with X2 as its left environment  (S3; S4 scratch)
+    const int rc = cr[q] * a.d[q];
+    env_apply_left(a, q + 1, rc, S2, Xq(q + 1), Oq(q + 1), S4, S3, gsm);
+    const int w3 = (a.kind == TRUNCATE) ? 1 : a.orr[q + 2], r3 = a.xr[q + 2], a3 = cr[q + 2], d1 = a.d[q + 1];
+    {  // M[(c, i, i'), a''] = sum_{(w'', r'')} Z[(c, i, i'), (w'', r'')] Re[q+2][a'', (w'', r'')]   (S1)
+      const int K = w3 * r3;
+      const double *R2 = Re + a.eoff[q + 2];
+      cta_gemm<kThreads>(rc * d1, a3, K, [&](int i, int k) { return S3[(size_t)i * K + k]; },
+                         [&](int k, int j) { return R2[(size_t)j * K + k]; },
+                         [&](int i, int j, double v) { S1[(size_t)i * a3 + j] = v; }, gsm);
+    }
+    __syncthreads();
+    const int m = rc, n = d1 * a3;
+    int p;
+    double *A = S4;                              // m x p, column-major
+    if (m <= n) {                                // R of M^T: M = R^T Q^T, A = R^T (lower triangular)
+      p = m;
+      for (int idx = tid; idx < m * n; idx += kThreads) S5[idx] = S1[idx];   // M^T column-major (n x m)
+      __syncthreads();
+      house_qr<double>(S5, n, m, tau, red);
+      for (int idx = tid; idx < m * m; idx += kThreads) {
+        const int j = idx / m, i = idx % m;
+        A[idx] = (i >= j) ? S5[j + (size_t)i * n] : 0.0;
+      }
+    } else {
+      p = n;
+      for (int idx = tid; idx < m * n; idx += kThreads) {
+        const int j = idx / m, i = idx % m;
+        A[idx] = S1[(size_t)i * n + j];
+      }
+    }
+    __syncthreads();
+    const int sweeps_done = jacobi<double>(A, m, p, noise_ok(a.eps, p) ? DBL_EPSILON * DBL_EPSILON : 0.0, red);
+    for (int j = tid >> 5; j < p; j += kWarps) {
+      double sq = 0.0;
+      for (int i = tid & 31; i < m; i += 32) sq = fma(A[(size_t)j * m + i], A[(size_t)j * m + i], sq);
+      sq = warp_sum(sq);
+      if ((tid & 31) == 0) sg[j] = isfinite(sq) ? sq : 0.0;
+      if ((tid & 31) == 0 && !isfinite(sq)) atomicOr(a.status, 1);
+    }
+    __syncthreads();
+    for (int j = tid; j < p; j += kThreads) {
+      const double sj = sg[j];
+      int rank = 0;
+      for (int l = 0; l < p; ++l) rank += (sg[l] > sj) || (sg[l] == sj && l < j);
+      perm[rank] = j;
+    }
+    __syncthreads();
+    if (tid == 0) {                              // SPEC.md:299, tails summed smallest first
+      double acc = 0.0;
+      for (int jj = p - 1; jj >= 0; --jj) acc += sg[perm[jj]];
+      const double tot = acc, thr = a.eps * a.eps * tot;
+      int k = p;
+      double tl = 0.0;
+      for (int kk = p - 1; kk >= 1; --kk) {      // tail[kk] = sum_{j >= kk} (sorted)
+        tl += sg[perm[kk]];
+        if (tl <= thr) k = kk;
+      }
+      if (a.max_rank > 0) k = min(k, a.max_rank);
+      k = min(k, a.cap[q + 1]);
+      if (tot == 0.0) k = 1;
+      k = max(k, 1);
+      double kept = 0.0;
+      for (int jj = 0; jj < k; ++jj) kept += sg[perm[jj]];
+      s_k[0] = (double)k;
+      s_k[1] = kept;
+      if (sweeps_done >= kMaxSweeps) atomicOr(a.status, 2);
+    }
+    __syncthreads();
+    const int k = (int)s_k[0];
+    // U columns normalised (a zero column -> e_kk, as the zip-up's a6)
+    for (int idx = tid; idx < k * m; idx += kThreads) {
+      const int kk = idx / m, i = idx % m, j = perm[kk];
+      const double s2 = sg[j];
+      A[(size_t)j * m + i] = (s2 > 0.0) ? A[(size_t)j * m + i] / sqrt(s2) : ((i == kk) ? 1.0 : 0.0);
+    }
+    __syncthreads();
+    double *Cq0 = Cw + a.coff[q], *Cq1 = Cw + a.coff[q + 1];
+    for (int idx = tid; idx < m * k; idx += kThreads) {
+      const int i = idx / k, kk = idx % k;
+      Cq0[idx] = A[(size_t)perm[kk] * m + i];
+    }
+    // C_{q+1}[kk, (i', a'')] = sum_i U[i, kk] M[i, (i', a'')]
+    cta_gemm<kThreads>(k, n, m, [&](int kk, int i) { return A[(size_t)perm[kk] * m + i]; },
+                       [&](int i, int col) { return S1[(size_t)i * n + col]; },
+                       [&](int kk, int col, double v) { Cq1[(size_t)kk * n + col] = v; }, gsm);
+    if (tid == 0) {
+      cr[q + 1] = k;
+      a.norms[(size_t)b * a.sweeps * 2 * L + cnt] = s_k[1];
+      if (!isfinite(s_k[1])) atomicOr(a.status, 1);
+    }
+    ++cnt;
+    __syncthreads();
+  };
+  // Le[q+1][c', (w', r')] = sum_{(c, i)} C_q[(c, i), c'] X2[(c, i), (w', r')]   (C_q left-orthonormal)
+  auto left_env = [&](int q) {
+    env_apply_left(a, q, cr[q], Le + a.eoff[q], Xq(q), Oq(q), S1, S2, gsm);
+    const int w2 = (a.kind == TRUNCATE) ? 1 : a.orr[q + 1], r2 = a.xr[q + 1], k = cr[q + 1];
+    const int rows = cr[q] * a.d[q];
+    const double *C = Cw + a.coff[q];
+    double *L1 = Le + a.eoff[q + 1];
+    const int N = w2 * r2;
+    cta_gemm<kThreads>(k, N, rows, [&](int i, int kk) { return C[(size_t)kk * k + i]; },
+                       [&](int kk, int j) { return S2[(size_t)kk * N + j]; },
+                       [&](int i, int j, double v) { L1[(size_t)i * N + j] = v; }, gsm);
+    __syncthreads();
+  };
+  if (a.ncores == 2) {
+    for (int sw = 0; sw < a.sweeps; ++sw) {
+      for (int q = 0; q < L - 1; ++q) {           // to the right: the centre moves to q+1
+        split(q);
+        left_env(q);
+      }
+      for (int q = L - 2; q >= 0; --q) {          // and back: C_{q+1} <- V_k^T by LQ, centre at q
+        split(q);
+        move_left(q + 1);
+        env_right(a, q + 1, cr[q + 1], cr[q + 2], Cw + a.coff[q + 1], Re + a.eoff[q + 2], Xq(q + 1), Oq(q + 1), S1,
+                  S2, Re + a.eoff[q + 1], gsm);
+      }
+    }
+  }
+  for (int sw = 0; sw < (a.ncores == 2 ? 0 : a.sweeps); ++sw) {
     for (int q = 0; q < L; ++q) {                 // to the right
       update(q);
       if (q == L - 1) break;
@@ -1074,8 +1212,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_variational(VarArgs a) {
 
 }  // namespace cplx
 
-static void var_sizes(const Shape &S, const qtt_trains_t *c, long long &member, long long *coff, long long *eoff,
-                      long long &e_n, long long &s_n, int &pmax) {
+static void var_sizes(const Shape &S, const qtt_trains_t *c, int ncores, long long &member, long long *coff,
+                      long long *eoff, long long &e_n, long long &s_n, int &pmax) {
   const int L = S.L;
   coff[0] = 0;
   eoff[0] = 0;
@@ -1092,9 +1230,18 @@ static void var_sizes(const Shape &S, const qtt_trains_t *c, long long &member, 
     s_n = std::max(s_n, cq * w * S.xr[q]);
     s_n = std::max(s_n, cq1 * S.d[q] * (q + 2 <= L ? (long long)c->ranks[std::min(q + 2, L)] : 1));
     pmax = (int)std::max<long long>(pmax, std::max(cq * S.d[q], cq1 * S.d[q]));
+    if (ncores == 2 && q + 1 < L) {            // two-site split of (q, q+1)
+      const long long d1 = S.d[q + 1], w3 = (S.kind == TRUNCATE) ? 1 : S.orr[q + 2], c2 = c->ranks[q + 2];
+      const long long rc = cq * S.d[q];
+      s_n = std::max(s_n, rc * w2 * S.dj[q + 1] * S.xr[q + 2]);
+      s_n = std::max(s_n, rc * d1 * w3 * S.xr[q + 2]);
+      s_n = std::max(s_n, rc * d1 * c2);
+      s_n = std::max(s_n, rc * std::min(rc, d1 * c2));
+      pmax = (int)std::max<long long>(pmax, std::max(rc, d1 * c2));
+    }
   }
   e_n = eoff[L] + 1;
-  member = coff[L] + 2 * e_n + 3 * s_n + pmax;
+  member = coff[L] + 2 * e_n + 5 * s_n + 3 * (long long)pmax;
   member = (member + 31) & ~31LL;
 }
 
@@ -1104,42 +1251,63 @@ using namespace qtt;
 
 extern "C" {
 
-size_t qtt_variational_workspace_bytes(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
-                                       const qtt_trains_t *c) {
+size_t qtt_variational_workspace_bytes_ex(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                                          const qtt_trains_t *c, int32_t ncores) {
   Shape S;
-  if (!c || qtt_zipup_analyse(subscripts, op, x, 0, S) != QTT_OK) return 0;
+  if (!c || (ncores != 1 && ncores != 2) || qtt_zipup_analyse(subscripts, op, x, 0, S) != QTT_OK) return 0;
   long long member, coff[65], eoff[65], e_n, s_n;
   int pmax;
-  var_sizes(S, c, member, coff, eoff, e_n, s_n, pmax);
+  var_sizes(S, c, ncores, member, coff, eoff, e_n, s_n, pmax);
   return (size_t)S.B * member * 8 + 256;
 }
 
-qtt_status_t qtt_variational(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
-                             const qtt_trains_t *c, int32_t *c_ranks, int32_t sweeps, double *center_norm2,
-                             int32_t *status, void *workspace, size_t workspace_bytes, void *stream) {
+size_t qtt_variational_workspace_bytes(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                                       const qtt_trains_t *c) {
+  return qtt_variational_workspace_bytes_ex(subscripts, op, x, c, 1);
+}
+
+qtt_status_t qtt_variational_ex(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                                const qtt_trains_t *seed, const int32_t *seed_ranks, const qtt_trains_t *c,
+                                int32_t *c_ranks, int32_t sweeps, int32_t ncores, double eps, int32_t max_rank,
+                                double *center_norm2, int32_t *status, void *workspace, size_t workspace_bytes,
+                                void *stream) {
   Shape S;
   qtt_status_t st = qtt_zipup_analyse(subscripts, op, x, 0, S);
   if (st != QTT_OK) return st;
-  if (!c || !c->cores || !c->ranks || !c_ranks || !center_norm2 || !status) { set_error("NULL argument"); return QTT_EINVAL; }
-  if ((x->dtype != QTT_F64) || (op && op->dtype != QTT_F64) || c->dtype != QTT_F64) {
+  if (!seed || !seed->cores || !seed_ranks || !c || !c->cores || !c->ranks || !c_ranks || !center_norm2 || !status) {
+    set_error("NULL argument");
+    return QTT_EINVAL;
+  }
+  if ((x->dtype != QTT_F64) || (op && op->dtype != QTT_F64) || c->dtype != QTT_F64 || seed->dtype != QTT_F64) {
     set_error("qtt_variational: QTT_F64 trains only");
     return QTT_EUNSUPPORTED;
   }
-  if (c->n_sites != S.L || c->batch != S.B || c->n_legs != 1) { set_error("seed train shape mismatch"); return QTT_ESHAPE; }
-  for (int q = 0; q < S.L; ++q)
-    if (c->d_out[q] != S.d[q]) { set_error("seed digit size mismatch at core %d", q); return QTT_ESHAPE; }
+  for (const qtt_trains_t *t : {seed, c}) {
+    if (t->n_sites != S.L || t->batch != S.B || t->n_legs != 1) { set_error("seed/output train shape mismatch"); return QTT_ESHAPE; }
+    for (int q = 0; q < S.L; ++q)
+      if (t->d_out[q] != S.d[q]) { set_error("seed/output digit size mismatch at core %d", q); return QTT_ESHAPE; }
+  }
+  for (int q = 0; q <= S.L; ++q)
+    if (c->ranks[q] < seed->ranks[q]) {
+      set_error("output capacity %d at bond %d below the seed's %d", c->ranks[q], q, seed->ranks[q]);
+      return QTT_ECAPACITY;
+    }
   if (sweeps < 1) { set_error("sweeps < 1"); return QTT_EINVAL; }
+  if (ncores != 1 && ncores != 2) { set_error("ncores must be 1 or 2"); return QTT_EUNSUPPORTED; }
+  if (ncores == 2 && S.L < 2) { set_error("ncores = 2 needs n_sites >= 2"); return QTT_EINVAL; }
+  if (!(eps >= 0.0 && eps < 1.0)) { set_error("eps %g outside [0,1)", eps); return QTT_EINVAL; }
   if (S.L > 64) { set_error("n_sites > 64"); return QTT_EUNSUPPORTED; }
   cplx::VarArgs a;
   memset(&a, 0, sizeof(a));
   long long member;
   int pmax;
-  var_sizes(S, c, member, a.coff, a.eoff, a.e_n, a.s_n, pmax);
+  var_sizes(S, c, ncores, member, a.coff, a.eoff, a.e_n, a.s_n, pmax);
   if (!workspace || workspace_bytes < (size_t)S.B * member * 8 + 256) {
     set_error("workspace %zu bytes < required %zu", workspace_bytes, (size_t)S.B * member * 8 + 256);
     return QTT_ECAPACITY;
   }
   a.L = S.L; a.B = S.B; a.kind = S.kind; a.op_batch = op ? op->batch : 1; a.sweeps = sweeps;
+  a.ncores = ncores; a.eps = eps; a.max_rank = max_rank; a.pmax = pmax;
   for (int q = 0; q < S.L; ++q) {
     a.d[q] = S.d[q]; a.dj[q] = S.dj[q];
     a.x[q] = (const double *)x->cores[q];
@@ -1148,11 +1316,13 @@ qtt_status_t qtt_variational(const char *subscripts, const qtt_trains_t *op, con
       a.op[q] = (const double *)op->cores[q];
       a.o_bs[q] = (long long)op->ranks[q] * op->d_out[q] * (op->n_legs == 2 ? op->d_in[q] : 1) * op->ranks[q + 1];
     }
+    a.sd[q] = (const double *)seed->cores[q];
+    a.sd_bs[q] = (long long)seed->ranks[q] * S.d[q] * seed->ranks[q + 1];
     a.c[q] = (double *)c->cores[q];
     a.c_bs[q] = (long long)c->ranks[q] * S.d[q] * c->ranks[q + 1];
   }
   for (int q = 0; q <= S.L; ++q) { a.xr[q] = S.xr[q]; a.orr[q] = S.orr[q]; a.cap[q] = c->ranks[q]; }
-  a.c_ranks = c_ranks; a.norms = center_norm2; a.status = status;
+  a.sd_ranks = seed_ranks; a.c_ranks = c_ranks; a.norms = center_norm2; a.status = status;
   a.ws = (double *)workspace;
   a.ws_member = member;
   cudaStream_t s = (cudaStream_t)stream;
@@ -1160,6 +1330,13 @@ qtt_status_t qtt_variational(const char *subscripts, const qtt_trains_t *op, con
   cplx::k_variational<<<S.B, kThreads, 0, s>>>(a);
   QTT_CUDA_TRY(cudaGetLastError());
   return QTT_OK;
+}
+
+qtt_status_t qtt_variational(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                             const qtt_trains_t *c, int32_t *c_ranks, int32_t sweeps, double *center_norm2,
+                             int32_t *status, void *workspace, size_t workspace_bytes, void *stream) {
+  return qtt_variational_ex(subscripts, op, x, c, c_ranks, c, c_ranks, sweeps, 1, 0.0, 0, center_norm2, status,
+                            workspace, workspace_bytes, stream);
 }
 
 }  // extern "C"

@@ -49,6 +49,7 @@ _lib = None
 
 SYMBOLS = ["qtt_zipup_capacity", "qtt_zipup_workspace_bytes", "qtt_zipup_workspace_bytes_flags", "qtt_zipup",
            "qtt_zipup_summary", "qtt_variational_workspace_bytes", "qtt_variational",
+           "qtt_variational_workspace_bytes_ex", "qtt_variational_ex",
            "qtt_round_capacity", "qtt_round_workspace_bytes", "qtt_round",
            "qtt_einsum_exact", "qtt_inner_workspace_bytes", "qtt_inner", "qtt_to_dense_workspace_bytes",
            "qtt_to_dense", "qtt_last_error", "qtt_version"]
@@ -77,6 +78,10 @@ def load_library(path: str = LIB_PATH):
     L.qtt_variational_workspace_bytes.restype = sz
     L.qtt_variational.argtypes = [ctypes.c_char_p, P, P, P, vp, i32, vp, vp, vp, sz, vp]
     L.qtt_variational.restype = i32
+    L.qtt_variational_workspace_bytes_ex.argtypes = [ctypes.c_char_p, P, P, P, i32]
+    L.qtt_variational_workspace_bytes_ex.restype = sz
+    L.qtt_variational_ex.argtypes = [ctypes.c_char_p, P, P, P, vp, P, vp, i32, i32, f64, i32, vp, vp, vp, sz, vp]
+    L.qtt_variational_ex.restype = i32
     L.qtt_zipup_summary.argtypes = [i32, i32, vp, vp, vp, vp, vp]
     L.qtt_zipup_summary.restype = i32
     L.qtt_round_capacity.argtypes = [P, i32, ctypes.POINTER(i32)]
@@ -398,29 +403,47 @@ class VariationalResult:
 
 
 def variational(subscripts: str, op: Optional[DeviceTrains], x: DeviceTrains, seed: ZipupResult, sweeps: int,
-                stream=None) -> VariationalResult:
-    """qtt_variational (f3): refine a zip-up result variationally.  The
-    seed's cores and ranks are copied first (the zip-up result is left intact)."""
+                stream=None, ncores: int = 1, eps: float = 0.0, max_rank: int = 0,
+                capacity: Optional[Sequence[int]] = None) -> VariationalResult:
+    """qtt_variational_ex (f3): refine a zip-up result variationally.  The
+    seed (the zip-up result) is read, not modified.  ncores = 2: two-site super-cores whose
+    split is truncated by (eps, max_rank) -- ranks adapt up to the output capacity, by default
+    min(max_rank, the digit products) per bond (gen-style clipping), else the seed's."""
     L = load_library()
-    c = DeviceTrains([t.clone() for t in seed.out.cores], list(seed.out.ranks), list(seed.out.d_out), None)
-    ranks = seed.ranks.clone()
+    n = x.n_sites
+    d = list(seed.out.d_out)
+    if capacity is None:
+        if ncores == 2 and max_rank > 0:
+            left, right = [1], [1]
+            for q in range(n):
+                left.append(left[-1] * d[q])
+                right.append(right[-1] * d[n - 1 - q])
+            capacity = [min(max(max_rank, seed.out.ranks[q]), left[q], right[n - q]) for q in range(n + 1)]
+            capacity = [max(c, s) for c, s in zip(capacity, seed.out.ranks)]
+        else:
+            capacity = list(seed.out.ranks)
+    dev = x.cores[0].device
+    c = empty_like_capacity(x.batch, d, capacity, dev)
+    ranks = torch.zeros_like(seed.ranks)
     xs, kx = x.c_struct()
     os_ = None
     if op is not None:
         os_, ko = op.c_struct()
+    ss, ks = seed.out.c_struct()
     cs, kc = c.c_struct()
-    B, n = x.batch, x.n_sites
-    dev = x.cores[0].device
+    B = x.batch
     norms = torch.zeros((B, sweeps * 2 * n), dtype=torch.float64, device=dev)
     status = torch.zeros((1,), dtype=torch.int32, device=dev)
-    nbytes = L.qtt_variational_workspace_bytes(subscripts.encode(), ctypes.byref(os_) if os_ is not None else None,
-                                               ctypes.byref(xs), ctypes.byref(cs))
+    nbytes = L.qtt_variational_workspace_bytes_ex(subscripts.encode(),
+                                                  ctypes.byref(os_) if os_ is not None else None,
+                                                  ctypes.byref(xs), ctypes.byref(cs), int(ncores))
     if nbytes == 0:
         raise QttError(2, L.qtt_last_error().decode())
     ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-    _check(L.qtt_variational(subscripts.encode(), ctypes.byref(os_) if os_ is not None else None, ctypes.byref(xs),
-                             ctypes.byref(cs), ranks.data_ptr(), int(sweeps), norms.data_ptr(), status.data_ptr(),
-                             ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
+    _check(L.qtt_variational_ex(subscripts.encode(), ctypes.byref(os_) if os_ is not None else None,
+                                ctypes.byref(xs), ctypes.byref(ss), seed.ranks.data_ptr(), ctypes.byref(cs),
+                                ranks.data_ptr(), int(sweeps), int(ncores), float(eps), int(max_rank),
+                                norms.data_ptr(), status.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)))
     return VariationalResult(c, ranks, norms, status)
 
 

@@ -10,24 +10,24 @@ from paper_2602_20226_b200 import gen
 pytestmark = pytest.mark.gpu
 
 
-def _run(lib, kind, op, x, eps, max_rank, sweeps, mpo=False):
+def _run(lib, kind, op, x, eps, max_rank, sweeps, mpo=False, **vkw):
     import torch
     subs = {"matvec": "ij,j->i", "hadamard": "i,i->i", "truncate": "i->i"}[kind]
     xd = lib.to_device(x)
     od = None if op is None else lib.to_device(op, mpo=mpo)
     z = lib.ZipupPlan(subs, od, xd, eps, max_rank).run(od, xd)
-    v = lib.variational(subs, od, xd, z, sweeps)
+    v = lib.variational(subs, od, xd, z, sweeps, **vkw)
     torch.cuda.synchronize()
     assert int(z.status.item()) == 0 and int(v.status.item()) == 0
     return z, v
 
 
-def _check(lib, kind, op, xs, z, v, sweeps, b=0, dense=True):
+def _check(lib, kind, op, xs, z, v, sweeps, b=0, dense=True, ncores=1, eps=0.0, max_rank=0):
     from oracle import tt
     from oracle.variational import variational as ovar
     seed = lib.member_cores(z.out, z.ranks[b].cpu().tolist(), b)
-    ref = ovar(kind, op, xs, seed, sweeps)
-    got_n = v.center_norm2[b].cpu().numpy()
+    ref = ovar(kind, op, xs, seed, sweeps, ncores=ncores, eps=eps, max_rank=max_rank)
+    got_n = v.center_norm2[b].cpu().numpy()[:len(ref["center_norm2"])]
     ref_n = np.array(ref["center_norm2"])
     scale = ref_n.max()
     np.testing.assert_allclose(got_n, ref_n, rtol=0, atol=1e-10 * scale)
@@ -73,3 +73,40 @@ def test_variational_cfg5_member(lib):
     p = probs[0]
     z, v = _run(lib, "matvec", p.op.cores, p.x.cores, 1e-10, 16, 1, mpo=True)
     _check(lib, "matvec", p.op.cores, p.x.cores, z, v, 1, dense=False)
+
+
+# ------------------------------------------------------------ two-site super-cores (ncores = 2)
+# PAPER.md:300 (multi-core strategies, rank control), PAPER.md:794 (ncores=2, cutoff=0.0,
+# max_rank=8); reading c-A37.
+
+@pytest.mark.parametrize("kind", ["matvec", "hadamard", "truncate"])
+def test_variational_two_site_random(lib, kind):
+    rng = np.random.default_rng(170)
+    dims = [2, 3, 2, 2, 5, 2, 2, 3]
+    x = gen.random_mps(dims, 9, rng).cores
+    op = {"matvec": gen.random_mpo(dims, 3, rng, 0.5).cores, "hadamard": gen.random_mps(dims, 3, rng).cores,
+          "truncate": None}[kind]
+    z, v = _run(lib, kind, op, x, 0.2, 4, 2, mpo=(kind == "matvec"), ncores=2, eps=0.0, max_rank=8)
+    _check(lib, kind, op, x, z, v, 2, ncores=2, eps=0.0, max_rank=8)
+    assert max(v.ranks[0].cpu().tolist()) > 4          # the ranks adapted beyond the seed's
+
+
+def test_variational_two_site_cutoff_and_paper_call(lib):
+    """The paper's call (max_rank=8, cutoff=0.0, ncores=2, nsweeps=2) and a cutoff
+    that decides ranks below max_rank."""
+    rng = np.random.default_rng(171)
+    dims = [2] * 10
+    x = gen.random_mps(dims, 6, rng).cores
+    op = gen.random_mpo(dims, 2, rng, 0.5).cores
+    z, v = _run(lib, "matvec", op, x, 0.3, 2, 2, mpo=True, ncores=2, eps=0.0, max_rank=8)
+    _check(lib, "matvec", op, x, z, v, 2, ncores=2, eps=0.0, max_rank=8)
+    z, v = _run(lib, "matvec", op, x, 0.3, 2, 2, mpo=True, ncores=2, eps=1e-3, max_rank=0)
+    _check(lib, "matvec", op, x, z, v, 2, ncores=2, eps=1e-3, max_rank=0)
+
+
+def test_variational_two_site_cfg5_member(lib):
+    """configs[4] shapes seeded with a max-rank-8 zip-up, two-site sweep to max rank 16."""
+    probs, xs, ops = gen.cfg5_batch_arrays([4])
+    p = probs[0]
+    z, v = _run(lib, "matvec", p.op.cores, p.x.cores, 1e-10, 8, 1, mpo=True, ncores=2, eps=0.0, max_rank=16)
+    _check(lib, "matvec", p.op.cores, p.x.cores, z, v, 1, dense=False, ncores=2, eps=0.0, max_rank=16)
