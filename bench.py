@@ -319,9 +319,18 @@ def cpu_baseline_single(p, budget_s, window=1):
     done = [0]
     t0 = time.perf_counter()
 
+    marks = [t0]
+
     def on_site(q):
+        # stop at a site boundary when the next site, predicted from the growth of the last two,
+        # would overrun the budget (a site cannot be interrupted)
         done[0] = q + 1
-        if time.perf_counter() - t0 > budget_s:
+        now = time.perf_counter()
+        marks.append(now)
+        last = marks[-1] - marks[-2]
+        prev = marks[-2] - marks[-3] if len(marks) > 2 else last
+        pred = last * min(8.0, max(1.0, last / max(prev, 1e-9)))
+        if now - t0 + pred > budget_s:
             raise _Budget()
 
     res = None
