@@ -226,6 +226,54 @@ qtt_status_t qtt_variational_ex(const char *subscripts, const qtt_trains_t *op, 
                                 double *center_norm2, int32_t *status, void *workspace, size_t workspace_bytes,
                                 void *stream);
 
+/* ---------------------------------------------------------------------------------------
+ * qtt_zipup_sharded -- ONE zip-up (fp64, batch 1, large-member path) split across the
+ * processes of a job, one GPU each (SURVEY.md §8(f) f4 "cross-GPU sharding of one zip-up",
+ * §8(e); the site matrix T_q -- "contracted exactly" -- is split by the
+ * SVD of PAPER.md:257/269).  The columns of every site matrix T_q (m = chi d rows, columns
+ * (w', r')) are split into S = world * local_shards shards by contiguous, balanced ranges of
+ * the state bond r' (r_{q+1}); shard t = rank * local_shards + s.  Per site:
+ *   1. each process contracts its shards' column slabs T_t = contract(G, x_q[:, :, r'-slice],
+ *      op_q) from the full carry G, and reduces each to an m x m factor F_t with
+ *      F_t^T F_t = T_t T_t^T (the R of T_t^H by the Householder QR of a3 when the slab has at
+ *      least m columns, else T_t^H itself), zero-padded to mcap x mcap, into send_r;
+ *   2. allgather(0): recv_r[t] = every shard's F_t (all processes, shard order);
+ *   3. R = the R of the stacked [F_0; ...; F_{S-1}] (same QR) -- the R of T^H, since
+ *      T T^T = sum_t F_t^T F_t; then a4-a6 exactly as qtt_zipup: one-sided Jacobi on R^T,
+ *      the SPEC.md:299 truncation (k <= min(max_rank, w' r')), C_q = U_k written by every
+ *      process (identical values on all);
+ *   4. each process forms its carry slabs U_k^T T_t (k x w' x slice) into send_c;
+ *   5. allgather(1): recv_c[t] = every shard's carry slab; the full carry (k, w', r') is
+ *      assembled for the next site.
+ * The last site (n = 1) and a1 run unsharded on every process.  Exchanges per site: S
+ * mcap^2 + S kcap ncap_slab doubles (the carry all-gather is the "carry exchange").
+ *   comm->allgather(phase, user) must ENQUEUE the all-gather of the phase's buffers on the
+ *   stream (e.g. torch.distributed / NCCL on the current stream) and return 0; it is called
+ *   from this function, in site order, the same number of times on every process.  With
+ *   world == 1 it may be NULL: the library copies send -> recv itself (several shards in one
+ *   process -- the same arithmetic as S processes).
+ *   Buffer sizes: qtt_zipup_sharded_sizes() -> elements of ONE shard's R slab and carry slab;
+ *   send_* hold local_shards slabs, recv_* hold world * local_shards.
+ * Outputs as qtt_zipup (member 0).  Errors: QTT_EUNSUPPORTED for batch != 1, non-f64,
+ * QTT_WINDOW2 or a site matrix the large-member path cannot stage; QTT_EINVAL for a bad comm.
+ */
+typedef int (*qtt_allgather_fn)(int32_t phase, void *user);
+typedef struct {
+  int32_t world, rank, local_shards;
+  qtt_allgather_fn allgather;
+  void *user;
+  double *send_r, *recv_r;   /* device: [local_shards] / [world*local_shards] x r_elems  */
+  double *send_c, *recv_c;   /* device: [local_shards] / [world*local_shards] x c_elems  */
+} qtt_shard_comm_t;
+qtt_status_t qtt_zipup_sharded_sizes(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                                     int32_t max_rank, int32_t world, int32_t local_shards, size_t *r_elems,
+                                     size_t *c_elems, size_t *workspace_bytes);
+qtt_status_t qtt_zipup_sharded(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x, double eps,
+                               int32_t max_rank, uint32_t flags, const qtt_trains_t *out, int32_t *out_ranks,
+                               double *delta2, double *norm2, int32_t *status, double *sigma, int32_t sigma_stride,
+                               const qtt_shard_comm_t *comm, void *workspace, size_t workspace_bytes,
+                               void *stream);
+
 /* qtt_zipup_summary -- the per-batch scalars that are all-reduced across GPUs
  * (SURVEY.md §8(a) a8): summary4 (device f64 [4]) = [sum_b sum_q delta2, sum_b norm2,
  * sum_b sum_q out_ranks[b][q+1] (q < L-1), B].  Deterministic fixed-order sums. */

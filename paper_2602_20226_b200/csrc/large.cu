@@ -77,6 +77,7 @@ __device__ __forceinline__ void grid_sync(GridBar *gb, unsigned nblocks, int tag
 
 struct SiteDims {
   int chi, r, r2, w, w2, d, dj, m, n, p, direct, k;
+  int kcap;        // > 0: k <= kcap besides max_rank (the sharded zip-up's true column count)
 };
 
 struct PlanArgs {
@@ -100,6 +101,7 @@ __global__ void k_plan(PlanArgs a) {
   D.direct = (D.m > D.n);
   D.p = D.direct ? D.n : D.m;
   D.k = 0;
+  D.kcap = 0;
   *a.dims = D;
   GemmSpec g0{};   // X = G (chi*w x r) * x_q (r x dj*r2)   [truncate: T = G (chi x r) * x_q]
   g0.M = D.chi * D.w; g0.K = D.r; g0.N = ((a.kind == HADAMARD || a.kind == TRUNCATE) ? D.d : D.dj) * D.r2;
@@ -782,8 +784,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_finish(FinishArgs a) {
     // recompute tail[k] in the same order as the oracle
     double tail = 0.0;
     for (int jj = p - 1; jj >= k; --jj) tail += a.s2[a.perm[jj]];
-    if (a.max_rank > 0 && k > a.max_rank) {
-      k = a.max_rank;
+    const int kc = (a.max_rank > 0 && D.kcap > 0) ? min(a.max_rank, D.kcap) : (a.max_rank > 0 ? a.max_rank : D.kcap);
+    if (kc > 0 && k > kc) {
+      k = kc;
       tail = 0.0;
       for (int jj = p - 1; jj >= k; --jj) tail += a.s2[a.perm[jj]];
     }
@@ -1298,5 +1301,513 @@ qtt_status_t large_zipup(const Shape &S, const qtt_trains_t *op, const qtt_train
   return QTT_OK;
 }
 
+
+// ======================================================================= f4: sharded zip-up
+// One zip-up split across processes (qtt.h qtt_zipup_sharded).  Column
+// shards of every site matrix by contiguous balanced ranges of the state bond r_{q+1}; each
+// shard's slab is reduced to an m x m factor F_t (F_t^T F_t = T_t T_t^T), the factors of all
+// shards are all-gathered and stacked, and the R of the stack is the R of T^H (the TSQR
+// identity: T T^T = sum_t T_t T_t^T).  a4-a6 then run on R as in the unsharded sweep; the
+// carry U_k^T T is formed per slab and all-gathered ("carry exchange").
+
+__device__ __forceinline__ void shard_range(int n, int S, int t, int &lo, int &hi) {
+  lo = (int)(((long long)t * n) / S);
+  hi = (int)(((long long)(t + 1) * n) / S);
+}
+
+// the state core's r'-slice of shard t into a contiguous slab (r, legs, cnt); xr_s[q] = r,
+// xr_s[q+1] = cnt (the slab's rank row for k_plan)
+struct SlabArgs {
+  const double *Xq;
+  const int *xr;
+  int q, legs, S, t;
+  double *slab;
+  int *xr_s;
+};
+__global__ void k_shard_slab(SlabArgs a) {
+  const int r = a.xr[a.q], r2 = a.xr[a.q + 1];
+  int lo, hi;
+  shard_range(r2, a.S, a.t, lo, hi);
+  const int cnt = hi - lo;
+  const long long n = (long long)r * a.legs * cnt;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % cnt);
+    const long long rj = i / cnt;
+    a.slab[i] = a.Xq[rj * r2 + lo + c];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) { a.xr_s[a.q] = r; a.xr_s[a.q + 1] = cnt; }
+}
+
+// F_t (mcap x mcap row-major, zero padded) from the shard's QR (R in A, row-major) or, when
+// the slab has fewer columns than rows (direct), from the slab itself: F_t = T_t^T
+__global__ void k_shard_factor(const SiteDims *dims, const double *A, const double *T, int mcap, double *F) {
+  const SiteDims D = *dims;
+  const long long n = (long long)mcap * mcap;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i / mcap), c = (int)(i % mcap);
+    double v = 0.0;
+    if (c < D.m) {
+      if (!D.direct) v = (j < D.m && c >= j) ? A[(size_t)j * D.m + c] : 0.0;
+      else v = (j < D.n) ? T[(size_t)c * D.n + j] : 0.0;
+    }
+    F[i] = v;
+  }
+}
+
+// the stacked factors as a "T" for k_qr_coop: Tw (m x S*mcap) row-major, Tw[c][t*mcap + j] =
+// F_t[j][c]; the stack's SiteDims: p = m, never direct, k <= kcap = w' r' (the true columns)
+struct StackArgs {
+  const SiteDims *dims0;
+  const double *recv;
+  long long f_elems;
+  int S, mcap;
+  const int *xr, *orr;
+  int q, kind;
+  double *Tw;
+  SiteDims *dims_st;
+};
+__global__ void k_shard_stack(StackArgs a) {
+  const SiteDims D0 = *a.dims0;
+  const int m = D0.m, ns = a.S * a.mcap;
+  const long long n = (long long)m * ns;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i / ns), col = (int)(i % ns), t = col / a.mcap, j = col % a.mcap;
+    a.Tw[i] = a.recv[(size_t)t * a.f_elems + (size_t)j * a.mcap + c];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    SiteDims D = D0;
+    const int w2 = (a.kind == TRUNCATE) ? 1 : a.orr[a.q + 1];
+    D.r2 = a.xr[a.q + 1];
+    D.w2 = w2;
+    D.n = ns;
+    D.direct = 0;
+    D.p = m;
+    D.k = 0;
+    D.kcap = w2 * D.r2;
+    *a.dims_st = D;
+  }
+}
+
+// carry slab spec: send_c[s][kk][w'][c] = sum_i C_q[i][kk] T_s[i][w' cnt + c]  (kk < k, c < cnt)
+struct CarrySpecArgs {
+  const SiteDims *dims_st, *dims_s;
+  const double *Cq, *Ts;
+  double *out;
+  int slice_cap;
+  GemmSpec *spec;
+};
+__global__ void k_shard_carry_spec(CarrySpecArgs a) {
+  if (threadIdx.x != 0) return;
+  const SiteDims D = *a.dims_st, Ds = *a.dims_s;
+  GemmSpec g{};
+  g.M = D.k; g.K = D.m; g.N = Ds.r2; g.nz1 = 1; g.nz2 = Ds.w2;
+  g.A = a.Cq; g.sam = 1; g.sak = D.k;
+  g.B = a.Ts; g.sbk = Ds.n; g.sbn = 1; g.sb2 = Ds.r2;
+  g.C = a.out; g.scm = (long long)Ds.w2 * a.slice_cap; g.scn = 1; g.sc2 = a.slice_cap;
+  if (Ds.n == 0 || Ds.r2 == 0) g.M = 0;          // empty slab: nothing to write
+  *a.spec = g;
+}
+
+// full carry G (k, w', r') from the all-gathered slabs
+struct AssembleArgs {
+  const SiteDims *dims_st;
+  const double *recv;
+  long long c_elems;
+  int S, slice_cap;
+  double *G;
+};
+__global__ void k_shard_assemble(AssembleArgs a) {
+  const SiteDims D = *a.dims_st;
+  const int k = D.k, w2 = D.w2, r2 = D.r2;
+  const long long n = (long long)k * w2 * r2;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int rr = (int)(i % r2);
+    const long long kw = i / r2;
+    const int ww = (int)(kw % w2), kk = (int)(kw / w2);
+    int t = (int)(((long long)rr * a.S) / max(r2, 1));
+    int lo, hi;
+    shard_range(r2, a.S, t, lo, hi);
+    while (rr >= hi) { ++t; shard_range(r2, a.S, t, lo, hi); }
+    while (rr < lo) { --t; shard_range(r2, a.S, t, lo, hi); }
+    a.G[i] = a.recv[(size_t)t * a.c_elems + ((size_t)kk * w2 + ww) * a.slice_cap + (rr - lo)];
+  }
+}
+
+struct ShardPlan {
+  int S, ls;                        // total shards, local shards
+  long long mcap, slab_ncap, slice_cap_max, gcap, xcap, tcap, acap, r_elems, c_elems;
+  std::vector<int> slice_cap;       // per site: ceil(xr[q+1] / S)
+  int Gqr_s, RB_s, Gqr_st, RB_st, Gjac, WB;
+  size_t qr_smem, jac_smem;
+  // offsets
+  size_t off_xo, off_oo, off_xr, off_or, off_a1, a1_bytes;
+  size_t off_G, off_Tst, off_Ast, off_part, off_wtot, off_gram, off_bc, off_s2, off_perm, off_flags, off_ver, off_sw,
+      off_bar, off_dims_st, off_spec_st, off_shard, shard_bytes, total;
+  // per-shard sub-offsets (relative to off_shard + s * shard_bytes)
+  size_t so_slab, so_X, so_T, so_Tw, so_A, so_xr, so_dims, so_spec;
+  LargeLayout a1;                   // the unsharded a1 / last-site layout
+};
+
+static qtt_status_t plan_shard(const Shape &S_, int world, int ls, uint32_t flags, ShardPlan &P) {
+  const Shape &S = S_;
+  const int L = S.L;
+  P.S = world * ls; P.ls = ls;
+  P.mcap = 1; P.slab_ncap = 1; P.gcap = 1; P.xcap = 1; P.tcap = 1; P.acap = 1; P.c_elems = 1;
+  P.slice_cap.assign(L + 1, 1);
+  long long full_ncap = 1;
+  for (int q = 0; q < L; ++q) {
+    const long long w = (S.kind == TRUNCATE) ? 1 : S.orr[q], w2 = (S.kind == TRUNCATE) ? 1 : S.orr[q + 1];
+    const long long m = (long long)S.cap[q] * S.d[q];
+    const long long sc = (S.xr[q + 1] + P.S - 1) / P.S;
+    P.slice_cap[q] = (int)sc;
+    P.mcap = std::max(P.mcap, m);
+    P.slab_ncap = std::max(P.slab_ncap, w2 * sc);
+    full_ncap = std::max(full_ncap, w2 * S.xr[q + 1]);
+    P.gcap = std::max(P.gcap, (long long)S.cap[q] * w * S.xr[q]);
+    P.gcap = std::max(P.gcap, (long long)S.cap[q + 1] * w2 * S.xr[q + 1]);
+    const long long legs = (S.kind == MATVEC) ? S.dj[q] : S.d[q];
+    P.xcap = std::max(P.xcap, (long long)S.cap[q] * w * legs * std::max(sc, (long long)(q == L - 1 ? S.xr[q + 1] : 1)));
+    P.tcap = std::max(P.tcap, m * std::max(w2 * sc, (long long)(q == L - 1 ? w2 * S.xr[q + 1] : 1)));
+    P.acap = std::max(P.acap, m * std::min(m, w2 * sc));
+    P.c_elems = std::max(P.c_elems, (long long)S.cap[q + 1] * w2 * sc);
+  }
+  P.acap = std::max(P.acap, P.mcap * P.mcap);
+  P.r_elems = P.mcap * P.mcap;
+  if (g_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  auto qr_geom = [&](long long rows, int &Gq, int &RB) -> qtt_status_t {
+    Gq = (int)std::min<long long>(g_sms, std::max<long long>(1, (rows + 31) / 32));
+    RB = (int)((rows + Gq - 1) / Gq);
+    RB = ((RB + 31) / 32) * 32;
+    if (RB > kQrRowsMax) { set_error("sharded zip-up: %lld rows of T^H per shard too many", rows); return QTT_EUNSUPPORTED; }
+    return QTT_OK;
+  };
+  qtt_status_t st = qr_geom(P.slab_ncap, P.Gqr_s, P.RB_s);
+  if (st != QTT_OK) return st;
+  st = qr_geom((long long)P.S * P.mcap, P.Gqr_st, P.RB_st);
+  if (st != QTT_OK) return st;
+  P.qr_smem = sizeof(double) * ((size_t)kNb * std::max(P.RB_s, P.RB_st) + 32 + kNb * kNb + 2 * kNb + kNb * 64);
+  int WB = kWarps;
+  while (WB > 1 && 2 * WB * (P.mcap + 1) * 8 > 200 * 1024) WB /= 2;
+  if (2 * WB * (P.mcap + 1) * 8 > 200 * 1024) { set_error("sharded zip-up: m = %lld too large", P.mcap); return QTT_EUNSUPPORTED; }
+  P.WB = WB;
+  P.Gjac = (int)std::min<long long>(g_sms, std::max<long long>(1, (P.mcap + 2 * WB - 1) / (2 * WB)));
+  P.jac_smem = sizeof(double) * (2 * WB * P.mcap + 2 * WB);
+  st = large_layout(S, flags, P.a1);  // unsharded layout: a1 operand slots + scratch (also the last site)
+  if (st != QTT_OK) return st;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+  P.off_a1 = take(P.a1.total);
+  P.off_G = take(8 * P.gcap);
+  P.off_Tst = take(8 * (size_t)P.mcap * P.S * P.mcap);
+  P.off_Ast = take(8 * (size_t)P.mcap * P.mcap);
+  const int Gmax = std::max(std::max(P.Gqr_s, P.Gqr_st), P.Gjac);
+  P.off_part = take(8 * ((size_t)Gmax * kNb * P.mcap + (size_t)Gmax * kNb * kNb + 16));
+  P.off_wtot = take(8 * (size_t)kNb * P.mcap);
+  P.off_gram = take(8 * kNb * kNb);
+  P.off_bc = take(8 * 64);
+  P.off_s2 = take(8 * P.mcap);
+  P.off_perm = take(4 * P.mcap);
+  P.off_flags = take(4 * 4);
+  P.off_ver = take(4 * ((size_t)P.mcap + 2));
+  P.off_sw = take(4 * 4);
+  P.off_bar = take(sizeof(GridBar) * 2);
+  P.off_dims_st = take(sizeof(SiteDims));
+  P.off_spec_st = take(sizeof(GemmSpec) * 3);
+  size_t so = 0;
+  auto stake = [&](size_t bytes) { size_t o = so; so += (bytes + 255) & ~size_t(255); return o; };
+  long long slab_max = 1;
+  for (int q = 0; q < L; ++q) {
+    const long long legs = (S.kind == MATVEC) ? S.dj[q] : S.d[q];
+    slab_max = std::max(slab_max, (long long)S.xr[q] * legs * P.slice_cap[q]);
+  }
+  P.so_slab = stake(8 * slab_max);
+  P.so_X = stake(8 * P.xcap);
+  P.so_T = stake(8 * P.tcap);
+  P.so_Tw = stake(8 * P.tcap);
+  P.so_A = stake(8 * P.acap);
+  P.so_xr = stake(4 * (L + 1));
+  P.so_dims = stake(sizeof(SiteDims));
+  P.so_spec = stake(sizeof(GemmSpec) * 4);
+  P.shard_bytes = so;
+  P.off_shard = take(so * ls);
+  P.total = off;
+  (void)full_ncap;
+  return QTT_OK;
+}
+
+qtt_status_t sharded_sizes(const Shape &S, int world, int ls, uint32_t flags, size_t *r_elems, size_t *c_elems,
+                           size_t *ws_bytes) {
+  ShardPlan P;
+  qtt_status_t st = plan_shard(S, world, ls, flags, P);
+  if (st != QTT_OK) return st;
+  if (r_elems) *r_elems = (size_t)P.r_elems;
+  if (c_elems) *c_elems = (size_t)P.c_elems;
+  if (ws_bytes) *ws_bytes = P.total;
+  return QTT_OK;
+}
+
+static qtt_status_t shard_exchange(const qtt_shard_comm_t *c, int phase, const ShardPlan &P, cudaStream_t s) {
+  if (c->allgather) {
+    if (c->allgather(phase, c->user) != 0) { set_error("allgather callback failed (phase %d)", phase); return QTT_EINVAL; }
+    return QTT_OK;
+  }
+  const size_t n = (phase == 0) ? (size_t)P.r_elems : (size_t)P.c_elems;
+  const double *src = (phase == 0) ? c->send_r : c->send_c;
+  double *dst = (phase == 0) ? c->recv_r : c->recv_c;
+  QTT_CUDA_TRY(cudaMemcpyAsync(dst + (size_t)c->rank * P.ls * n, src, sizeof(double) * n * P.ls,
+                               cudaMemcpyDeviceToDevice, s));
+  return QTT_OK;
+}
+
+qtt_status_t large_zipup_sharded(const Shape &S, const qtt_trains_t *op, const qtt_trains_t *x, uint32_t flags,
+                                 const LargeIO &io, const qtt_shard_comm_t *comm, void *workspace,
+                                 size_t workspace_bytes, cudaStream_t s) {
+  ShardPlan P;
+  qtt_status_t st = plan_shard(S, comm->world, comm->local_shards, flags, P);
+  if (st != QTT_OK) return st;
+  if (!workspace || workspace_bytes < P.total) {
+    set_error("workspace %zu bytes < required %zu", workspace_bytes, P.total);
+    return QTT_ECAPACITY;
+  }
+  const int L = S.L, kind = S.kind;
+  char *ws = (char *)workspace;
+  // ---- a1 on the full operands (every process, identical results): the unsharded layout
+  char *wa = ws + P.off_a1;
+  double *Xo = (double *)(wa + P.a1.off_xo), *Oo = (double *)(wa + P.a1.off_oo);
+  int *xr = (int *)(wa + P.a1.off_xr), *orr = (int *)(wa + P.a1.off_or);
+  char *scratch = wa + P.a1.off_scratch;
+  const bool has_op = kind != TRUNCATE;
+  for (int q = 0; q < L; ++q) {
+    const long long nx = (long long)S.xr[q] * S.dj[q] * S.xr[q + 1];
+    k_copy_member<<<(unsigned)std::min<long long>((nx + 255) / 256, 4096), 256, 0, s>>>(
+        (const double *)x->cores[q], Xo + S.xoff[q], nx);
+    if (has_op) {
+      const long long no = S.ooff[q + 1] - S.ooff[q];
+      k_copy_member<<<(unsigned)std::min<long long>((no + 255) / 256, 4096), 256, 0, s>>>(
+          (const double *)op->cores[q], Oo + S.ooff[q], no);
+    }
+  }
+  QTT_CUDA_TRY(cudaGetLastError());
+  {
+    RankRow rx, ro;
+    for (int q = 0; q <= L; ++q) { rx.v[q] = S.xr[q]; ro.v[q] = S.orr[q]; }
+    k_set_ranks<<<1, 64, 0, s>>>(xr, rx, L + 1);
+    k_set_ranks<<<1, 64, 0, s>>>(orr, ro, L + 1);
+    QTT_CUDA_TRY(cudaGetLastError());
+  }
+  st = orth_operand(P.a1.px, Xo, S.xoff, xr, io.status, scratch, s);
+  if (st != QTT_OK) return st;
+  if (P.a1.po.active) {
+    st = orth_operand(P.a1.po, Oo, S.ooff, orr, io.status, scratch, s);
+    if (st != QTT_OK) return st;
+  }
+  QTT_CUDA_TRY(cudaFuncSetAttribute(k_qr_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  QTT_CUDA_TRY(cudaFuncSetAttribute(k_jacobi_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)dgemm::SMEM_BYTES));
+  QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_dmma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)dgemm::SMEM_BYTES));
+  // ---- shared buffers
+  double *G = (double *)(ws + P.off_G), *Tst = (double *)(ws + P.off_Tst), *Ast = (double *)(ws + P.off_Ast);
+  double *part = (double *)(ws + P.off_part), *wtot = (double *)(ws + P.off_wtot), *gram = (double *)(ws + P.off_gram);
+  double *bc = (double *)(ws + P.off_bc), *s2 = (double *)(ws + P.off_s2);
+  int *perm = (int *)(ws + P.off_perm), *jflags = (int *)(ws + P.off_flags), *ver = (int *)(ws + P.off_ver);
+  int *sw_scr = (int *)(ws + P.off_sw);
+  GridBar *bar = (GridBar *)(ws + P.off_bar);
+  SiteDims *dims_st = (SiteDims *)(ws + P.off_dims_st);
+  GemmSpec *spec_st = (GemmSpec *)(ws + P.off_spec_st);
+  QTT_CUDA_TRY(cudaMemsetAsync(bar, 0, sizeof(GridBar) * 2, s));
+  k_site0_init<<<1, 32, 0, s>>>(G, io.out_ranks);
+  QTT_CUDA_TRY(cudaGetLastError());
+  auto shard_base = [&](int sl) { return ws + P.off_shard + (size_t)sl * P.shard_bytes; };
+  const int grank = comm->rank;
+  for (int q = 0; q < L; ++q) {
+    const long long w = (kind == TRUNCATE) ? 1 : S.orr[q], w2 = (kind == TRUNCATE) ? 1 : S.orr[q + 1];
+    const long long legs = (kind == MATVEC) ? S.dj[q] : S.d[q];
+    const long long m_cap = (long long)S.cap[q] * S.d[q];
+    const double *Xq = Xo + S.xoff[q];
+    const double *Oq = has_op ? Oo + S.ooff[q] : nullptr;
+    double *Cq = (double *)io.out->cores[q];
+    auto contract = [&](char *sb, const double *xsrc, const int *xr_row, long long ncols_cap) -> qtt_status_t {
+      SiteDims *dims = (SiteDims *)(sb + P.so_dims);
+      GemmSpec *spec = (GemmSpec *)(sb + P.so_spec);
+      double *X = (double *)(sb + P.so_X), *T = (double *)(sb + P.so_T);
+      PlanArgs pa;
+      pa.q = q; pa.L = L; pa.kind = kind; pa.d = S.d[q]; pa.dj = S.dj[q];
+      pa.xr = xr_row; pa.orr = orr; pa.yr = io.out_ranks;
+      pa.Xq = xsrc; pa.Oq = Oq;
+      pa.G = G; pa.X = X; pa.T = T; pa.Cq = Cq;
+      pa.dims = dims; pa.spec = spec;
+      k_plan<<<1, 32, 0, s>>>(pa);
+      QTT_CUDA_TRY(cudaGetLastError());
+      launch_gemm_spec(spec + 0, (long long)S.cap[q] * w, legs * ncols_cap, 1, 1, true, false, s);
+      QTT_CUDA_TRY(cudaGetLastError());
+      const unsigned ew = (unsigned)std::min<long long>((m_cap * w2 * ncols_cap + kThreads - 1) / kThreads, 8192);
+      if (kind == MATVEC) {
+        k_mpo_apply<<<std::max(ew, 1u), kThreads, 0, s>>>(dims, X, Oq, T);
+        QTT_CUDA_TRY(cudaGetLastError());
+      } else if (kind == HADAMARD) {
+        launch_gemm_spec(spec + 1, w2, ncols_cap, S.cap[q], S.d[q], false, false, s);
+        QTT_CUDA_TRY(cudaGetLastError());
+      }
+      return QTT_OK;
+    };
+    if (q == L - 1) {            // a7: unsharded on every process
+      char *sb = shard_base(0);
+      st = contract(sb, Xq, xr, S.xr[q + 1]);
+      if (st != QTT_OK) return st;
+      k_last<<<1, kThreads, 0, s>>>((SiteDims *)(sb + P.so_dims), (double *)(sb + P.so_T), Cq, io.norm2,
+                                    io.delta2 + q, io.out_ranks + L, io.status);
+      QTT_CUDA_TRY(cudaGetLastError());
+      if (io.sweeps) QTT_CUDA_TRY(cudaMemsetAsync(io.sweeps + q, 0, sizeof(int), s));
+      break;
+    }
+    const int sc = P.slice_cap[q];
+    // 1. local shards: slab, contraction, factor F_t
+    for (int sl = 0; sl < P.ls; ++sl) {
+      char *sb = shard_base(sl);
+      const int t = grank * P.ls + sl;
+      SlabArgs ka{Xq, xr, q, (int)legs, P.S, t, (double *)(sb + P.so_slab), (int *)(sb + P.so_xr)};
+      const long long nslab = (long long)S.xr[q] * legs * sc;
+      k_shard_slab<<<(unsigned)std::max<long long>(1, std::min<long long>((nslab + 255) / 256, 4096)), 256, 0, s>>>(ka);
+      QTT_CUDA_TRY(cudaGetLastError());
+      st = contract(sb, (double *)(sb + P.so_slab), (int *)(sb + P.so_xr), sc);
+      if (st != QTT_OK) return st;
+      SiteDims *dims = (SiteDims *)(sb + P.so_dims);
+      double *T = (double *)(sb + P.so_T), *Tw = (double *)(sb + P.so_Tw), *A = (double *)(sb + P.so_A);
+      const unsigned ew = (unsigned)std::max<long long>(1, std::min<long long>((m_cap * w2 * sc + kThreads - 1) / kThreads, 8192));
+      k_copy_T<<<ew, kThreads, 0, s>>>(dims, T, Tw, A);
+      QTT_CUDA_TRY(cudaGetLastError());
+      QrArgs qa;
+      qa.dims = dims; qa.Tw = Tw; qa.Rout = A; qa.part = part; qa.wtot = wtot; qa.gram = gram;
+      qa.bc = bc; qa.bar = bar; qa.G = P.Gqr_s; qa.RB = P.RB_s; qa.mcap = (int)P.mcap;
+      st = coop_launch((const void *)k_qr_coop, P.Gqr_s, P.qr_smem, &qa, s);
+      if (st != QTT_OK) return st;
+      const long long fe = P.r_elems;
+      k_shard_factor<<<(unsigned)std::min<long long>((fe + 255) / 256, 4096), 256, 0, s>>>(
+          dims, A, T, (int)P.mcap, comm->send_r + (size_t)sl * fe);
+      QTT_CUDA_TRY(cudaGetLastError());
+    }
+    // 2. exchange the factors
+    st = shard_exchange(comm, 0, P, s);
+    if (st != QTT_OK) return st;
+    // 3. R of the stack, Jacobi, truncation + emit
+    {
+      StackArgs sa{(SiteDims *)(shard_base(0) + P.so_dims), comm->recv_r, P.r_elems, P.S, (int)P.mcap, xr, orr,
+                   q, kind, Tst, dims_st};
+      if (kind == TRUNCATE) sa.orr = xr;          // unused (w2 = 1)
+      const long long ne = m_cap * P.S * P.mcap;
+      k_shard_stack<<<(unsigned)std::min<long long>((ne + 255) / 256, 8192), 256, 0, s>>>(sa);
+      QTT_CUDA_TRY(cudaGetLastError());
+      QrArgs qa;
+      qa.dims = dims_st; qa.Tw = Tst; qa.Rout = Ast; qa.part = part; qa.wtot = wtot; qa.gram = gram;
+      qa.bc = bc; qa.bar = bar; qa.G = P.Gqr_st; qa.RB = P.RB_st; qa.mcap = (int)P.mcap;
+      st = coop_launch((const void *)k_qr_coop, P.Gqr_st, P.qr_smem, &qa, s);
+      if (st != QTT_OK) return st;
+      JacArgs ja;
+      ja.dims = dims_st; ja.A = Ast; ja.bar = bar + 1; ja.flags = jflags; ja.ver = ver; ja.part = part; ja.nrm = s2;
+      ja.G = P.Gjac; ja.WB = P.WB;
+      ja.noise_ok = noise_ok(io.eps, (int)P.mcap);
+      ja.sweeps_out = io.sweeps ? io.sweeps + q : sw_scr; ja.status = io.status;
+      QTT_CUDA_TRY(cudaMemsetAsync(jflags, 0, sizeof(int) * 3, s));
+      QTT_CUDA_TRY(cudaMemsetAsync(ver, 0, sizeof(int) * (P.mcap + 2), s));
+      st = coop_launch((const void *)k_jacobi_coop, P.Gjac, P.jac_smem, &ja, s);
+      if (st != QTT_OK) return st;
+      FinishArgs fa;
+      fa.dims = dims_st; fa.A = Ast; fa.Cq = Cq; fa.yr_next = io.out_ranks + q + 1; fa.delta2 = io.delta2 + q;
+      fa.sigma = io.sigma ? io.sigma + (size_t)q * io.sigma_stride : nullptr; fa.sigma_stride = io.sigma_stride;
+      fa.s2 = s2; fa.perm = perm; fa.eps = io.eps; fa.max_rank = io.max_rank; fa.status = io.status;
+      fa.carry = spec_st + 2; fa.T = Tst; fa.Gout = G;
+      k_finish<<<1, kThreads, 0, s>>>(fa);
+      QTT_CUDA_TRY(cudaGetLastError());
+    }
+    // 4. carry slabs U_k^T T_t
+    for (int sl = 0; sl < P.ls; ++sl) {
+      char *sb = shard_base(sl);
+      GemmSpec *cs = (GemmSpec *)(sb + P.so_spec) + 3;
+      CarrySpecArgs ca{dims_st, (SiteDims *)(sb + P.so_dims), Cq, (double *)(sb + P.so_T),
+                       comm->send_c + (size_t)sl * P.c_elems, sc, cs};
+      k_shard_carry_spec<<<1, 32, 0, s>>>(ca);
+      QTT_CUDA_TRY(cudaGetLastError());
+      launch_gemm_spec(cs, S.cap[q + 1], sc, 1, w2, false, false, s);
+      QTT_CUDA_TRY(cudaGetLastError());
+    }
+    // 5. exchange the carry slabs, assemble the full carry
+    st = shard_exchange(comm, 1, P, s);
+    if (st != QTT_OK) return st;
+    {
+      AssembleArgs aa{dims_st, comm->recv_c, P.c_elems, P.S, sc, G};
+      const long long ne = (long long)S.cap[q + 1] * w2 * S.xr[q + 1];
+      k_shard_assemble<<<(unsigned)std::max<long long>(1, std::min<long long>((ne + 255) / 256, 8192)), 256, 0, s>>>(aa);
+      QTT_CUDA_TRY(cudaGetLastError());
+    }
+  }
+  return QTT_OK;
+}
+
 }  // namespace qtt
 
+
+using namespace qtt;
+
+static qtt_status_t sharded_check(const char *subs, const qtt_trains_t *op, const qtt_trains_t *x, int32_t max_rank,
+                                  int32_t world, int32_t ls, Shape &S) {
+  if (!x || x->dtype != QTT_F64 || (op && op->dtype != QTT_F64)) {
+    set_error("qtt_zipup_sharded: QTT_F64 trains only");
+    return QTT_EUNSUPPORTED;
+  }
+  qtt_status_t st = qtt_zipup_analyse(subs, op, x, max_rank, S);
+  if (st != QTT_OK) return st;
+  if (S.B != 1) { set_error("qtt_zipup_sharded: batch must be 1 (one zip-up split across processes)"); return QTT_EUNSUPPORTED; }
+  if (world < 1 || ls < 1) { set_error("qtt_zipup_sharded: world %d / local_shards %d", world, ls); return QTT_EINVAL; }
+  return QTT_OK;
+}
+
+extern "C" {
+
+qtt_status_t qtt_zipup_sharded_sizes(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x,
+                                     int32_t max_rank, int32_t world, int32_t local_shards, size_t *r_elems,
+                                     size_t *c_elems, size_t *workspace_bytes) {
+  Shape S;
+  qtt_status_t st = sharded_check(subscripts, op, x, max_rank, world, local_shards, S);
+  if (st != QTT_OK) return st;
+  return sharded_sizes(S, world, local_shards, 0, r_elems, c_elems, workspace_bytes);
+}
+
+qtt_status_t qtt_zipup_sharded(const char *subscripts, const qtt_trains_t *op, const qtt_trains_t *x, double eps,
+                               int32_t max_rank, uint32_t flags, const qtt_trains_t *out, int32_t *out_ranks,
+                               double *delta2, double *norm2, int32_t *status, double *sigma, int32_t sigma_stride,
+                               const qtt_shard_comm_t *comm, void *workspace, size_t workspace_bytes,
+                               void *stream) {
+  if (!(eps >= 0.0 && eps < 1.0)) { set_error("eps %g outside [0,1)", eps); return QTT_EINVAL; }
+  if (flags & QTT_WINDOW2) { set_error("qtt_zipup_sharded: window 1 only"); return QTT_EUNSUPPORTED; }
+  if (!comm) { set_error("comm is NULL"); return QTT_EINVAL; }
+  Shape S;
+  qtt_status_t st = sharded_check(subscripts, op, x, max_rank, comm->world, comm->local_shards, S);
+  if (st != QTT_OK) return st;
+  if (comm->rank < 0 || comm->rank >= comm->world) { set_error("rank %d outside [0, %d)", comm->rank, comm->world); return QTT_EINVAL; }
+  if (comm->world > 1 && !comm->allgather) { set_error("world > 1 needs an allgather callback"); return QTT_EINVAL; }
+  if (!comm->send_r || !comm->recv_r || !comm->send_c || !comm->recv_c) { set_error("NULL exchange buffer"); return QTT_EINVAL; }
+  if (!out || !out->cores || !out->ranks || !out_ranks || !delta2 || !norm2 || !status) {
+    set_error("NULL output argument");
+    return QTT_EINVAL;
+  }
+  if (out->n_sites != S.L || out->batch != 1 || out->n_legs != 1) { set_error("output train shape mismatch"); return QTT_ESHAPE; }
+  for (int q = 0; q <= S.L; ++q)
+    if (out->ranks[q] < S.cap[q]) {
+      set_error("output capacity %d at bond %d below required %d", out->ranks[q], q, S.cap[q]);
+      return QTT_ECAPACITY;
+    }
+  if (sigma && sigma_stride < 1) { set_error("sigma_stride < 1"); return QTT_EINVAL; }
+  cudaStream_t s = (cudaStream_t)stream;
+  QTT_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), s));
+  LargeIO io{out, out_ranks, delta2, norm2, sigma, sigma_stride, nullptr, status, eps, max_rank};
+  return large_zipup_sharded(S, op, x, flags, io, comm, workspace, workspace_bytes, s);
+}
+
+}  // extern "C"

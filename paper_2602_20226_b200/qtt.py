@@ -50,6 +50,7 @@ _lib = None
 SYMBOLS = ["qtt_zipup_capacity", "qtt_zipup_workspace_bytes", "qtt_zipup_workspace_bytes_flags", "qtt_zipup",
            "qtt_zipup_summary", "qtt_variational_workspace_bytes", "qtt_variational",
            "qtt_variational_workspace_bytes_ex", "qtt_variational_ex",
+           "qtt_zipup_sharded_sizes", "qtt_zipup_sharded",
            "qtt_round_capacity", "qtt_round_workspace_bytes", "qtt_round",
            "qtt_einsum_exact", "qtt_inner_workspace_bytes", "qtt_inner", "qtt_to_dense_workspace_bytes",
            "qtt_to_dense", "qtt_last_error", "qtt_version"]
@@ -82,6 +83,11 @@ def load_library(path: str = LIB_PATH):
     L.qtt_variational_workspace_bytes_ex.restype = sz
     L.qtt_variational_ex.argtypes = [ctypes.c_char_p, P, P, P, vp, P, vp, i32, i32, f64, i32, vp, vp, vp, sz, vp]
     L.qtt_variational_ex.restype = i32
+    L.qtt_zipup_sharded_sizes.argtypes = [ctypes.c_char_p, P, P, i32, i32, i32, vp, vp, vp]
+    L.qtt_zipup_sharded_sizes.restype = i32
+    L.qtt_zipup_sharded.argtypes = [ctypes.c_char_p, P, P, f64, i32, ctypes.c_uint32, P, vp, vp, vp, vp, vp, i32,
+                                    vp, vp, sz, vp]
+    L.qtt_zipup_sharded.restype = i32
     L.qtt_zipup_summary.argtypes = [i32, i32, vp, vp, vp, vp, vp]
     L.qtt_zipup_summary.restype = i32
     L.qtt_round_capacity.argtypes = [P, i32, ctypes.POINTER(i32)]

@@ -10,13 +10,13 @@ from paper_2602_20226_b200 import gen
 pytestmark = pytest.mark.gpu
 
 
-def _run(lib, kind, op, x, eps, max_rank, sweeps, mpo=False, **vkw):
+def _run(lib, kind, op, x, eps, max_rank, sweeps, mpo=False, vkw=None):
     import torch
     subs = {"matvec": "ij,j->i", "hadamard": "i,i->i", "truncate": "i->i"}[kind]
     xd = lib.to_device(x)
     od = None if op is None else lib.to_device(op, mpo=mpo)
     z = lib.ZipupPlan(subs, od, xd, eps, max_rank).run(od, xd)
-    v = lib.variational(subs, od, xd, z, sweeps, **vkw)
+    v = lib.variational(subs, od, xd, z, sweeps, **(vkw or {}))
     torch.cuda.synchronize()
     assert int(z.status.item()) == 0 and int(v.status.item()) == 0
     return z, v
@@ -86,7 +86,7 @@ def test_variational_two_site_random(lib, kind):
     x = gen.random_mps(dims, 9, rng).cores
     op = {"matvec": gen.random_mpo(dims, 3, rng, 0.5).cores, "hadamard": gen.random_mps(dims, 3, rng).cores,
           "truncate": None}[kind]
-    z, v = _run(lib, kind, op, x, 0.2, 4, 2, mpo=(kind == "matvec"), ncores=2, eps=0.0, max_rank=8)
+    z, v = _run(lib, kind, op, x, 0.2, 4, 2, mpo=(kind == "matvec"), vkw=dict(ncores=2, eps=0.0, max_rank=8))
     _check(lib, kind, op, x, z, v, 2, ncores=2, eps=0.0, max_rank=8)
     assert max(v.ranks[0].cpu().tolist()) > 4          # the ranks adapted beyond the seed's
 
@@ -98,9 +98,9 @@ def test_variational_two_site_cutoff_and_paper_call(lib):
     dims = [2] * 10
     x = gen.random_mps(dims, 6, rng).cores
     op = gen.random_mpo(dims, 2, rng, 0.5).cores
-    z, v = _run(lib, "matvec", op, x, 0.3, 2, 2, mpo=True, ncores=2, eps=0.0, max_rank=8)
+    z, v = _run(lib, "matvec", op, x, 0.3, 2, 2, mpo=True, vkw=dict(ncores=2, eps=0.0, max_rank=8))
     _check(lib, "matvec", op, x, z, v, 2, ncores=2, eps=0.0, max_rank=8)
-    z, v = _run(lib, "matvec", op, x, 0.3, 2, 2, mpo=True, ncores=2, eps=1e-3, max_rank=0)
+    z, v = _run(lib, "matvec", op, x, 0.3, 2, 2, mpo=True, vkw=dict(ncores=2, eps=1e-3, max_rank=0))
     _check(lib, "matvec", op, x, z, v, 2, ncores=2, eps=1e-3, max_rank=0)
 
 
@@ -108,5 +108,5 @@ def test_variational_two_site_cfg5_member(lib):
     """configs[4] shapes seeded with a max-rank-8 zip-up, two-site sweep to max rank 16."""
     probs, xs, ops = gen.cfg5_batch_arrays([4])
     p = probs[0]
-    z, v = _run(lib, "matvec", p.op.cores, p.x.cores, 1e-10, 8, 1, mpo=True, ncores=2, eps=0.0, max_rank=16)
+    z, v = _run(lib, "matvec", p.op.cores, p.x.cores, 1e-10, 8, 1, mpo=True, vkw=dict(ncores=2, eps=0.0, max_rank=16))
     _check(lib, "matvec", p.op.cores, p.x.cores, z, v, 1, dense=False, ncores=2, eps=0.0, max_rank=16)
