@@ -26,6 +26,8 @@ struct GemmSpec {
   double *C;
   long long sam, sak, sbk, sbn, scm, scn;
   long long sa1, sa2, sb1, sb2, sc1, sc2;
+  int kchunk;        // > 0: split-K -- batch index z1 takes K range [z1 kchunk, (z1+1) kchunk)
+                     // (the caller sets sa1 = kchunk sak, sb1 = kchunk sbk, sc1 = the partial stride)
 };
 
 namespace dgemm {
@@ -53,11 +55,24 @@ __device__ __forceinline__ void dmma_884(double &c0, double &c1, double a, doubl
 }
 
 // grid: x = tiles_m * tiles_n (capacity), z = nz1cap * nz2cap; block = 256 threads.
-template <bool A_KCONTIG>
+// B_KCONTIG: B is K-contiguous (sbk == 1, e.g. the transposed operand of a Gram matrix T T^T).
+template <bool A_KCONTIG, bool B_KCONTIG = false>
 __global__ void __launch_bounds__(256, 1) k_gemm_dmma(const GemmSpec *spec, int tiles_n, int nz2_cap) {
   using namespace dgemm;
   extern __shared__ double gsm[];
-  const GemmSpec g = *spec;
+  GemmSpec g = *spec;
+  if (g.kchunk > 0) g.K = min(g.kchunk, g.K - (int)(blockIdx.z / nz2_cap) * g.kchunk);
+  if (g.K <= 0) {                                   // empty K chunk: a zero partial
+    const int z1 = blockIdx.z / nz2_cap, z2 = blockIdx.z % nz2_cap;
+    if (z1 >= g.nz1 || z2 >= g.nz2) return;
+    const int m0 = (blockIdx.x / tiles_n) * TM, n0 = (blockIdx.x % tiles_n) * TN;
+    double *C = g.C + z1 * g.sc1 + z2 * g.sc2;
+    for (int idx = threadIdx.x; idx < TM * TN; idx += 256) {
+      const int gm = m0 + idx / TN, gn = n0 + idx % TN;
+      if (gm < g.M && gn < g.N) C[(long long)gm * g.scm + (long long)gn * g.scn] = 0.0;
+    }
+    return;
+  }
   const int z1 = blockIdx.z / nz2_cap, z2 = blockIdx.z % nz2_cap;
   if (z1 >= g.nz1 || z2 >= g.nz2) return;
   const int m0 = (blockIdx.x / tiles_n) * TM, n0 = (blockIdx.x % tiles_n) * TN;
@@ -91,7 +106,15 @@ __global__ void __launch_bounds__(256, 1) k_gemm_dmma(const GemmSpec *spec, int 
         cp_async8(as + k * LDA_M + mh + e, ok ? A + (long long)gm * g.sam + (long long)gk * g.sak : A, ok);
       }
     }
-    {                         // Bs[k][n]: thread -> k = tid/16, 8 consecutive n
+    if (B_KCONTIG) {          // Bs[k][n] from K-contiguous B: thread -> n = tid/2, 8 consecutive k
+      const int n = tid >> 1, kh = (tid & 1) * 8, gn = n0 + n;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int gk = k0 + kh + e;
+        const bool ok = gn < g.N && gk < g.K;
+        cp_async8(bs + (kh + e) * LDB + n, ok ? B + (long long)gn * g.sbn + gk : B, ok);
+      }
+    } else {                  // Bs[k][n]: thread -> k = tid/16, 8 consecutive n
       const int k = tid >> 4, nh = (tid & 15) * 8, gk = k0 + k;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {

@@ -159,8 +159,9 @@ __global__ void k_mpo_apply(const SiteDims *dims, const double *X, const double 
   }
 }
 
-__global__ void k_copy_T(const SiteDims *dims, const double *T, double *Tw, double *A) {
+__global__ void k_copy_T(const SiteDims *dims, const double *T, double *Tw, double *A, const int *skip = nullptr) {
   const SiteDims D = *dims;
+  if (!D.direct && skip && *skip) return;        // CholeskyQR2 produced R: the Householder copy is not needed
   const long long total = (long long)D.m * D.n;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -172,6 +173,66 @@ __global__ void k_copy_T(const SiteDims *dims, const double *T, double *Tw, doub
       Tw[idx] = v;
     }
   }
+}
+
+// ------------------------------------------------------------------ a3: CholeskyQR2 (cholqr.cuh)
+}  // namespace qtt
+#include "cholqr.cuh"
+namespace qtt {
+
+struct CqPlanArgs {
+  const SiteDims *dims;
+  int S, mmin;
+  const double *T;
+  double *Tw, *P, *Rinv, *R1, *R2, *Rout;
+  long long pstride;
+  GemmSpec *spec;          // [4]
+  int *ok, *mdim;
+  double *dev;
+};
+
+// decides whether the site takes CholeskyQR2 (wide: m <= n, m >= mmin) and fills its GEMM specs
+__global__ void k_cq_plan(CqPlanArgs a) {
+  if (threadIdx.x != 0) return;
+  const SiteDims D = *a.dims;
+  const int m = D.m, n = D.n;
+  const int use = (!D.direct && m >= a.mmin && m <= n) ? 1 : 0;
+  *a.ok = use;
+  *a.mdim = use ? m : 0;
+  *a.dev = 0.0;
+  const int kc = ((n + a.S - 1) / a.S + 15) / 16 * 16;
+  GemmSpec g{};
+  // [0] P_s = T[:, chunk s] T[:, chunk s]^T   (A = T K-contiguous, B = T^T K-contiguous)
+  g.M = use ? m : 0; g.N = m; g.K = n; g.nz1 = a.S; g.nz2 = 1; g.kchunk = kc;
+  g.A = a.T; g.sam = n; g.sak = 1; g.sa1 = kc;
+  g.B = a.T; g.sbk = 1; g.sbn = n; g.sb1 = kc;
+  g.C = a.P; g.scm = m; g.scn = 1; g.sc1 = a.pstride;
+  a.spec[0] = g;
+  // [1] Q1^T = Rinv^T T (m x n): A[i][k] = Rinv[k][i] (M-contiguous), B = T
+  GemmSpec h{};
+  h.M = use ? m : 0; h.N = n; h.K = m; h.nz1 = 1; h.nz2 = 1;
+  h.A = a.Rinv; h.sam = 1; h.sak = m;
+  h.B = a.T; h.sbk = n; h.sbn = 1;
+  h.C = a.Tw; h.scm = n; h.scn = 1;
+  a.spec[1] = h;
+  // [2] P_s = Q1^T Q1 partials
+  GemmSpec g2 = g;
+  g2.A = a.Tw; g2.B = a.Tw;
+  a.spec[2] = g2;
+  // [3] R = R2 R1 (row-major, ld m) -> Rout
+  GemmSpec r{};
+  r.M = use ? m : 0; r.N = m; r.K = m; r.nz1 = 1; r.nz2 = 1;
+  r.A = a.R2; r.sam = m; r.sak = 1;
+  r.B = a.R1; r.sbk = m; r.sbn = 1;
+  r.C = a.Rout; r.scm = m; r.scn = 1;
+  a.spec[3] = r;
+}
+
+// after a Cholesky: when the gate closed, the remaining CholeskyQR2 GEMMs become empty
+__global__ void k_cq_gate(const int *ok, GemmSpec *spec, int from) {
+  if (threadIdx.x != 0) return;
+  if (*ok == 0)
+    for (int i = from; i < 4; ++i) spec[i].M = 0;
 }
 
 // ------------------------------------------------------------------ a3: cooperative QR
@@ -193,6 +254,7 @@ struct QrArgs {
   double *bc;          // broadcast row-j values of the panel columns [2][32] (column parity)
   GridBar *bar;
   int G, RB, mcap;
+  const int *skip;     // non-NULL and set: R already computed (CholeskyQR2 accepted): return
 };
 
 // Reduce a per-CTA scalar triple of arrays: block sum of v over kThreads.
@@ -202,6 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qr_coop(QrArgs a) {
   extern __shared__ double smq[];
   const SiteDims D = *a.dims;
   if (D.direct) return;                         // uniform across the grid
+  if (a.skip && *a.skip) return;
   const int m = D.m, n = D.n, g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r0 = g * a.RB, r1 = min(n, r0 + a.RB), nr = max(0, r1 - r0);
   double *P = smq;                              // [kNb][RB] panel (my rows)
@@ -911,7 +974,12 @@ struct SweepPlan {
   size_t qr_smem, jac_smem;
   size_t off_G, off_X, off_T, off_Tw, off_A, off_part, off_wtot, off_gram, off_bc, off_s2, off_perm, off_flags,
       off_ver, off_sw, off_bar, off_dims, off_spec, total;
+  // CholeskyQR2 (cholqr.cuh) for the wide sites
+  int cq, cq_S, cq_nblk, cq_G;
+  size_t off_cqP, off_cqR1, off_cqR2, off_cqRinv, off_cqDinv, off_cqI, off_cqDev, off_cqSpec;
 };
+
+constexpr int kCqMinRows = 64;        // smaller site matrices keep the Householder QR (cheap there)
 
 static qtt_status_t plan_sweep(int L, const std::vector<int> &d, const std::vector<int> &dj, const std::vector<int> &xr,
                                const std::vector<int> &orr, const std::vector<int> &cap, int kind, SweepPlan &P) {
@@ -961,6 +1029,23 @@ static qtt_status_t plan_sweep(int L, const std::vector<int> &d, const std::vect
   P.off_bar = take(sizeof(GridBar) * 2);
   P.off_dims = take(sizeof(SiteDims));
   P.off_spec = take(sizeof(GemmSpec) * 3);
+  // CholeskyQR2: only when some site can be wide with m >= kCqMinRows
+  P.cq = (P.mcap >= kCqMinRows && getenv("QTT_NO_CHOLQR") == nullptr) ? 1 : 0;
+  if (P.cq) {
+    const long long tiles = ((P.mcap + dgemm::TM - 1) / dgemm::TM) * ((P.mcap + dgemm::TN - 1) / dgemm::TN);
+    P.cq_S = (int)std::max<long long>(1, std::min<long long>(16, g_sms / tiles));
+    P.cq_nblk = (int)((P.mcap + kCholNb - 1) / kCholNb);
+    P.cq_G = (int)std::min<long long>(g_sms, std::max<long long>(1, (long long)P.cq_nblk * (P.cq_nblk + 1) / 2));
+    const size_t m2 = (size_t)P.mcap * P.mcap;
+    P.off_cqP = take(8 * m2 * P.cq_S);
+    P.off_cqR1 = take(8 * m2);
+    P.off_cqR2 = take(8 * m2);
+    P.off_cqRinv = take(8 * m2);
+    P.off_cqDinv = take(8 * (size_t)P.cq_nblk * kCholNb * kCholNb);
+    P.off_cqI = take(4 * 4);
+    P.off_cqDev = take(8 * 2);
+    P.off_cqSpec = take(sizeof(GemmSpec) * 4);
+  }
   P.total = off;
   return QTT_OK;
 }
@@ -1009,6 +1094,8 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
                                       (int)dgemm::SMEM_BYTES));
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_dmma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)dgemm::SMEM_BYTES));
+    QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_dmma<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)dgemm::SMEM_BYTES));
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_tf32<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)tf32g::SMEM_BYTES));
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_tf32<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1048,13 +1135,58 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
       if (io.sweeps) QTT_CUDA_TRY(cudaMemsetAsync(io.sweeps + q, 0, sizeof(int), s));
       break;
     }
-    // a3
-    k_copy_T<<<ew_grid, kThreads, 0, s>>>(Bf.dims, Bf.T, Bf.Tw, Bf.A);
+    // a3: CholeskyQR2 when the gate accepts the site, else the Householder QR
+    int *cq_ok = nullptr;
+    if (P.cq) {
+      cq_ok = (int *)(ws + P.off_cqI);
+      int *cq_m = cq_ok + 1;
+      double *cq_dev = (double *)(ws + P.off_cqDev);
+      GemmSpec *cs = (GemmSpec *)(ws + P.off_cqSpec);
+      double *R1 = (double *)(ws + P.off_cqR1), *R2 = (double *)(ws + P.off_cqR2);
+      double *Rinv = (double *)(ws + P.off_cqRinv), *Dinv = (double *)(ws + P.off_cqDinv);
+      double *Pp = (double *)(ws + P.off_cqP);
+      const long long m2 = P.mcap * P.mcap;
+      CqPlanArgs ca{Bf.dims, P.cq_S, kCqMinRows, Bf.T, Bf.Tw, Pp, Rinv, R1, R2, Bf.A, m2, cs, cq_ok, cq_m, cq_dev};
+      k_cq_plan<<<1, 32, 0, s>>>(ca);
+      QTT_CUDA_TRY(cudaGetLastError());
+      const long long mc = std::min<long long>(m_cap, n_cap);
+      const long long tm = (mc + dgemm::TM - 1) / dgemm::TM, tn = tm;
+      const unsigned rgrid = (unsigned)std::min<long long>((mc * mc + 255) / 256, 2048);
+      auto gram = [&](int which, double *Wout, double *dev) -> qtt_status_t {
+        k_gemm_dmma<true, true><<<dim3((unsigned)(tm * tn), 1, (unsigned)P.cq_S), 256, dgemm::SMEM_BYTES, s>>>(
+            cs + which, (int)tn, 1);
+        QTT_CUDA_TRY(cudaGetLastError());
+        RedArgs ra{Pp, m2, P.cq_S, cq_m, cq_ok, Wout, dev};
+        k_gram_reduce<<<rgrid, kThreads, 0, s>>>(ra);
+        QTT_CUDA_TRY(cudaGetLastError());
+        return QTT_OK;
+      };
+      auto chol = [&](double *W, double *dev) -> qtt_status_t {
+        CholArgs ch{W, Dinv, cq_m, cq_ok, dev, 0.25, Bf.bar, P.cq_G};
+        return coop_launch((const void *)k_chol_coop, P.cq_G, 0, &ch, s);
+      };
+      qtt_status_t st = gram(0, R1, nullptr);                          // W = T T^T
+      if (st == QTT_OK) st = chol(R1, nullptr);                        // R1
+      if (st != QTT_OK) return st;
+      k_cq_gate<<<1, 32, 0, s>>>(cq_ok, cs, 1);
+      TrinvArgs ta{R1, Dinv, Rinv, cq_m, cq_ok};
+      k_trinv<<<(unsigned)P.cq_nblk, kThreads, 0, s>>>(ta);            // Rinv = R1^-1
+      QTT_CUDA_TRY(cudaGetLastError());
+      launch_gemm_spec(cs + 1, mc, n_cap, 1, 1, false, false, s);      // Q1^T = Rinv^T T -> Tw
+      QTT_CUDA_TRY(cudaGetLastError());
+      st = gram(2, R2, cq_dev);                                        // W2 = Q1^T Q1, |W2 - I|_F^2
+      if (st == QTT_OK) st = chol(R2, cq_dev);                         // R2 (gate |W2 - I|_F <= 1/2)
+      if (st != QTT_OK) return st;
+      k_cq_gate<<<1, 32, 0, s>>>(cq_ok, cs, 3);
+      k_gemm_dmma<true, false><<<dim3((unsigned)(tm * tn), 1, 1), 256, dgemm::SMEM_BYTES, s>>>(cs + 3, (int)tn, 1);
+      QTT_CUDA_TRY(cudaGetLastError());                                // R = R2 R1 -> A
+    }
+    k_copy_T<<<ew_grid, kThreads, 0, s>>>(Bf.dims, Bf.T, Bf.Tw, Bf.A, cq_ok);
     QTT_CUDA_TRY(cudaGetLastError());
     {
       QrArgs qa;
       qa.dims = Bf.dims; qa.Tw = Bf.Tw; qa.Rout = Bf.A; qa.part = Bf.part; qa.wtot = Bf.wtot; qa.gram = Bf.gram;
-      qa.bc = Bf.bc; qa.bar = Bf.bar; qa.G = P.Gqr; qa.RB = P.RB; qa.mcap = (int)P.mcap;
+      qa.bc = Bf.bc; qa.bar = Bf.bar; qa.G = P.Gqr; qa.RB = P.RB; qa.mcap = (int)P.mcap; qa.skip = cq_ok;
       qtt_status_t st = coop_launch((const void *)k_qr_coop, P.Gqr, P.qr_smem, &qa, s);
       if (st != QTT_OK) return st;
     }
@@ -1685,7 +1817,7 @@ qtt_status_t large_zipup_sharded(const Shape &S, const qtt_trains_t *op, const q
       QTT_CUDA_TRY(cudaGetLastError());
       QrArgs qa;
       qa.dims = dims; qa.Tw = Tw; qa.Rout = A; qa.part = part; qa.wtot = wtot; qa.gram = gram;
-      qa.bc = bc; qa.bar = bar; qa.G = P.Gqr_s; qa.RB = P.RB_s; qa.mcap = (int)P.mcap;
+      qa.bc = bc; qa.bar = bar; qa.G = P.Gqr_s; qa.RB = P.RB_s; qa.mcap = (int)P.mcap; qa.skip = nullptr;
       st = coop_launch((const void *)k_qr_coop, P.Gqr_s, P.qr_smem, &qa, s);
       if (st != QTT_OK) return st;
       const long long fe = P.r_elems;
@@ -1706,7 +1838,7 @@ qtt_status_t large_zipup_sharded(const Shape &S, const qtt_trains_t *op, const q
       QTT_CUDA_TRY(cudaGetLastError());
       QrArgs qa;
       qa.dims = dims_st; qa.Tw = Tst; qa.Rout = Ast; qa.part = part; qa.wtot = wtot; qa.gram = gram;
-      qa.bc = bc; qa.bar = bar; qa.G = P.Gqr_st; qa.RB = P.RB_st; qa.mcap = (int)P.mcap;
+      qa.bc = bc; qa.bar = bar; qa.G = P.Gqr_st; qa.RB = P.RB_st; qa.mcap = (int)P.mcap; qa.skip = nullptr;
       st = coop_launch((const void *)k_qr_coop, P.Gqr_st, P.qr_smem, &qa, s);
       if (st != QTT_OK) return st;
       JacArgs ja;

@@ -419,13 +419,20 @@ def variational(subscripts: str, op: Optional[DeviceTrains], x: DeviceTrains, se
     n = x.n_sites
     d = list(seed.out.d_out)
     if capacity is None:
-        if ncores == 2 and max_rank > 0:
+        if ncores == 2:
+            # the largest rank a split can keep at bond q: min(max_rank, the digit products on
+            # either side, the bond of the exact product w_q r_q) -- and at least the seed's
             left, right = [1], [1]
             for q in range(n):
                 left.append(left[-1] * d[q])
                 right.append(right[-1] * d[n - 1 - q])
-            capacity = [min(max(max_rank, seed.out.ranks[q]), left[q], right[n - q]) for q in range(n + 1)]
-            capacity = [max(c, s) for c, s in zip(capacity, seed.out.ranks)]
+            exact = [a * b for a, b in zip(op.ranks, x.ranks)] if op is not None else list(x.ranks)
+            capacity = []
+            for q in range(n + 1):
+                c = min(left[q], right[n - q], exact[q])
+                if max_rank > 0:
+                    c = min(c, max_rank)
+                capacity.append(max(c, seed.out.ranks[q]))
         else:
             capacity = list(seed.out.ranks)
     dev = x.cores[0].device
