@@ -159,9 +159,11 @@ __global__ void k_mpo_apply(const SiteDims *dims, const double *X, const double 
   }
 }
 
-__global__ void k_copy_T(const SiteDims *dims, const double *T, double *Tw, double *A, const int *skip = nullptr) {
+__global__ void k_copy_T(const SiteDims *dims, const double *T, double *Tw, double *A, const int *skip = nullptr,
+                         const int *skip_tall = nullptr) {
   const SiteDims D = *dims;
   if (!D.direct && skip && *skip) return;        // CholeskyQR2 produced R: the Householder copy is not needed
+  if (D.direct && skip_tall && *skip_tall) return;   // tall CholeskyQR2 orthonormalised the site: no Jacobi
   const long long total = (long long)D.m * D.n;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -228,11 +230,74 @@ __global__ void k_cq_plan(CqPlanArgs a) {
   a.spec[3] = r;
 }
 
+// Tall variant for the exact orthonormalisation sweeps (a1: truncate with eps = 0, the site
+// matrix T with m > n): T = Q R by CholeskyQR2 with Q explicit; the output core is Q (m x n,
+// the SVD path's U_p up to an orthogonal n x n gauge -- a1's result is gauge-invariant, c-A3) and
+// the carry is R, so no Jacobi runs.  Specs: [0] P_s = T^T T partials, [1] Q1 = T Rinv1 -> Tw,
+// [2] P_s = Q1^T Q1 partials, [3] Q = Q1 Rinv2 -> C_q, [4] R = R2 R1 -> G.
+struct CqtPlanArgs {
+  const SiteDims *dims;
+  int S, nmin;
+  const double *T;
+  double *Tw, *P, *Rinv, *R1, *R2, *Cq, *Gout;
+  long long pstride;
+  GemmSpec *spec;          // [5]
+  int *ok, *ndim;
+  double *dev;
+};
+__global__ void k_cqt_plan(CqtPlanArgs a) {
+  if (threadIdx.x != 0) return;
+  const SiteDims D = *a.dims;
+  const int m = D.m, n = D.n;
+  const int use = (D.direct && n >= a.nmin && m > n) ? 1 : 0;
+  *a.ok = use;
+  *a.ndim = use ? n : 0;
+  *a.dev = 0.0;
+  const int kc = ((m + a.S - 1) / a.S + 15) / 16 * 16;
+  GemmSpec g{};            // [0] T^T T: A[i][k] = T[k][i] (M-contiguous), B = T
+  g.M = use ? n : 0; g.N = n; g.K = m; g.nz1 = a.S; g.nz2 = 1; g.kchunk = kc;
+  g.A = a.T; g.sam = 1; g.sak = n; g.sa1 = (long long)kc * n;
+  g.B = a.T; g.sbk = n; g.sbn = 1; g.sb1 = (long long)kc * n;
+  g.C = a.P; g.scm = n; g.scn = 1; g.sc1 = a.pstride;
+  a.spec[0] = g;
+  GemmSpec h{};            // [1] Q1 = T Rinv (m x n)
+  h.M = use ? m : 0; h.N = n; h.K = n; h.nz1 = 1; h.nz2 = 1;
+  h.A = a.T; h.sam = n; h.sak = 1;
+  h.B = a.Rinv; h.sbk = n; h.sbn = 1;
+  h.C = a.Tw; h.scm = n; h.scn = 1;
+  a.spec[1] = h;
+  GemmSpec g2 = g;         // [2] Q1^T Q1
+  g2.A = a.Tw; g2.B = a.Tw;
+  a.spec[2] = g2;
+  GemmSpec q = h;          // [3] Q = Q1 Rinv2 -> the output core
+  q.A = a.Tw; q.C = a.Cq;
+  a.spec[3] = q;
+  GemmSpec r{};            // [4] R = R2 R1 -> the carry (n x n)
+  r.M = use ? n : 0; r.N = n; r.K = n; r.nz1 = 1; r.nz2 = 1;
+  r.A = a.R2; r.sam = n; r.sak = 1;
+  r.B = a.R1; r.sbk = n; r.sbn = 1;
+  r.C = a.Gout; r.scm = n; r.scn = 1;
+  a.spec[4] = r;
+}
+
+// the tall site's a5/a6 bookkeeping when CholeskyQR2 was accepted: rank n, nothing discarded,
+// the carry already in G (the sweep's own carry GEMM becomes empty)
+__global__ void k_cqt_finish(const int *ok, SiteDims *dims, int *yr_next, double *delta2, GemmSpec *carry,
+                             int *sweeps) {
+  if (threadIdx.x != 0 || *ok == 0) return;
+  const int n = dims->n;
+  dims->k = n;
+  *yr_next = n;
+  *delta2 = 0.0;
+  carry->M = 0;
+  if (sweeps) *sweeps = 0;
+}
+
 // after a Cholesky: when the gate closed, the remaining CholeskyQR2 GEMMs become empty
-__global__ void k_cq_gate(const int *ok, GemmSpec *spec, int from) {
+__global__ void k_cq_gate(const int *ok, GemmSpec *spec, int from, int count = 4) {
   if (threadIdx.x != 0) return;
   if (*ok == 0)
-    for (int i = from; i < 4; ++i) spec[i].M = 0;
+    for (int i = from; i < count; ++i) spec[i].M = 0;
 }
 
 // ------------------------------------------------------------------ a3: cooperative QR
@@ -445,6 +510,7 @@ struct JacArgs {
   int G, WB;               // CTAs, block width (columns)
   int *sweeps_out;
   int *status;
+  const int *skip;         // non-NULL and set: the site was orthonormalised by CholeskyQR2 (a1 sweeps)
 };
 
 // One Jacobi pair (one warp): exact dot product, column norms nrm_i / nrm_j carried in shared
@@ -654,6 +720,7 @@ __device__ __forceinline__ void block_copy_out(const double *src, double *A, int
 
 __global__ void __launch_bounds__(kThreads, 1) k_jacobi_coop(JacArgs a) {
   extern __shared__ double smj[];
+  if (a.skip && *a.skip) return;                        // uniform
   const SiteDims D = *a.dims;
   const int m = D.m, p = D.p, WB = a.WB, g = blockIdx.x, tid = threadIdx.x, warp = tid >> 5;
   const int NB = 2 * ((p + 2 * WB - 1) / (2 * WB));     // even number of blocks
@@ -812,10 +879,12 @@ struct FinishArgs {
   GemmSpec *carry;        // spec[2]: G' = Cq^T T
   const double *T;
   double *Gout;
+  const int *skip;        // non-NULL and set: the site was done by CholeskyQR2 (a1 sweeps)
 };
 
 __global__ void __launch_bounds__(kThreads, 1) k_finish(FinishArgs a) {
   __shared__ double sc[4];
+  if (a.skip && *a.skip) return;
   SiteDims D = *a.dims;
   const int m = D.m, p = D.p, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int j = warp; j < p; j += kWarps) {
@@ -1044,7 +1113,7 @@ static qtt_status_t plan_sweep(int L, const std::vector<int> &d, const std::vect
     P.off_cqDinv = take(8 * (size_t)P.cq_nblk * kCholNb * kCholNb);
     P.off_cqI = take(4 * 4);
     P.off_cqDev = take(8 * 2);
-    P.off_cqSpec = take(sizeof(GemmSpec) * 4);
+    P.off_cqSpec = take(sizeof(GemmSpec) * 9);     // [0..3] wide, [4..8] tall
   }
   P.total = off;
   return QTT_OK;
@@ -1135,6 +1204,57 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
       if (io.sweeps) QTT_CUDA_TRY(cudaMemsetAsync(io.sweeps + q, 0, sizeof(int), s));
       break;
     }
+    // a1 sweeps (truncate, eps = 0): tall sites orthonormalised by CholeskyQR2 with Q explicit
+    int *cqt_ok = nullptr;
+    if (P.cq && kind == TRUNCATE && io.eps == 0.0 && io.max_rank <= 0 && !io.sigma) {
+      cqt_ok = (int *)(ws + P.off_cqI) + 2;
+      int *cqt_n = cqt_ok + 1;
+      double *cq_dev = (double *)(ws + P.off_cqDev) + 1;
+      GemmSpec *cs = (GemmSpec *)(ws + P.off_cqSpec) + 4;
+      double *R1 = (double *)(ws + P.off_cqR1), *R2 = (double *)(ws + P.off_cqR2);
+      double *Rinv = (double *)(ws + P.off_cqRinv), *Dinv = (double *)(ws + P.off_cqDinv);
+      double *Pp = (double *)(ws + P.off_cqP);
+      const long long m2 = P.mcap * P.mcap;
+      CqtPlanArgs ta{Bf.dims, P.cq_S, 32, Bf.T, Bf.Tw, Pp, Rinv, R1, R2, io.Cq[q], Bf.G, m2, cs, cqt_ok, cqt_n, cq_dev};
+      k_cqt_plan<<<1, 32, 0, s>>>(ta);
+      QTT_CUDA_TRY(cudaGetLastError());
+      const long long nc = std::min<long long>(m_cap, n_cap);
+      const long long tn = (nc + dgemm::TM - 1) / dgemm::TM;
+      const unsigned rgrid = (unsigned)std::min<long long>((nc * nc + 255) / 256, 2048);
+      auto gram = [&](int which, double *Wout, double *dev) -> qtt_status_t {
+        k_gemm_dmma<false, false><<<dim3((unsigned)(tn * tn), 1, (unsigned)P.cq_S), 256, dgemm::SMEM_BYTES, s>>>(
+            cs + which, (int)tn, 1);
+        QTT_CUDA_TRY(cudaGetLastError());
+        RedArgs ra{Pp, m2, P.cq_S, cqt_n, cqt_ok, Wout, dev};
+        k_gram_reduce<<<rgrid, kThreads, 0, s>>>(ra);
+        QTT_CUDA_TRY(cudaGetLastError());
+        return QTT_OK;
+      };
+      auto chol = [&](double *W, double *dev) -> qtt_status_t {
+        CholArgs ch{W, Dinv, cqt_n, cqt_ok, dev, 0.25, Bf.bar, P.cq_G};
+        return coop_launch((const void *)k_chol_coop, P.cq_G, 0, &ch, s);
+      };
+      auto trinv = [&](double *R) -> qtt_status_t {
+        TrinvArgs tv{R, Dinv, Rinv, cqt_n, cqt_ok};
+        k_trinv<<<(unsigned)P.cq_nblk, kThreads, 0, s>>>(tv);
+        QTT_CUDA_TRY(cudaGetLastError());
+        return QTT_OK;
+      };
+      qtt_status_t st = gram(0, R1, nullptr);                          // W = T^T T
+      if (st == QTT_OK) st = chol(R1, nullptr);
+      if (st == QTT_OK) { k_cq_gate<<<1, 32, 0, s>>>(cqt_ok, cs, 1, 5); st = trinv(R1); }
+      if (st != QTT_OK) return st;
+      launch_gemm_spec(cs + 1, m_cap, nc, 1, 1, true, false, s);        // Q1 = T Rinv1 -> Tw
+      QTT_CUDA_TRY(cudaGetLastError());
+      st = gram(2, R2, cq_dev);                                        // W2 = Q1^T Q1
+      if (st == QTT_OK) st = chol(R2, cq_dev);
+      if (st == QTT_OK) { k_cq_gate<<<1, 32, 0, s>>>(cqt_ok, cs, 3, 5); st = trinv(R2); }
+      if (st != QTT_OK) return st;
+      launch_gemm_spec(cs + 3, m_cap, nc, 1, 1, true, false, s);        // Q = Q1 Rinv2 -> C_q
+      QTT_CUDA_TRY(cudaGetLastError());
+      k_gemm_dmma<true, false><<<dim3((unsigned)(tn * tn), 1, 1), 256, dgemm::SMEM_BYTES, s>>>(cs + 4, (int)tn, 1);
+      QTT_CUDA_TRY(cudaGetLastError());                                // R = R2 R1 -> carry G
+    }
     // a3: CholeskyQR2 when the gate accepts the site, else the Householder QR
     int *cq_ok = nullptr;
     if (P.cq) {
@@ -1181,7 +1301,7 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
       k_gemm_dmma<true, false><<<dim3((unsigned)(tm * tn), 1, 1), 256, dgemm::SMEM_BYTES, s>>>(cs + 3, (int)tn, 1);
       QTT_CUDA_TRY(cudaGetLastError());                                // R = R2 R1 -> A
     }
-    k_copy_T<<<ew_grid, kThreads, 0, s>>>(Bf.dims, Bf.T, Bf.Tw, Bf.A, cq_ok);
+    k_copy_T<<<ew_grid, kThreads, 0, s>>>(Bf.dims, Bf.T, Bf.Tw, Bf.A, cq_ok, cqt_ok);
     QTT_CUDA_TRY(cudaGetLastError());
     {
       QrArgs qa;
@@ -1194,7 +1314,7 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
     {
       JacArgs ja;
       ja.dims = Bf.dims; ja.A = Bf.A; ja.bar = Bf.bar + 1; ja.flags = Bf.flags; ja.ver = Bf.ver; ja.part = Bf.part; ja.nrm = Bf.s2; ja.G = P.Gjac; ja.WB = P.WB;
-      ja.noise_ok = noise_ok(io.eps, P.pcap);
+      ja.noise_ok = noise_ok(io.eps, P.pcap); ja.skip = cqt_ok;
       ja.sweeps_out = io.sweeps ? io.sweeps + q : Bf.sweeps_scratch; ja.status = io.status;
       QTT_CUDA_TRY(cudaMemsetAsync(Bf.flags, 0, sizeof(int) * 3, s));
       QTT_CUDA_TRY(cudaMemsetAsync(Bf.ver, 0, sizeof(int) * (P.pcap + 2), s));
@@ -1207,9 +1327,14 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
       fa.dims = Bf.dims; fa.A = Bf.A; fa.Cq = io.Cq[q]; fa.yr_next = io.yr + q + 1; fa.delta2 = io.delta2 + q;
       fa.sigma = io.sigma ? io.sigma + (size_t)q * io.sigma_stride : nullptr; fa.sigma_stride = io.sigma_stride;
       fa.s2 = Bf.s2; fa.perm = Bf.perm; fa.eps = io.eps; fa.max_rank = io.max_rank; fa.status = io.status;
-      fa.carry = Bf.spec + 2; fa.T = Bf.T; fa.Gout = Bf.G;
+      fa.carry = Bf.spec + 2; fa.T = Bf.T; fa.Gout = Bf.G; fa.skip = cqt_ok;
       k_finish<<<1, kThreads, 0, s>>>(fa);
       QTT_CUDA_TRY(cudaGetLastError());
+      if (cqt_ok) {
+        k_cqt_finish<<<1, 32, 0, s>>>(cqt_ok, Bf.dims, io.yr + q + 1, io.delta2 + q, Bf.spec + 2,
+                                      io.sweeps ? io.sweeps + q : nullptr);
+        QTT_CUDA_TRY(cudaGetLastError());
+      }
     }
     launch_gemm_spec(Bf.spec + 2, io.cap[q + 1], n_cap, 1, 1, false, io.tf32, s);
     QTT_CUDA_TRY(cudaGetLastError());
@@ -1844,7 +1969,7 @@ qtt_status_t large_zipup_sharded(const Shape &S, const qtt_trains_t *op, const q
       JacArgs ja;
       ja.dims = dims_st; ja.A = Ast; ja.bar = bar + 1; ja.flags = jflags; ja.ver = ver; ja.part = part; ja.nrm = s2;
       ja.G = P.Gjac; ja.WB = P.WB;
-      ja.noise_ok = noise_ok(io.eps, (int)P.mcap);
+      ja.noise_ok = noise_ok(io.eps, (int)P.mcap); ja.skip = nullptr;
       ja.sweeps_out = io.sweeps ? io.sweeps + q : sw_scr; ja.status = io.status;
       QTT_CUDA_TRY(cudaMemsetAsync(jflags, 0, sizeof(int) * 3, s));
       QTT_CUDA_TRY(cudaMemsetAsync(ver, 0, sizeof(int) * (P.mcap + 2), s));
@@ -1854,7 +1979,7 @@ qtt_status_t large_zipup_sharded(const Shape &S, const qtt_trains_t *op, const q
       fa.dims = dims_st; fa.A = Ast; fa.Cq = Cq; fa.yr_next = io.out_ranks + q + 1; fa.delta2 = io.delta2 + q;
       fa.sigma = io.sigma ? io.sigma + (size_t)q * io.sigma_stride : nullptr; fa.sigma_stride = io.sigma_stride;
       fa.s2 = s2; fa.perm = perm; fa.eps = io.eps; fa.max_rank = io.max_rank; fa.status = io.status;
-      fa.carry = spec_st + 2; fa.T = Tst; fa.Gout = G;
+      fa.carry = spec_st + 2; fa.T = Tst; fa.Gout = G; fa.skip = nullptr;
       k_finish<<<1, kThreads, 0, s>>>(fa);
       QTT_CUDA_TRY(cudaGetLastError());
     }
