@@ -57,6 +57,8 @@ def parse():
                     help="f32: the fp32 variant (binary32 cores; large-path contractions as 3xTF32 on tcgen05)")
     ap.add_argument("--window", type=int, default=1, choices=[1, 2],
                     help="2: QTT_WINDOW2 super-cores of two sites (SURVEY.md §8(f) f4; per-member kernel)")
+    ap.add_argument("--ncores", type=int, default=1, choices=[1, 2],
+                    help="--workload variational: 1 = single-site sweeps, 2 = two-site super-cores (PAPER.md:300)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -742,6 +744,35 @@ def run_qft(args, rank, world, local):
         dist.destroy_process_group()
 
 
+def variational_flops(kind, L, d, dj, xr, orr, cr, ncores):
+    """Algorithmic flops of one variational sweep of one member (contractions + QR/LQ centre
+    moves; the two-site split's Jacobi excluded, as for the zip-up) from the
+    final ranks cr of C (two-site ranks adapt during the sweep: an estimate at the final ranks)."""
+    f = 0.0
+    for q in range(L):
+        c, c2, r, r2 = cr[q], cr[q + 1], xr[q], xr[q + 1]
+        w, w2 = (orr[q], orr[q + 1]) if kind != "truncate" else (1, 1)
+        left = 2.0 * c * w * r * dj[q] * r2 + 2.0 * c * d[q] * w2 * r2 * w * dj[q]      # X1, X2 (env_apply_left)
+        if ncores == 1:
+            upd = left + 2.0 * c * d[q] * w2 * r2 * c2                                    # C_q = X2 Re^T
+            move = 2.0 * (c * d[q]) * c2 * c2 - (2.0 / 3.0) * c2 ** 3                      # QR / LQ
+            env = 2.0 * c2 * w2 * r2 * c * d[q] + (2.0 * c * d[q] * c2 * w2 * r2 + 2.0 * c * w * dj[q] * r2 * d[q] * w2
+                                                   + 2.0 * c * w * r * dj[q] * r2)          # Le / Re updates
+            f += 2 * (upd + move) + env
+        elif q < L - 1:
+            c3, r3 = cr[q + 2], xr[q + 2]
+            w3 = orr[q + 2] if kind != "truncate" else 1
+            m, n = c * d[q], d[q + 1] * c3
+            second = 2.0 * m * w2 * r2 * dj[q + 1] * r3 + 2.0 * m * d[q + 1] * w3 * r3 * w2 * dj[q + 1]
+            split = 2.0 * m * d[q + 1] * w3 * r3 * c3                                        # S = Z Re^T
+            qr = (2.0 * n * m * m - (2.0 / 3.0) * m ** 3) if m <= n else (2.0 * m * n * n - (2.0 / 3.0) * n ** 3)
+            carry = 2.0 * c2 * m * n
+            env = 2.0 * c2 * w2 * r2 * c * d[q] + (2.0 * c * d[q] * c2 * w2 * r2 + 2.0 * c * w * dj[q] * r2 * d[q] * w2
+                                                   + 2.0 * c * w * r * dj[q] * r2)
+            f += 2 * (left + second + split + qr + carry) + env
+    return f
+
+
 def run_variational(args, rank, world, local):
     """--workload variational (f3): cfg5 members (this rank's shard) seeded by a max-rank-16
     zip-up (untimed); one step = one qtt_variational sweep (right and back) over every member.
@@ -759,8 +790,10 @@ def run_variational(args, rank, world, local):
     xd, od = qtt.to_device(xs), qtt.to_device(ops, mpo=True)
     seed = qtt.ZipupPlan("ij,j->i", od, xd, 1e-10, 16).run(od, xd)
     L, B = xd.n_sites, xd.batch
+    nc = args.ncores
+    vkw = dict(ncores=nc, eps=0.0, max_rank=16) if nc == 2 else {}
     for _ in range(max(args.warmup, 3)):
-        v = qtt.variational("ij,j->i", od, xd, seed, 1)
+        v = qtt.variational("ij,j->i", od, xd, seed, 1, **vkw)
     torch.cuda.synchronize()
     assert int(v.status.item()) == 0
     clocks = ClockSampler(local)
@@ -771,13 +804,20 @@ def run_variational(args, rank, world, local):
     t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for _ in range(args.steps):
-        v = qtt.variational("ij,j->i", od, xd, seed, 1)
+        v = qtt.variational("ij,j->i", od, xd, seed, 1, **vkw)
     t1.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
     ms = qdist.max_over_ranks(t0.elapsed_time(t1) / args.steps, "cuda", dist)
-    units = max(world, 1) * B * 2 * L
+    units = max(world, 1) * B * (2 * L if nc == 1 else 2 * (L - 1))
     value = units / (ms * 1e-3)
+    vr = v.ranks.cpu().numpy()
+    d5 = [2] * L
+    flops = sum(variational_flops("matvec", L, d5, d5, xd.ranks, od.ranks, [int(t) for t in vr[b]], nc)
+                for b in range(B))
+    peaks = fp64_peaks(torch, stream)
+    fp64_peak = max(peaks["dfma_tflops"], peaks["dmma_tflops"])
+    achieved = flops / (ms * 1e-3) / 1e12
     cpu = None
     gain = None
     if rank == 0 and world == 1:
@@ -790,23 +830,29 @@ def run_variational(args, rank, world, local):
         gain = {"member": b, "dist_seed": tt.diff_norm(sd, ex), "dist_after_1_sweep": tt.diff_norm(got, ex)}
         if not args.no_cpu_baseline:
             c0 = time.perf_counter()
-            ref = ovar("matvec", probs[b].op.cores, probs[b].x.cores, sd, 1)
+            ref = ovar("matvec", probs[b].op.cores, probs[b].x.cores, sd, 1, ncores=nc, eps=0.0,
+                       max_rank=16 if nc == 2 else 0)
             cdt = time.perf_counter() - c0
             gain["parity_vs_oracle"] = tt.diff_norm(got, ref["cores"]) / tt.qr_norm(ref["cores"])
-            cpu = {"value": 2 * L / cdt, "unit": "site-updates/s", "cores": os.cpu_count(), "kind": "oracle",
+            cpu = {"value": (units / max(world, 1) / B) / cdt, "unit": "site-updates/s", "cores": os.cpu_count(), "kind": "oracle",
                    "sample": f"one member, one sweep, NumPy einsum + LAPACK QR, {cdt:.2f} s wall"}
     if rank == 0:
         line = {"metric": "variational site updates/sec (f3)", "value": round(value, 3), "unit": "site-updates/s",
                 "n_gpus": max(world, 1), "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (cfg5 members, seeded generators)",
-                "config": {"workload": "f3: one single-site variational sweep (PAPER.md:277-301) on cfg5 members "
-                                       "seeded by a max-rank-16 zip-up", "members_per_gpu": M,
+                "config": {"workload": ("f3: one single-site variational sweep" if nc == 1 else
+                                        "f3: one two-site (ncores=2, max_rank 16, cutoff 0) variational sweep")
+                                       + " (PAPER.md:277-301) on cfg5 members seeded by a max-rank-16 zip-up",
+                           "members_per_gpu": M, "ncores": nc,
                            "global_batch": M * max(world, 1), "L": L, "seed_max_rank": 16,
                            "parallelism": f"dp{max(world, 1)} (members sharded)"},
                 "roofline": {"kernel": "k_variational (one CTA per member, environments in global memory)",
-                             "bound": "alu", "achieved": None, "peak": None, "unit": "TFLOP/s", "frac": None,
-                             "traffic": None, "note": "first plain version; no flop model yet"},
+                             "bound": "fp64", "achieved": round(achieved, 4), "peak": fp64_peak, "unit": "TFLOP/s",
+                             "frac": round(achieved / fp64_peak, 5), "traffic": None,
+                             "achieved_def": "bench.variational_flops (contractions + centre-move QR; the two-site "
+                                             "split's Jacobi excluded) at the final ranks / sweep time",
+                             "peak_source": "FP64 measured in this run by csrc/probe/peak.cu"},
                 "distance": gain, "cpu_baseline": cpu, "e2e": None,
                 "gpu_launches": args.steps, "clocks": clk}
         print(json.dumps(line), flush=True)
@@ -825,11 +871,12 @@ def run_variational_reference(args, rank):
     p = probs[0]
     seed = ozip("matvec", p.op.cores, p.x.cores, 1e-10, 16)["cores"]
     L = len(p.x.cores)
+    nc = args.ncores
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        ovar("matvec", p.op.cores, p.x.cores, seed, 1)
+        ovar("matvec", p.op.cores, p.x.cores, seed, 1, ncores=nc, eps=0.0, max_rank=16 if nc == 2 else 0)
     dt = (time.perf_counter() - t0) / args.steps
-    value = 2 * L / dt
+    value = (2 * L if nc == 1 else 2 * (L - 1)) / dt
     line = {"metric": "variational site updates/sec (f3)", "value": round(value, 3), "unit": "site-updates/s",
             "n_gpus": 1, "steps": args.steps, "warmup": 0, "ms_per_step": round(dt * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",

@@ -124,7 +124,8 @@ def _variational2(kind, op, x, seed, sweeps, eps, max_rank):
 
     def split(q):
         # S[c, i, k, a] = Le[q] W_q x_q W_{q+1} x_{q+1} Re[q+2]        (Eq. variational, N = 2)
-        S = np.einsum("cwr,wijv,rjs,vklu,slt,aut->cika", Le[q], W[q], X[q], W[q + 1], X[q + 1], Re[q + 2])
+        S = np.einsum("cwr,wijv,rjs,vklu,slt,aut->cika", Le[q], W[q], X[q], W[q + 1], X[q + 1], Re[q + 2],
+                      optimize=True)
         c, d1, d2, a = S.shape
         U, sig, Vh = np.linalg.svd(S.reshape(c * d1, d2 * a), full_matrices=False)
         k = truncation_rank(sig, eps, max_rank)
