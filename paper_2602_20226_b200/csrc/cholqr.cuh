@@ -34,43 +34,38 @@ struct CholArgs {
   int G;
 };
 
-// Cholesky of one nb x nb diagonal block in shared memory (upper: D = U^T U), then U^-1.
+// Cholesky of one nb x nb (nb = 32) diagonal block in shared memory (upper: D = U^T U), then
+// U^-1 into Ui -- one warp (lane c owns column c); the calling CTA's other warps skip it.
 __device__ void chol_diag_block(double *D, double *Ui, int nb, int *fail) {
-  const int tid = threadIdx.x;
-  for (int j = 0; j < nb; ++j) {
-    __syncthreads();
-    if (tid == 0) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    for (int j = 0; j < nb; ++j) {
       double d = D[j * nb + j];
-      if (!(d > 0.0) || !isfinite(d)) { *fail = 1; d = 1.0; }
-      D[j * nb + j] = sqrt(d);
+      if (!(d > 0.0) || !isfinite(d)) { if (lane == 0) *fail = 1; d = 1.0; }
+      const double piv = sqrt(d);
+      __syncwarp();
+      if (lane > j) D[j * nb + lane] /= piv;
+      if (lane == j) D[j * nb + j] = piv;
+      __syncwarp();
+      const double ujc = D[j * nb + lane];
+      for (int r = j + 1; r <= lane; ++r) D[r * nb + lane] -= D[j * nb + r] * ujc;   // column `lane`, rows j < r <= lane
+      __syncwarp();
     }
-    __syncthreads();
-    const double piv = D[j * nb + j];
-    for (int c = j + 1 + tid; c < nb; c += blockDim.x) D[j * nb + c] /= piv;
-    __syncthreads();
-    for (int idx = tid; idx < nb * nb; idx += blockDim.x) {      // trailing: D[r][c] -= U[j][r] U[j][c]
-      const int r = idx / nb, c = idx % nb;
-      if (r > j && c >= r) D[r * nb + c] -= D[j * nb + r] * D[j * nb + c];
-    }
-  }
-  __syncthreads();
-  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
-    const int r = idx / nb, c = idx % nb;
-    if (c < r) D[idx] = 0.0;
-  }
-  __syncthreads();
-  // U^-1 (upper) by columns: X[c][c] = 1/U[c][c]; X[r][c] = -(sum_{l=r+1..c} U[r][l] X[l][c]) / U[r][r]
-  for (int c = tid; c < nb; c += blockDim.x) {
-    for (int r = nb - 1; r >= 0; --r) {
-      double v;
-      if (r > c) v = 0.0;
-      else if (r == c) v = 1.0 / D[r * nb + r];
-      else {
-        double sacc = 0.0;
-        for (int l = r + 1; l <= c; ++l) sacc = fma(D[r * nb + l], Ui[l * nb + c], sacc);
-        v = -sacc / D[r * nb + r];
+    for (int r = lane + 1; r < nb; ++r) D[r * nb + lane] = 0.0;                    // below the diagonal
+    __syncwarp();
+    // U^-1 column `lane`: X[c][c] = 1/U[c][c], X[r][c] = -(sum_{l=r+1..c} U[r][l] X[l][c]) / U[r][r]
+    const int c = lane;
+    for (int r = nb - 1; r > c; --r) Ui[r * nb + c] = 0.0;
+    Ui[c * nb + c] = 1.0 / D[c * nb + c];
+    for (int r = c - 1; r >= 0; --r) {
+      double s0 = 0.0, s1 = 0.0;
+      int l = r + 1;
+      for (; l + 1 <= c; l += 2) {
+        s0 = fma(D[r * nb + l], Ui[l * nb + c], s0);
+        s1 = fma(D[r * nb + l + 1], Ui[(l + 1) * nb + c], s1);
       }
-      Ui[r * nb + c] = v;
+      if (l <= c) s0 = fma(D[r * nb + l], Ui[l * nb + c], s0);
+      Ui[r * nb + c] = -(s0 + s1) / D[r * nb + r];
     }
   }
   __syncthreads();
@@ -102,18 +97,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_chol_coop(CholArgs a) {
       if (r < m && c < m) a.W[(size_t)r * m + c] = src[idx];
     }
   };
+  auto factor_diag = [&](int kb, double *blk) {    // CTA 0: blk (smem) holds W[kb][kb]
+    if (tid == 0) s_fail = 0;
+    __syncthreads();
+    chol_diag_block(blk, sB, nb, &s_fail);
+    st(blk, kb, kb);
+    for (int idx = tid; idx < nb * nb; idx += kThreads) a.Dinv[(size_t)kb * nb * nb + idx] = sB[idx];
+    if (tid == 0 && s_fail) *a.ok = 0;
+    __syncthreads();
+  };
+  if (g == 0) {
+    ld(sA, 0, 0);
+    factor_diag(0, sA);
+  }
   for (int kb = 0; kb < nblk; ++kb) {
-    if (g == 0) {
-      if (tid == 0) s_fail = 0;
-      ld(sA, kb, kb);
-      __syncthreads();
-      chol_diag_block(sA, sB, nb, &s_fail);
-      st(sA, kb, kb);
-      for (int idx = tid; idx < nb * nb; idx += kThreads) a.Dinv[(size_t)kb * nb * nb + idx] = sB[idx];
-      if (tid == 0 && s_fail) *a.ok = 0;
-      __syncthreads();
-    }
-    grid_sync(a.bar, a.G, 21);
+    grid_sync(a.bar, a.G, 21);                     // diagonal block kb factored (by CTA 0)
     if (__ldcg(a.ok) == 0) return;                 // uniform after the barrier
     // row panel: R[kb][j] = Dinv^T W[kb][j]  (j > kb)
     for (int jb = kb + 1 + g; jb < nblk; jb += a.G) {
@@ -153,10 +151,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_chol_coop(CholArgs a) {
         sC[idx] = sacc;
       }
       __syncthreads();
-      st(sC, IB, JB);
+      if (t == 0) factor_diag(IB, sC);              // the next diagonal block, right after its update
+      else st(sC, IB, JB);
       __syncthreads();
     }
-    grid_sync(a.bar, a.G, 23);
   }
   // zeros below the diagonal (R is consumed as a full row-major matrix)
   for (long long idx = (long long)g * kThreads + tid; idx < (long long)m * m; idx += (long long)a.G * kThreads) {
@@ -245,10 +243,12 @@ __global__ void k_gram_reduce(RedArgs a) {
   double dv = 0.0;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)m * m;
        idx += (long long)gridDim.x * blockDim.x) {
-    double sacc = 0.0;
-    for (int s = 0; s < a.S; ++s) sacc += a.P[(size_t)s * a.pstride + idx];
-    a.W[idx] = sacc;
     const int r = (int)(idx / m), c = (int)(idx % m);
+    // the Gram GEMMs compute the upper tiles only (GemmSpec.upper): read (min, max)
+    const long long src = (c >= r) ? idx : (long long)c * m + r;
+    double sacc = 0.0;
+    for (int s = 0; s < a.S; ++s) sacc += a.P[(size_t)s * a.pstride + src];
+    a.W[idx] = sacc;
     const double e = sacc - ((r == c) ? 1.0 : 0.0);
     dv = fma(e, e, dv);
   }

@@ -28,6 +28,9 @@ struct GemmSpec {
   long long sa1, sa2, sb1, sb2, sc1, sc2;
   int kchunk;        // > 0: split-K -- batch index z1 takes K range [z1 kchunk, (z1+1) kchunk)
                      // (the caller sets sa1 = kchunk sak, sb1 = kchunk sbk, sc1 = the partial stride)
+  int upper;         // 1: C is symmetric, only tiles on or above the diagonal are computed
+  int tri;           // 1: A[i][k] = 0 for k > i (K stops at the tile's last row);
+                     // 2: B[k][j] = 0 for k > j (K stops at the tile's last column)
 };
 
 namespace dgemm {
@@ -77,6 +80,9 @@ __global__ void __launch_bounds__(256, 1) k_gemm_dmma(const GemmSpec *spec, int 
   if (z1 >= g.nz1 || z2 >= g.nz2) return;
   const int m0 = (blockIdx.x / tiles_n) * TM, n0 = (blockIdx.x % tiles_n) * TN;
   if (m0 >= g.M || n0 >= g.N) return;
+  if (g.upper && m0 > n0) return;
+  if (g.tri == 1) g.K = min(g.K, m0 + TM);
+  if (g.tri == 2) g.K = min(g.K, n0 + TN);
   const double *A = g.A + z1 * g.sa1 + z2 * g.sa2;
   const double *B = g.B + z1 * g.sb1 + z2 * g.sb2;
   double *C = g.C + z1 * g.sc1 + z2 * g.sc2;

@@ -209,10 +209,11 @@ __global__ void k_cq_plan(CqPlanArgs a) {
   g.A = a.T; g.sam = n; g.sak = 1; g.sa1 = kc;
   g.B = a.T; g.sbk = 1; g.sbn = n; g.sb1 = kc;
   g.C = a.P; g.scm = m; g.scn = 1; g.sc1 = a.pstride;
+  g.upper = 1;
   a.spec[0] = g;
-  // [1] Q1^T = Rinv^T T (m x n): A[i][k] = Rinv[k][i] (M-contiguous), B = T
+  // [1] Q1^T = Rinv^T T (m x n): A[i][k] = Rinv[k][i] (M-contiguous, lower triangular), B = T
   GemmSpec h{};
-  h.M = use ? m : 0; h.N = n; h.K = m; h.nz1 = 1; h.nz2 = 1;
+  h.M = use ? m : 0; h.N = n; h.K = m; h.nz1 = 1; h.nz2 = 1; h.tri = 1;
   h.A = a.Rinv; h.sam = 1; h.sak = m;
   h.B = a.T; h.sbk = n; h.sbn = 1;
   h.C = a.Tw; h.scm = n; h.scn = 1;
@@ -223,7 +224,7 @@ __global__ void k_cq_plan(CqPlanArgs a) {
   a.spec[2] = g2;
   // [3] R = R2 R1 (row-major, ld m) -> Rout
   GemmSpec r{};
-  r.M = use ? m : 0; r.N = m; r.K = m; r.nz1 = 1; r.nz2 = 1;
+  r.M = use ? m : 0; r.N = m; r.K = m; r.nz1 = 1; r.nz2 = 1; r.tri = 2;
   r.A = a.R2; r.sam = m; r.sak = 1;
   r.B = a.R1; r.sbk = m; r.sbn = 1;
   r.C = a.Rout; r.scm = m; r.scn = 1;
@@ -259,9 +260,10 @@ __global__ void k_cqt_plan(CqtPlanArgs a) {
   g.A = a.T; g.sam = 1; g.sak = n; g.sa1 = (long long)kc * n;
   g.B = a.T; g.sbk = n; g.sbn = 1; g.sb1 = (long long)kc * n;
   g.C = a.P; g.scm = n; g.scn = 1; g.sc1 = a.pstride;
+  g.upper = 1;
   a.spec[0] = g;
-  GemmSpec h{};            // [1] Q1 = T Rinv (m x n)
-  h.M = use ? m : 0; h.N = n; h.K = n; h.nz1 = 1; h.nz2 = 1;
+  GemmSpec h{};            // [1] Q1 = T Rinv (m x n), Rinv upper triangular
+  h.M = use ? m : 0; h.N = n; h.K = n; h.nz1 = 1; h.nz2 = 1; h.tri = 2;
   h.A = a.T; h.sam = n; h.sak = 1;
   h.B = a.Rinv; h.sbk = n; h.sbn = 1;
   h.C = a.Tw; h.scm = n; h.scn = 1;
@@ -273,7 +275,7 @@ __global__ void k_cqt_plan(CqtPlanArgs a) {
   q.A = a.Tw; q.C = a.Cq;
   a.spec[3] = q;
   GemmSpec r{};            // [4] R = R2 R1 -> the carry (n x n)
-  r.M = use ? n : 0; r.N = n; r.K = n; r.nz1 = 1; r.nz2 = 1;
+  r.M = use ? n : 0; r.N = n; r.K = n; r.nz1 = 1; r.nz2 = 1; r.tri = 2;
   r.A = a.R2; r.sam = n; r.sak = 1;
   r.B = a.R1; r.sbk = n; r.sbn = 1;
   r.C = a.Gout; r.scm = n; r.scn = 1;
