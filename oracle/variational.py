@@ -71,11 +71,11 @@ def variational(kind: str, op: Optional[Sequence[np.ndarray]], x: Sequence[np.nd
     Le[0] = np.ones((1, 1, 1))
     Re[L] = np.ones((1, 1, 1))
     for q in range(L - 1, 0, -1):
-        Re[q] = np.einsum("cia,wijv,rjs,avs->cwr", C[q], W[q], X[q], Re[q + 1])
+        Re[q] = np.einsum("cia,wijv,rjs,avs->cwr", C[q], W[q], X[q], Re[q + 1], optimize=True)
     norms = []
 
     def update(q):
-        C[q] = np.einsum("cwr,wijv,rjs,avs->cia", Le[q], W[q], X[q], Re[q + 1])     # Eq. variational
+        C[q] = np.einsum("cwr,wijv,rjs,avs->cia", Le[q], W[q], X[q], Re[q + 1], optimize=True)  # Eq. variational
         norms.append(float(np.sum(C[q] * C[q])))
 
     for _ in range(sweeps):
@@ -85,16 +85,16 @@ def variational(kind: str, op: Optional[Sequence[np.ndarray]], x: Sequence[np.nd
                 c, d, a = C[q].shape
                 Q, R = np.linalg.qr(C[q].reshape(c * d, a))
                 C[q] = Q.reshape(c, d, Q.shape[1])
-                C[q + 1] = np.einsum("ab,bis->ais", R, C[q + 1])
-                Le[q + 1] = np.einsum("cia,cwr,wijv,rjs->avs", C[q], Le[q], W[q], X[q])
+                C[q + 1] = np.einsum("ab,bis->ais", R, C[q + 1], optimize=True)
+                Le[q + 1] = np.einsum("cia,cwr,wijv,rjs->avs", C[q], Le[q], W[q], X[q], optimize=True)
         for q in range(L - 1, -1, -1):                       # and back
             update(q)
             if q > 0:
                 c, d, a = C[q].shape
                 Q, R = np.linalg.qr(C[q].reshape(c, d * a).T)   # C_q = R^T Q^T
                 C[q] = Q.T.reshape(Q.shape[1], d, a)
-                C[q - 1] = np.einsum("cia,ab->cib", C[q - 1], R.T)
-                Re[q] = np.einsum("cia,wijv,rjs,avs->cwr", C[q], W[q], X[q], Re[q + 1])
+                C[q - 1] = np.einsum("cia,ab->cib", C[q - 1], R.T, optimize=True)
+                Re[q] = np.einsum("cia,wijv,rjs,avs->cwr", C[q], W[q], X[q], Re[q + 1], optimize=True)
     return {"cores": C, "center_norm2": norms, "ranks": [int(C[0].shape[0])] + [int(c.shape[-1]) for c in C]}
 
 
@@ -113,10 +113,10 @@ def _variational2(kind, op, x, seed, sweeps, eps, max_rank):
     Re[L] = np.ones((1, 1, 1))
 
     def right_env(q):
-        Re[q] = np.einsum("cia,wijv,rjs,avs->cwr", C[q], W[q], X[q], Re[q + 1])
+        Re[q] = np.einsum("cia,wijv,rjs,avs->cwr", C[q], W[q], X[q], Re[q + 1], optimize=True)
 
     def left_env(q):                             # Le[q+1] from the left-orthonormal C_q
-        Le[q + 1] = np.einsum("cia,cwr,wijv,rjs->avs", C[q], Le[q], W[q], X[q])
+        Le[q + 1] = np.einsum("cia,cwr,wijv,rjs->avs", C[q], Le[q], W[q], X[q], optimize=True)
 
     for q in range(L - 1, 1, -1):
         right_env(q)

@@ -38,10 +38,13 @@ def _svd(M: np.ndarray):
 def site_matrix(kind: str, G: np.ndarray, Xq: np.ndarray, Oq: Optional[np.ndarray]) -> np.ndarray:
     """Exact local contraction of the carry G (chi, w, r) with the operand cores
     (Eq. einsum).  Returns T (chi, i, w', r')."""
+    # optimize=True: numpy evaluates the same sum pairwise (G with the state core first) instead
+    # of one nested loop over all six indices -- the definition is unchanged, only the order of
+    # the floating-point additions; without it a cfg3 site (256^5 x 2 terms) takes tens of minutes
     if kind == "matvec":     # 'ij,j->i': sum over r and j, w
-        return np.einsum("cwr,rjs,wijv->civs", G, Xq, Oq)
+        return np.einsum("cwr,rjs,wijv->civs", G, Xq, Oq, optimize=True)
     if kind == "hadamard":   # 'i,i->i': i shared, not summed
-        return np.einsum("cab,bis,aiv->civs", G, Xq, Oq)
+        return np.einsum("cab,bis,aiv->civs", G, Xq, Oq, optimize=True)
     if kind == "truncate":   # identity operation (PAPER.md:710 truncate)
         return np.einsum("cr,ris->cis", G[:, 0, :], Xq)[:, :, None, :]
     raise ValueError(kind)
@@ -111,9 +114,9 @@ def _absorb(kind: str, C: np.ndarray, Xq: np.ndarray, Oq: Optional[np.ndarray]) 
     pending sites -- by one site, exactly (Eq. einsum): returns
     (chi, P, i, w', r')."""
     if kind == "matvec":
-        return np.einsum("cpwr,rjs,wijv->cpivs", C, Xq, Oq)
+        return np.einsum("cpwr,rjs,wijv->cpivs", C, Xq, Oq, optimize=True)
     if kind == "hadamard":
-        return np.einsum("cpab,bis,aiv->cpivs", C, Xq, Oq)
+        return np.einsum("cpab,bis,aiv->cpivs", C, Xq, Oq, optimize=True)
     if kind == "truncate":
         return np.einsum("cpr,ris->cpis", C[:, :, 0, :], Xq)[:, :, :, None, :]
     raise ValueError(kind)
