@@ -1103,10 +1103,13 @@ static qtt_status_t plan_sweep(int L, const std::vector<int> &d, const std::vect
   // CholeskyQR2: only when some site can be wide with m >= kCqMinRows
   P.cq = (P.mcap >= kCqMinRows && getenv("QTT_NO_CHOLQR") == nullptr) ? 1 : 0;
   if (P.cq) {
-    const long long tiles = ((P.mcap + dgemm::TM - 1) / dgemm::TM) * ((P.mcap + dgemm::TN - 1) / dgemm::TN);
+    const long long tt = (P.mcap + dgemm::TM - 1) / dgemm::TM;
+    const long long tiles = tt * (tt + 1) / 2;                 // the Gram GEMMs compute upper tiles only
     P.cq_S = (int)std::max<long long>(1, std::min<long long>(16, g_sms / tiles));
     P.cq_nblk = (int)((P.mcap + kCholNb - 1) / kCholNb);
-    P.cq_G = (int)std::min<long long>(g_sms, std::max<long long>(1, (long long)P.cq_nblk * (P.cq_nblk + 1) / 2));
+    // the Cholesky's trailing work is small (<= nblk^2/2 tiles of 32^3 per block row): a few CTAs
+    // keep its 2 nblk grid barriers short
+    P.cq_G = (int)std::min<long long>(32, std::max<long long>(1, (long long)P.cq_nblk * (P.cq_nblk + 1) / 2));
     const size_t m2 = (size_t)P.mcap * P.mcap;
     P.off_cqP = take(8 * m2 * P.cq_S);
     P.off_cqR1 = take(8 * m2);
