@@ -97,7 +97,11 @@ def test_f32_cfg3_full_oracle_parity(lib):
     res = run32(lib, "hadamard", op, x, p.eps, p.max_rank)
     ranks = res.ranks[0].cpu().tolist()
     cores = lib.member_cores(res.out, ranks, 0)
+    # sigma: 1e-4 s_1 here (c-A32): the 3xTF32 contraction error of each split (~1.2e-6 s_1,
+    # measured: profiles/r02/cfg3_fp32_full_parity.log) accumulates linearly through the 29
+    # chained carries to 3.4e-5 s_1 -- the c-A28 fp32 budget of 1e-4, not the per-site 1e-5 of
+    # the reduced tests
     out = compare("hadamard", op, x, p.eps, p.max_rank, cores, ranks, res.sigma[0].cpu().numpy(),
-                  res.delta2[0].cpu().numpy(), float(res.norm2[0].item()), rel_tol=1e-4, sig_tol=1e-5,
+                  res.delta2[0].cpu().numpy(), float(res.norm2[0].item()), rel_tol=1e-4, sig_tol=1e-4,
                   dense=False, u=U32, ref=ref)
     print("cfg3 fp32 full:", {k: v for k, v in out.items() if k != "ref"})
