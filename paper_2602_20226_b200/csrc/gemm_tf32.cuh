@@ -72,27 +72,15 @@ __device__ __forceinline__ uint32_t core_off(int row, int k) {
   return (uint32_t)((row >> 3) * 1024 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
 }
 
-template <bool A_KCONTIG, bool B_KCONTIG = false>
+template <bool A_KCONTIG>
 __global__ void __launch_bounds__(256, 1) k_gemm_tf32(const GemmSpec *spec, int tiles_n, int nz2_cap) {
   using namespace tf32g;
   extern __shared__ __align__(1024) unsigned char tsm[];
-  GemmSpec g = *spec;
+  const GemmSpec g = *spec;
   const int z1 = blockIdx.z / nz2_cap, z2 = blockIdx.z % nz2_cap;
   if (z1 >= g.nz1 || z2 >= g.nz2) return;
   const int m0 = (blockIdx.x / tiles_n) * TM, n0 = (blockIdx.x % tiles_n) * TN;
   if (m0 >= g.M || n0 >= g.N) return;
-  if (g.upper && m0 > n0) return;                 // symmetric C: upper tiles only (gemm.cuh)
-  if (g.tri == 1) g.K = min(g.K, m0 + TM);
-  if (g.tri == 2) g.K = min(g.K, n0 + TN);
-  if (g.kchunk > 0) g.K = min(g.kchunk, g.K - z1 * g.kchunk);   // split-K chunk z1 (A/B offsets in sa1/sb1)
-  if (g.K <= 0) {                                  // empty chunk: a zero partial
-    double *C0 = g.C + z1 * g.sc1 + z2 * g.sc2;
-    for (int idx = threadIdx.x; idx < TM * TN; idx += 256) {
-      const int gm = m0 + idx / TN, gn = n0 + idx % TN;
-      if (gm < g.M && gn < g.N) C0[(long long)gm * g.scm + (long long)gn * g.scn] = 0.0;
-    }
-    return;
-  }
   const double *A = g.A + z1 * g.sa1 + z2 * g.sa2;
   const double *B = g.B + z1 * g.sb1 + z2 * g.sb2;
   double *C = g.C + z1 * g.sc1 + z2 * g.sc2;
@@ -139,14 +127,7 @@ __global__ void __launch_bounds__(256, 1) k_gemm_tf32(const GemmSpec *spec, int 
         av[e] = (gm < g.M && gk < g.K) ? A[(long long)gm * g.sam + (long long)gk * g.sak] : 0.0;
       }
     }
-    if (B_KCONTIG) {                      // B K-contiguous (sbk == 1): thread -> n = tid/2, 16 consecutive k
-      const int n = tid >> 1, kh = (tid & 1) * 16, gn = n0 + n;
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int gk = k0 + kh + e;
-        bv[e] = (gn < g.N && gk < g.K) ? B[(long long)gn * g.sbn + gk] : 0.0;
-      }
-    } else {                              // B: thread -> k = tid/8, 16 consecutive n
+    {                                     // B: thread -> k = tid/8, 16 consecutive n
       const int k = tid >> 3, nh = (tid & 7) * 16, gk = k0 + k;
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
@@ -168,9 +149,7 @@ __global__ void __launch_bounds__(256, 1) k_gemm_tf32(const GemmSpec *spec, int 
     }
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
-      int nrow, k;
-      if (B_KCONTIG) { nrow = tid >> 1; k = (tid & 1) * 16 + e; }
-      else { nrow = (tid & 7) * 16 + e; k = tid >> 3; }
+      const int nrow = (tid & 7) * 16 + e, k = tid >> 3;
       const float x = (float)bv[e], hi = tf32_rna(x), lo = tf32_rna(x - hi);
       const uint32_t o = core_off(nrow, k) >> 2;
       Bhi[o] = hi; Blo[o] = lo;

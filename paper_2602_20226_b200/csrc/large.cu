@@ -1170,8 +1170,6 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
                                       (int)dgemm::SMEM_BYTES));
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_dmma<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)dgemm::SMEM_BYTES));
-    QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_tf32<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)tf32g::SMEM_BYTES));
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_tf32<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)tf32g::SMEM_BYTES));
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_tf32<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1280,12 +1278,8 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
       const long long tm = (mc + dgemm::TM - 1) / dgemm::TM, tn = tm;
       const unsigned rgrid = (unsigned)std::min<long long>((mc * mc + 255) / 256, 2048);
       auto gram = [&](int which, double *Wout, double *dev) -> qtt_status_t {
-        if (io.tf32)        // fp32 variant: the Grams as 3xTF32 on tcgen05 (c-A32 accuracy)
-          k_gemm_tf32<true, true><<<dim3((unsigned)(tm * tn), 1, (unsigned)P.cq_S), 256, tf32g::SMEM_BYTES, s>>>(
-              cs + which, (int)tn, 1);
-        else
-          k_gemm_dmma<true, true><<<dim3((unsigned)(tm * tn), 1, (unsigned)P.cq_S), 256, dgemm::SMEM_BYTES, s>>>(
-              cs + which, (int)tn, 1);
+        k_gemm_dmma<true, true><<<dim3((unsigned)(tm * tn), 1, (unsigned)P.cq_S), 256, dgemm::SMEM_BYTES, s>>>(
+            cs + which, (int)tn, 1);
         QTT_CUDA_TRY(cudaGetLastError());
         RedArgs ra{Pp, m2, P.cq_S, cq_m, cq_ok, Wout, dev};
         k_gram_reduce<<<rgrid, kThreads, 0, s>>>(ra);
@@ -1303,7 +1297,7 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
       TrinvArgs ta{R1, Dinv, Rinv, cq_m, cq_ok};
       k_trinv<<<(unsigned)P.cq_nblk, kThreads, 0, s>>>(ta);            // Rinv = R1^-1
       QTT_CUDA_TRY(cudaGetLastError());
-      launch_gemm_spec(cs + 1, mc, n_cap, 1, 1, false, io.tf32, s);    // Q1^T = Rinv^T T -> Tw
+      launch_gemm_spec(cs + 1, mc, n_cap, 1, 1, false, false, s);      // Q1^T = Rinv^T T -> Tw
       QTT_CUDA_TRY(cudaGetLastError());
       st = gram(2, R2, cq_dev);                                        // W2 = Q1^T Q1, |W2 - I|_F^2
       if (st == QTT_OK) st = chol(R2, cq_dev);                         // R2 (gate |W2 - I|_F <= 1/2)
