@@ -73,3 +73,43 @@ def test_to_dense_guard_host_only():
     out = ctypes.c_void_p(1)
     st = lib.qtt_to_dense(ctypes.byref(x), None, out, 0, None, 0, None)
     assert st == 6 and b"guard" in lib.qtt_last_error()   # 2^25 > 2^24 (SURVEY c-A30)
+
+
+def test_sharded_and_variational_ex_validation_host_only():
+    """qtt_zipup_sharded(_sizes) and qtt_variational_ex refuse bad arguments before any GPU
+    work (SURVEY.md §8(f) f3/f4 entry points; qtt.h error conventions)."""
+    from paper_2602_20226_b200 import qtt
+    from paper_2602_20226_b200.shard import _Comm, _ALLGATHER
+    lib = qtt.load_library()
+    x, kx = _mps_struct(qtt, [2] * 6, [1, 2, 4, 8, 4, 2, 1])
+    r_el, c_el, wsb = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+    assert lib.qtt_zipup_sharded_sizes(b"i,i->i", ctypes.byref(x), ctypes.byref(x), 0, 2, 2, ctypes.byref(r_el),
+                                       ctypes.byref(c_el), ctypes.byref(wsb)) == 0
+    assert r_el.value >= 1 and c_el.value >= 1 and wsb.value > 0
+    xb, kxb = _mps_struct(qtt, [2] * 6, [1, 2, 4, 8, 4, 2, 1], batch=2)
+    assert lib.qtt_zipup_sharded_sizes(b"i,i->i", ctypes.byref(xb), ctypes.byref(xb), 0, 2, 1, ctypes.byref(r_el),
+                                       ctypes.byref(c_el), ctypes.byref(wsb)) == 8        # batch != 1
+    assert lib.qtt_zipup_sharded_sizes(b"i,i->i", ctypes.byref(x), ctypes.byref(x), 0, 0, 1, ctypes.byref(r_el),
+                                       ctypes.byref(c_el), ctypes.byref(wsb)) == 1        # world 0
+    one = ctypes.c_void_p(1)
+    comm = _Comm(2, 0, 1, _ALLGATHER(), None, 1, 1, 1, 1)                                # world 2, no callback
+    st = lib.qtt_zipup_sharded(b"i,i->i", ctypes.byref(x), ctypes.byref(x), 1e-8, 0, ctypes.c_uint32(0),
+                               ctypes.byref(x), one, one, one, one, None, 1, ctypes.byref(comm), one, 1 << 30, None)
+    assert st == 1 and b"callback" in lib.qtt_last_error()
+    comm = _Comm(1, 3, 1, _ALLGATHER(), None, 1, 1, 1, 1)                                # rank outside [0, world)
+    st = lib.qtt_zipup_sharded(b"i,i->i", ctypes.byref(x), ctypes.byref(x), 1e-8, 0, ctypes.c_uint32(0),
+                               ctypes.byref(x), one, one, one, one, None, 1, ctypes.byref(comm), one, 1 << 30, None)
+    assert st == 1 and b"rank" in lib.qtt_last_error()
+    st = lib.qtt_zipup_sharded(b"i,i->i", ctypes.byref(x), ctypes.byref(x), 1e-8, 0, ctypes.c_uint32(2),
+                               ctypes.byref(x), one, one, one, one, None, 1, ctypes.byref(comm), one, 1 << 30, None)
+    assert st == 8                                                                        # QTT_WINDOW2
+    # qtt_variational_ex: ncores must be 1 or 2; the output capacity must hold the seed
+    st = lib.qtt_variational_ex(b"i->i", None, ctypes.byref(x), ctypes.byref(x), one, ctypes.byref(x), one, 1, 3,
+                                0.0, 0, one, one, one, 1 << 30, None)
+    assert st == 8 and b"ncores" in lib.qtt_last_error()
+    small, ks = _mps_struct(qtt, [2] * 6, [1, 2, 2, 2, 2, 2, 1])
+    st = lib.qtt_variational_ex(b"i->i", None, ctypes.byref(x), ctypes.byref(x), one, ctypes.byref(small), one, 1, 2,
+                                0.0, 0, one, one, one, 1 << 30, None)
+    assert st == 5 and b"capacity" in lib.qtt_last_error()
+    assert lib.qtt_variational_workspace_bytes_ex(b"i->i", None, ctypes.byref(x), ctypes.byref(x), 2) > 0
+    assert lib.qtt_variational_workspace_bytes_ex(b"i->i", None, ctypes.byref(x), ctypes.byref(x), 4) == 0
