@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_chol_coop(CholArgs a) {
   const int m = *a.mdim, nb = kCholNb, g = blockIdx.x, tid = threadIdx.x;
   if (m <= 0) return;
   if (*a.ok == 0) return;                          // uniform: an earlier step already failed
-  if (a.dev && *a.dev > a.dev_max) {               // second pass: Q1 too far from orthonormal
+  if (a.dev && !(*a.dev <= a.dev_max)) {           // second pass: Q1 too far from orthonormal (or NaN)
     if (g == 0 && tid == 0) *a.ok = 0;
     return;
   }
