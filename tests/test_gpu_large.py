@@ -141,3 +141,21 @@ def test_cfg3_full_oracle_parity(lib):
                   dense=False, ref=ref)
     assert max(ranks) == 256
     print("cfg3 full:", {k: v for k, v in out.items() if k != "ref"})
+
+
+def test_large_exact_truncate_rank_deficient(lib):
+    """eps = 0 truncation (the exact sweep a1 uses) of the redundant rank-256 train of 1 (exact
+    rank 1 stored at rank 256, random orthogonal gauges): the result must still be 1 at every
+    sampled index -- guards the large path's exact sweeps against rank-deficient site matrices
+    (CholeskyQR2 gate -> Householder / Jacobi fallback)."""
+    import torch
+    from oracle import tt
+    L, R = 30, 256
+    ones = _redundant_ones(L, R)
+    xd = lib.to_device(ones)
+    res = lib.ZipupPlan("i->i", None, xd, 0.0, 0).run(None, xd)
+    torch.cuda.synchronize()
+    assert int(res.status.item()) == 0
+    y = lib.member_cores(res.out, res.ranks[0].cpu().tolist(), 0)
+    dig = np.random.default_rng(19).integers(0, 2, size=(512, L))
+    np.testing.assert_allclose(tt.evaluate(y, dig), 1.0, rtol=1e-8)
