@@ -55,8 +55,11 @@ __device__ void chol_diag_block(double *D, double *Ui, int nb, int *fail) {
     __syncwarp();
     // U^-1 column `lane`: X[c][c] = 1/U[c][c], X[r][c] = -(sum_{l=r+1..c} U[r][l] X[l][c]) / U[r][r]
     const int c = lane;
+    double *rinv = Ui + nb * nb;                   // [nb] reciprocals of the diagonal (one per lane)
+    rinv[c] = 1.0 / D[c * nb + c];
+    __syncwarp();
     for (int r = nb - 1; r > c; --r) Ui[r * nb + c] = 0.0;
-    Ui[c * nb + c] = 1.0 / D[c * nb + c];
+    Ui[c * nb + c] = rinv[c];
     for (int r = c - 1; r >= 0; --r) {
       double s0 = 0.0, s1 = 0.0;
       int l = r + 1;
@@ -65,7 +68,7 @@ __device__ void chol_diag_block(double *D, double *Ui, int nb, int *fail) {
         s1 = fma(D[r * nb + l + 1], Ui[(l + 1) * nb + c], s1);
       }
       if (l <= c) s0 = fma(D[r * nb + l], Ui[l * nb + c], s0);
-      Ui[r * nb + c] = -(s0 + s1) / D[r * nb + r];
+      Ui[r * nb + c] = -(s0 + s1) * rinv[r];
     }
   }
   __syncthreads();
@@ -75,7 +78,7 @@ __device__ void chol_diag_block(double *D, double *Ui, int nb, int *fail) {
 //   for each block row kb: CTA 0 factors the diagonal block (and its inverse); all CTAs form
 //   the row panel R[kb][j] = U^-T W[kb][j]; all CTAs update the trailing upper blocks.
 __global__ void __launch_bounds__(kThreads, 1) k_chol_coop(CholArgs a) {
-  __shared__ double sA[kCholNb * kCholNb], sB[kCholNb * kCholNb], sC[kCholNb * kCholNb];
+  __shared__ double sA[kCholNb * kCholNb], sB[kCholNb * kCholNb + kCholNb], sC[kCholNb * kCholNb];
   __shared__ int s_fail;
   const int m = *a.mdim, nb = kCholNb, g = blockIdx.x, tid = threadIdx.x;
   if (m <= 0) return;
@@ -130,8 +133,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_chol_coop(CholArgs a) {
     }
     grid_sync(a.bar, a.G, 22);
     // trailing: W[ib][jb] -= R[kb][ib]^T R[kb][jb]  (kb < ib <= jb)
+    // CTA 0 takes only tile (0, 0) -- the next diagonal block, which it then factors (the
+    // critical path); the other tiles go to CTAs 1..G-1
     const int nt = nblk - kb - 1;
-    for (int t = g; t < nt * (nt + 1) / 2; t += a.G) {
+    const int t0 = (g == 0) ? 0 : g, tstep = (g == 0) ? (1 << 30) : max(a.G - 1, 1);
+    for (int t = (a.G == 1) ? g : t0; t < nt * (nt + 1) / 2; t += (a.G == 1) ? 1 : tstep) {
       int ib = 0, rem = t;                          // t -> (ib <= jb) upper-triangular pair
       while (rem >= nt - ib) { rem -= nt - ib; ++ib; }
       const int jb = ib + rem;
