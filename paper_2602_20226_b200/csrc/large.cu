@@ -1318,12 +1318,25 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
     // a4
     {
       JacArgs ja;
-      ja.dims = Bf.dims; ja.A = Bf.A; ja.bar = Bf.bar + 1; ja.flags = Bf.flags; ja.ver = Bf.ver; ja.part = Bf.part; ja.nrm = Bf.s2; ja.G = P.Gjac; ja.WB = P.WB;
+      // per-site block width: the widest WB whose two blocks of this site's (capacity) rows fit
+      // in shared memory -- the plan's WB is sized for the tallest site of the sweep
+      int WBq = P.WB;
+      size_t smq = P.jac_smem;
+      int Gq = P.Gjac;
+      if (!getenv("QTT_COOP_WB")) {
+        WBq = kWarps;
+        while (WBq > 1 && 2 * WBq * (m_cap + 1) * 8 > 200 * 1024) WBq /= 2;
+        WBq = std::max(WBq, P.WB);
+        const long long pq = std::min(m_cap, n_cap);
+        Gq = (int)std::min<long long>(g_sms, std::max<long long>(1, (pq + 2 * WBq - 1) / (2 * WBq)));
+        smq = sizeof(double) * (2 * WBq * m_cap + 2 * WBq);
+      }
+      ja.dims = Bf.dims; ja.A = Bf.A; ja.bar = Bf.bar + 1; ja.flags = Bf.flags; ja.ver = Bf.ver; ja.part = Bf.part; ja.nrm = Bf.s2; ja.G = Gq; ja.WB = WBq;
       ja.noise_ok = noise_ok(io.eps, P.pcap); ja.skip = cqt_ok;
       ja.sweeps_out = io.sweeps ? io.sweeps + q : Bf.sweeps_scratch; ja.status = io.status;
       QTT_CUDA_TRY(cudaMemsetAsync(Bf.flags, 0, sizeof(int) * 3, s));
       QTT_CUDA_TRY(cudaMemsetAsync(Bf.ver, 0, sizeof(int) * (P.pcap + 2), s));
-      qtt_status_t st = coop_launch((const void *)k_jacobi_coop, P.Gjac, P.jac_smem, &ja, s);
+      qtt_status_t st = coop_launch((const void *)k_jacobi_coop, Gq, smq, &ja, s);
       if (st != QTT_OK) return st;
     }
     // a5/a6
