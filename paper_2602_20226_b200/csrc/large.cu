@@ -322,6 +322,7 @@ struct QrArgs {
   GridBar *bar;
   int G, RB, mcap;
   const int *skip;     // non-NULL and set: R already computed (CholeskyQR2 accepted): return
+  double *tau_out;     // non-NULL: the Householder scalars tau_j are kept (explicit Q later)
 };
 
 // Reduce a per-CTA scalar triple of arrays: block sum of v over kThreads.
@@ -376,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qr_coop(QrArgs a) {
         householder(__ldcg(a.bc + slot + jj), s, tj, beta, scale);
       }
       if (tid == 0) tau[jj] = tj;
+      if (a.tau_out && g == 0 && tid == 0) a.tau_out[j] = tj;
       if (tid < kNb) {
         double w = 0.0;
         if (tid > jj && tid < nb && tj != 0.0) {
@@ -496,6 +498,200 @@ __global__ void __launch_bounds__(kThreads, 1) k_qr_coop(QrArgs a) {
     const int j = (int)(idx / m), c = (int)(idx % m);
     a.Rout[idx] = (c >= j) ? a.Tw[(size_t)c * n + j] : 0.0;
   }
+}
+
+// ------------------------------------------------------------------ tall sites: QR first
+// A direct site (m > n: T is taller than wide) whose Jacobi would run on m-row columns is first
+// reduced by a Householder QR, T = Q R (k_qr_coop on T^T, the reflectors kept): the Jacobi then
+// runs on the n x n columns of R (fewer rows per rotation, and a wider block), and its left
+// singular vectors U_R become U_T = Q [U_R; 0] by applying the reflectors (k_qapply_coop).  The
+// host marks a site a candidate when its capacities satisfy m_cap >= 2 n_cap, n_cap >= 32 (cfg4's
+// d = 5 sites: 2560 x 1000, 1875 x 200); the device takes the route when the site is direct.  On a
+// candidate the Jacobi's columns have at most n_cap rows either way, which sizes its block.
+
+struct TqPlanArgs {
+  const SiteDims *dims;   // the site
+  SiteDims *dims_j;       // out: the Jacobi / finish dims (R's n x n, or a copy of the site's)
+  SiteDims *dims_t;       // out: the QR's dims (T^T as a wide "T")
+  SiteDims *dims_2;       // out: the second QR's dims (R1^T, n x n)
+  int *tq, *ntq;          // out: 1 / 0 when the site takes the QR-first route
+  const int *busy;        // non-NULL and set: the site is handled otherwise (tall CholeskyQR2)
+};
+__global__ void k_tq_plan(TqPlanArgs a) {
+  if (threadIdx.x != 0) return;
+  const SiteDims D = *a.dims;
+  const int use = (D.direct && !(a.busy && *a.busy)) ? 1 : 0;
+  *a.tq = use; *a.ntq = 1 - use;
+  SiteDims J = D;
+  if (use) { J.m = D.n; J.n = D.n; J.p = D.n; J.direct = 0; }
+  J.k = 0;
+  *a.dims_j = J;
+  SiteDims T = D;
+  T.m = D.n; T.n = D.m; T.p = D.n; T.direct = 0;
+  *a.dims_t = T;
+  T.n = D.n;
+  *a.dims_2 = T;
+}
+// ||T||_F^2 partial sums (one per CTA): the QR runs on T scaled by a power of two with
+// ||T||_F^2 in [1, 4) (as k_jacobi_coop does), so that no sum of squares in the Householder
+// steps underflows for any input magnitude; R is scaled back exactly in k_tq_toA
+__global__ void k_tq_sq(const SiteDims *dims, const int *tq, const double *T, double *part) {
+  __shared__ double red[kWarps];
+  if (!*tq) return;
+  const long long mn = (long long)dims->m * dims->n;
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < mn; i += (long long)gridDim.x * blockDim.x) {
+    const double v = T[i];
+    s = fma(v, v, s);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+// Tw (n x m row-major) = 2^e T^T, so that k_qr_coop's "T^H" is the tall T (scaled)
+__global__ void k_tq_copy(const SiteDims *dims, const int *tq, const double *T, const double *part, int nparts,
+                          double *Tw, double *scale_out) {
+  __shared__ double sc;
+  if (!*tq) return;
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int t = 0; t < nparts; ++t) tot += part[t];
+    double f = 1.0;
+    if (tot > 0.0 && isfinite(tot)) f = ldexp(1.0, -(ilogb(tot) >> 1));
+    sc = f;
+    if (blockIdx.x == 0) *scale_out = f;
+  }
+  __syncthreads();
+  const double f = sc;
+  const SiteDims D = *dims;
+  const long long mn = (long long)D.m * D.n;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < mn; i += (long long)gridDim.x * blockDim.x) {
+    const long long j = i / D.m, r = i % D.m;
+    Tw[i] = T[r * D.n + j] * f;
+  }
+}
+// A (n x n column-major) = R / 2^e: A[j*n + i] = R[i][j] (R row-major, upper); with `as_is`
+// A = R's storage / 2^e (the column-major R^T; R may alias A)
+__global__ void k_tq_toA(const SiteDims *dims, const int *tq, const double *R, const double *scale, double *A,
+                         int as_is) {
+  if (!*tq) return;
+  const int n = dims->n;
+  const double inv = 1.0 / *scale;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)n * n; i += (long long)gridDim.x * blockDim.x) {
+    if (as_is) { A[i] = R[i] * inv; continue; }
+    const int j = (int)(i / n), r = (int)(i % n);
+    A[i] = (r <= j) ? R[(size_t)r * n + j] * inv : 0.0;
+  }
+}
+
+struct QapplyArgs {
+  const SiteDims *dims;   // the site (m rows, n reflectors)
+  const SiteDims *dims_j; // k of the split
+  const int *tq;
+  const double *Yw;       // reflectors: column j in Yw[j*m + r], r > j (unit at r == j)
+  const double *tau;      // [n]
+  double *C;              // m x k row-major: in [U_R; garbage below n], out Q [U_R; 0]
+  double *part, *wtot, *gram;
+  GemmSpec *carry;        // the carry spec: K <- m
+  GridBar *bar;
+  int G, RB;
+};
+__global__ void __launch_bounds__(kThreads, 1) k_qapply_coop(QapplyArgs a) {
+  extern __shared__ double smq[];
+  if (!*a.tq) return;                          // uniform
+  const SiteDims D = *a.dims;
+  const int m = D.m, n = D.n, k = a.dims_j->k, g = blockIdx.x, tid = threadIdx.x, lane = tid & 31,
+            warp = tid >> 5;
+  const int r0 = g * a.RB, r1 = min(m, r0 + a.RB), nr = max(0, r1 - r0);
+  double *Y = smq;                             // [kNb][RB]
+  double *tw = Y + kNb * a.RB;                 // [kNb * kNb]
+  double *Mt = tw + kNb * kNb;                 // [kNb * 64]
+  const unsigned G = a.G;
+  // rows >= n of C start at zero (C = [U_R; 0])
+  for (long long idx = (long long)g * kThreads + tid; idx < (long long)(m - n) * k; idx += (long long)G * kThreads)
+    a.C[(size_t)n * k + idx] = 0.0;
+  grid_sync(a.bar, G, 31);
+  const int npan = (n + kNb - 1) / kNb;
+  for (int pan = npan - 1; pan >= 0; --pan) {
+    const int j0 = pan * kNb, nb = min(kNb, n - j0);
+    for (int idx = tid; idx < kNb * nr; idx += kThreads) {
+      const int cc = idx / nr, i = idx % nr, r = r0 + i, j = j0 + cc;
+      Y[cc * a.RB + i] = (cc >= nb) ? 0.0 : (r > j ? a.Yw[(size_t)j * m + r] : (r == j ? 1.0 : 0.0));
+    }
+    __syncthreads();
+    // partial W[cc][c] = sum_r Y[r][cc] C[r][c] and partial Y^T Y over my rows
+    for (int c = warp; c < k; c += kWarps) {
+      double acc[kNb];
+#pragma unroll
+      for (int cc = 0; cc < kNb; ++cc) acc[cc] = 0.0;
+      for (int i = lane; i < nr; i += 32) {
+        const double x = a.C[(size_t)(r0 + i) * k + c];
+#pragma unroll
+        for (int cc = 0; cc < kNb; ++cc) acc[cc] = fma(Y[cc * a.RB + i], x, acc[cc]);
+      }
+#pragma unroll
+      for (int cc = 0; cc < kNb; ++cc) {
+        const double t = warp_sum(acc[cc]);
+        if (lane == 0) a.part[((size_t)g * kNb + cc) * k + c] = t;
+      }
+    }
+    double *gpart = a.part + (size_t)G * kNb * k;
+    for (int e = warp; e < kNb * kNb; e += kWarps) {
+      const int k1 = e / kNb, k2 = e % kNb;
+      double sacc = 0.0;
+      for (int i = lane; i < nr; i += 32) sacc = fma(Y[k1 * a.RB + i], Y[k2 * a.RB + i], sacc);
+      sacc = warp_sum(sacc);
+      if (lane == 0) gpart[(size_t)g * kNb * kNb + e] = sacc;
+    }
+    grid_sync(a.bar, G, 32);
+    for (int idx = g * kThreads + tid; idx < kNb * k; idx += G * kThreads) {
+      double sacc = 0.0;
+      for (unsigned gg = 0; gg < G; ++gg) sacc += __ldcg(a.part + (size_t)gg * kNb * k + idx);
+      a.wtot[idx] = sacc;
+    }
+    if (g == 0)
+      for (int e = tid; e < kNb * kNb; e += kThreads) {
+        double sacc = 0.0;
+        for (unsigned gg = 0; gg < G; ++gg) sacc += __ldcg(gpart + (size_t)gg * kNb * kNb + e);
+        a.gram[e] = sacc;
+      }
+    grid_sync(a.bar, G, 33);
+    // T_wy of H_{j0} ... H_{j0+nb-1} (upper): T_jj = tau_j, T[0:j, j] = -tau_j T[0:j,0:j] (Y^T y_j)[0:j]
+    if (tid == 0) {
+      for (int e = 0; e < kNb * kNb; ++e) tw[e] = 0.0;
+      for (int j = 0; j < nb; ++j) {
+        const double tj = __ldcg(a.tau + j0 + j);
+        tw[j * kNb + j] = tj;
+        for (int i = 0; i < j; ++i) {
+          double sacc = 0.0;
+          for (int l = i; l < j; ++l) sacc += tw[i * kNb + l] * __ldcg(a.gram + l * kNb + j);
+          tw[i * kNb + j] = -tj * sacc;
+        }
+      }
+    }
+    __syncthreads();
+    // C -= Y (T W), columns in chunks of 64
+    for (int cb = 0; cb < k; cb += 64) {
+      const int ncb = min(64, k - cb);
+      for (int idx = tid; idx < kNb * ncb; idx += kThreads) {
+        const int kk = idx / ncb, c = idx % ncb;
+        double sacc = 0.0;
+        for (int l = kk; l < kNb; ++l) sacc = fma(tw[kk * kNb + l], __ldcg(a.wtot + (size_t)l * k + cb + c), sacc);
+        Mt[kk * 64 + c] = sacc;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < nr * ncb; idx += kThreads) {
+        const int i = idx / ncb, c = idx % ncb;
+        double *cp = a.C + (size_t)(r0 + i) * k + cb + c;
+        double sacc = *cp;
+#pragma unroll
+        for (int kk = 0; kk < kNb; ++kk) sacc = fma(-Y[kk * a.RB + i], Mt[kk * 64 + c], sacc);
+        *cp = sacc;
+      }
+      __syncthreads();
+    }
+    grid_sync(a.bar, G, 34);
+  }
+  if (g == 0 && tid == 0) a.carry->K = m;        // the carry G = U_T^T T runs over the site's m rows
 }
 
 // ------------------------------------------------------------------ a4: cooperative Jacobi
@@ -1045,6 +1241,9 @@ struct SweepPlan {
   size_t qr_smem, jac_smem;
   size_t off_G, off_X, off_T, off_Tw, off_A, off_part, off_wtot, off_gram, off_bc, off_s2, off_perm, off_flags,
       off_ver, off_sw, off_bar, off_dims, off_spec, total;
+  // tall sites: Householder QR first, explicit Q applied to U_R
+  int tq;
+  size_t off_tqDims, off_tqI, off_tqR, off_tqTau;
   // CholeskyQR2 (cholqr.cuh) for the wide sites
   int cq, cq_S, cq_nblk, cq_G;
   size_t off_cqP, off_cqR1, off_cqR2, off_cqRinv, off_cqDinv, off_cqI, off_cqDev, off_cqSpec;
@@ -1088,7 +1287,9 @@ static qtt_status_t plan_sweep(int L, const std::vector<int> &d, const std::vect
   P.off_T = take(8 * P.tcap);
   P.off_Tw = take(8 * P.tcap);
   P.off_A = take(8 * P.acap);
-  P.off_part = take(8 * ((size_t)P.Gqr * kNb * P.mcap + (size_t)P.Gqr * kNb * kNb + 16));
+  // (the tall-site QR / Q apply run on up to ceil(mcap / 32) CTAs)
+  const size_t Gpart = std::max<size_t>(P.Gqr, std::min<size_t>(g_sms, (P.mcap + 31) / 32));
+  P.off_part = take(8 * (Gpart * kNb * P.mcap + Gpart * kNb * kNb + 16 + g_sms));
   P.off_wtot = take(8 * (size_t)kNb * P.mcap);
   P.off_gram = take(8 * kNb * kNb);
   P.off_bc = take(8 * 64);
@@ -1100,6 +1301,13 @@ static qtt_status_t plan_sweep(int L, const std::vector<int> &d, const std::vect
   P.off_bar = take(sizeof(GridBar) * 2);
   P.off_dims = take(sizeof(SiteDims));
   P.off_spec = take(sizeof(GemmSpec) * 3);
+  P.tq = (P.mcap >= 64 && getenv("QTT_NO_TALLQR") == nullptr) ? 1 : 0;
+  if (P.tq) {
+    P.off_tqDims = take(sizeof(SiteDims) * 3);
+    P.off_tqI = take(32);                       // tq, ntq, (pad), the QR's scale (double at +16)
+    P.off_tqR = take(8 * (size_t)P.pcap * P.pcap);
+    P.off_tqTau = take(8 * (size_t)P.pcap);
+  }
   // CholeskyQR2: only when some site can be wide with m >= kCqMinRows
   P.cq = (P.mcap >= kCqMinRows && getenv("QTT_NO_CHOLQR") == nullptr) ? 1 : 0;
   if (P.cq) {
@@ -1163,6 +1371,7 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
   Bf.dims = (SiteDims *)(ws + P.off_dims); Bf.spec = (GemmSpec *)(ws + P.off_spec);
   {  // dynamic-smem opt-in on the current device, every call (per-device setting; cheap, thread-safe)
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_qr_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    QTT_CUDA_TRY(cudaFuncSetAttribute(k_qapply_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_jacobi_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     QTT_CUDA_TRY(cudaFuncSetAttribute(k_gemm_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)dgemm::SMEM_BYTES));
@@ -1311,9 +1520,56 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
     {
       QrArgs qa;
       qa.dims = Bf.dims; qa.Tw = Bf.Tw; qa.Rout = Bf.A; qa.part = Bf.part; qa.wtot = Bf.wtot; qa.gram = Bf.gram;
-      qa.bc = Bf.bc; qa.bar = Bf.bar; qa.G = P.Gqr; qa.RB = P.RB; qa.mcap = (int)P.mcap; qa.skip = cq_ok;
+      qa.bc = Bf.bc; qa.bar = Bf.bar; qa.G = P.Gqr; qa.RB = P.RB; qa.mcap = (int)P.mcap; qa.skip = cq_ok; qa.tau_out = nullptr;
       qtt_status_t st = coop_launch((const void *)k_qr_coop, P.Gqr, P.qr_smem, &qa, s);
       if (st != QTT_OK) return st;
+    }
+    // tall sites (m >= 2n): Householder QR of T first; the Jacobi / finish then see R's dims
+    SiteDims *dims_j = Bf.dims;
+    int *tq = nullptr, tq_G = 0, tq_RB = 0;
+    size_t tq_smem = 0;
+    const bool tq_cand = P.tq && m_cap >= 2 * n_cap && n_cap >= 64 && m_cap >= 1024;
+    if (tq_cand) {
+      dims_j = (SiteDims *)(ws + P.off_tqDims);
+      SiteDims *dims_t = dims_j + 1;
+      tq = (int *)(ws + P.off_tqI);
+      int *ntq = tq + 1;
+      double *Rt = (double *)(ws + P.off_tqR), *tauv = (double *)(ws + P.off_tqTau);
+      SiteDims *dims_2 = dims_j + 2;
+      TqPlanArgs tp{Bf.dims, dims_j, dims_t, dims_2, tq, ntq, cqt_ok};
+      k_tq_plan<<<1, 32, 0, s>>>(tp);
+      double *tq_scale = (double *)(ws + P.off_tqI + 16);
+      k_tq_sq<<<g_sms, kThreads, 0, s>>>(Bf.dims, tq, Bf.T, Bf.part);
+      k_tq_copy<<<ew_grid, kThreads, 0, s>>>(Bf.dims, tq, Bf.T, Bf.part, g_sms, Bf.Tw, tq_scale);
+      QTT_CUDA_TRY(cudaGetLastError());
+      QrArgs qt;
+      qt.dims = dims_t; qt.Tw = Bf.Tw; qt.Rout = Rt; qt.part = Bf.part; qt.wtot = Bf.wtot; qt.gram = Bf.gram;
+      // the QR's grid from this site's rows (fewer CTAs in each column step's barrier)
+      tq_G = (int)std::min<long long>(g_sms, (m_cap + 31) / 32);
+      tq_RB = (int)(((m_cap + tq_G - 1) / tq_G + 31) / 32 * 32);
+      tq_smem = sizeof(double) * ((size_t)kNb * tq_RB + 32 + kNb * kNb + 2 * kNb + kNb * 64);
+      qt.bc = Bf.bc; qt.bar = Bf.bar; qt.G = tq_G; qt.RB = tq_RB; qt.mcap = (int)P.mcap; qt.skip = ntq;
+      qt.tau_out = tauv;
+      qtt_status_t st = coop_launch((const void *)k_qr_coop, tq_G, tq_smem, &qt, s);
+      if (st != QTT_OK) return st;
+      // second QR, of R1^T (its columns are R1's rows, i.e. Rt as k_qr_coop's row-major input):
+      // R1^T = Q2 R2, so R1 = R2^T Q2^T and the Jacobi on R2^T's columns yields R1's -- hence
+      // (after Q1) T's -- left singular vectors with no rotation accumulation, in about half the
+      // sweeps of the Jacobi on R1 (measured on cfg4's 2560 x 1000 site: 13 against 27)
+      const bool qr2 = getenv("QTT_TQ_QR1") == nullptr;
+      if (qr2) {
+        QrArgs q2 = qt;
+        const long long n2 = n_cap;
+        q2.dims = dims_2; q2.Tw = Rt; q2.Rout = Bf.A; q2.tau_out = nullptr;
+        q2.G = (int)std::min<long long>(g_sms, (n2 + 31) / 32);
+        q2.RB = (int)(((n2 + q2.G - 1) / q2.G + 31) / 32 * 32);
+        const size_t sm2 = sizeof(double) * ((size_t)kNb * q2.RB + 32 + kNb * kNb + 2 * kNb + kNb * 64);
+        st = coop_launch((const void *)k_qr_coop, q2.G, sm2, &q2, s);
+        if (st != QTT_OK) return st;
+      }
+      k_tq_toA<<<(unsigned)std::min<long long>((P.pcap * P.pcap + 255) / 256, 4096), 256, 0, s>>>(
+          Bf.dims, tq, qr2 ? Bf.A : Rt, tq_scale, Bf.A, qr2 ? 1 : 0);
+      QTT_CUDA_TRY(cudaGetLastError());
     }
     // a4
     {
@@ -1325,13 +1581,14 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
       int Gq = P.Gjac;
       if (!getenv("QTT_COOP_WB")) {
         WBq = kWarps;
-        while (WBq > 1 && 2 * WBq * (m_cap + 1) * 8 > 200 * 1024) WBq /= 2;
+        const long long rows = tq_cand ? n_cap : m_cap;
+        while (WBq > 1 && 2 * WBq * (rows + 1) * 8 > 200 * 1024) WBq /= 2;
         WBq = std::max(WBq, P.WB);
         const long long pq = std::min(m_cap, n_cap);
         Gq = (int)std::min<long long>(g_sms, std::max<long long>(1, (pq + 2 * WBq - 1) / (2 * WBq)));
-        smq = sizeof(double) * (2 * WBq * m_cap + 2 * WBq);
+        smq = sizeof(double) * (2 * WBq * rows + 2 * WBq);
       }
-      ja.dims = Bf.dims; ja.A = Bf.A; ja.bar = Bf.bar + 1; ja.flags = Bf.flags; ja.ver = Bf.ver; ja.part = Bf.part; ja.nrm = Bf.s2; ja.G = Gq; ja.WB = WBq;
+      ja.dims = dims_j; ja.A = Bf.A; ja.bar = Bf.bar + 1; ja.flags = Bf.flags; ja.ver = Bf.ver; ja.part = Bf.part; ja.nrm = Bf.s2; ja.G = Gq; ja.WB = WBq;
       ja.noise_ok = noise_ok(io.eps, P.pcap); ja.skip = cqt_ok;
       ja.sweeps_out = io.sweeps ? io.sweeps + q : Bf.sweeps_scratch; ja.status = io.status;
       QTT_CUDA_TRY(cudaMemsetAsync(Bf.flags, 0, sizeof(int) * 3, s));
@@ -1342,7 +1599,7 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
     // a5/a6
     {
       FinishArgs fa;
-      fa.dims = Bf.dims; fa.A = Bf.A; fa.Cq = io.Cq[q]; fa.yr_next = io.yr + q + 1; fa.delta2 = io.delta2 + q;
+      fa.dims = dims_j; fa.A = Bf.A; fa.Cq = io.Cq[q]; fa.yr_next = io.yr + q + 1; fa.delta2 = io.delta2 + q;
       fa.sigma = io.sigma ? io.sigma + (size_t)q * io.sigma_stride : nullptr; fa.sigma_stride = io.sigma_stride;
       fa.s2 = Bf.s2; fa.perm = Bf.perm; fa.eps = io.eps; fa.max_rank = io.max_rank; fa.status = io.status;
       fa.carry = Bf.spec + 2; fa.T = Bf.T; fa.Gout = Bf.G; fa.skip = cqt_ok;
@@ -1352,6 +1609,15 @@ static qtt_status_t run_sweep(const SweepIO &io, const SweepPlan &P, char *ws, c
         k_cqt_finish<<<1, 32, 0, s>>>(cqt_ok, Bf.dims, io.yr + q + 1, io.delta2 + q, Bf.spec + 2,
                                       io.sweeps ? io.sweeps + q : nullptr);
         QTT_CUDA_TRY(cudaGetLastError());
+      }
+      if (tq) {                                    // U_T = Q [U_R; 0]
+        QapplyArgs qa2;
+        qa2.dims = Bf.dims; qa2.dims_j = dims_j; qa2.tq = tq; qa2.Yw = Bf.Tw;
+        qa2.tau = (double *)(ws + P.off_tqTau); qa2.C = io.Cq[q];
+        qa2.part = Bf.part; qa2.wtot = Bf.wtot; qa2.gram = Bf.gram; qa2.carry = Bf.spec + 2;
+        qa2.bar = Bf.bar; qa2.G = tq_G; qa2.RB = tq_RB;
+        qtt_status_t st = coop_launch((const void *)k_qapply_coop, tq_G, tq_smem, &qa2, s);
+        if (st != QTT_OK) return st;
       }
     }
     launch_gemm_spec(Bf.spec + 2, io.cap[q + 1], n_cap, 1, 1, false, io.tf32, s);
@@ -1960,7 +2226,7 @@ qtt_status_t large_zipup_sharded(const Shape &S, const qtt_trains_t *op, const q
       QTT_CUDA_TRY(cudaGetLastError());
       QrArgs qa;
       qa.dims = dims; qa.Tw = Tw; qa.Rout = A; qa.part = part; qa.wtot = wtot; qa.gram = gram;
-      qa.bc = bc; qa.bar = bar; qa.G = P.Gqr_s; qa.RB = P.RB_s; qa.mcap = (int)P.mcap; qa.skip = nullptr;
+      qa.bc = bc; qa.bar = bar; qa.G = P.Gqr_s; qa.RB = P.RB_s; qa.mcap = (int)P.mcap; qa.skip = nullptr; qa.tau_out = nullptr;
       st = coop_launch((const void *)k_qr_coop, P.Gqr_s, P.qr_smem, &qa, s);
       if (st != QTT_OK) return st;
       const long long fe = P.r_elems;
@@ -1981,7 +2247,7 @@ qtt_status_t large_zipup_sharded(const Shape &S, const qtt_trains_t *op, const q
       QTT_CUDA_TRY(cudaGetLastError());
       QrArgs qa;
       qa.dims = dims_st; qa.Tw = Tst; qa.Rout = Ast; qa.part = part; qa.wtot = wtot; qa.gram = gram;
-      qa.bc = bc; qa.bar = bar; qa.G = P.Gqr_st; qa.RB = P.RB_st; qa.mcap = (int)P.mcap; qa.skip = nullptr;
+      qa.bc = bc; qa.bar = bar; qa.G = P.Gqr_st; qa.RB = P.RB_st; qa.mcap = (int)P.mcap; qa.skip = nullptr; qa.tau_out = nullptr;
       st = coop_launch((const void *)k_qr_coop, P.Gqr_st, P.qr_smem, &qa, s);
       if (st != QTT_OK) return st;
       JacArgs ja;
