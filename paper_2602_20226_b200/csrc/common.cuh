@@ -172,14 +172,22 @@ __device__ __forceinline__ void householder(double alpha, double xnorm2, double 
   scale = 1.0 / (alpha - beta);
 }
 
+// the rare path of householder_fast<true> out of line (IEEE sqrt and divisions inlined into
+// every unrolled panel column only cost instruction-cache space)
+static __device__ __noinline__ void householder_slow(double alpha, double xnorm2, double &tau, double &beta, double &scale) {
+  householder(alpha, xnorm2, tau, beta, scale);
+}
+
 // householder() with MUFU-seeded Newton rcp / rsqrt instead of IEEE sqrt and two divisions
 // (same values to a few ulps; shortens the serial chain of a panel factorisation).
 // tau = (beta - alpha)/beta = 1 + |alpha|/nrm;  scale = 1/(alpha - beta) = sign(alpha)/(|alpha| + nrm).
+template <bool OOL = false>
 __device__ __forceinline__ void householder_fast(double alpha, double xnorm2, double &tau, double &beta,
                                                  double &scale) {
   const double a2 = fma(alpha, alpha, xnorm2);
   if (xnorm2 == 0.0 || !(a2 > 1e-280 && a2 < 1e280)) {   // zero column / outside the ftz-safe range
-    householder(alpha, xnorm2, tau, beta, scale);
+    if (OOL) householder_slow(alpha, xnorm2, tau, beta, scale);
+    else householder(alpha, xnorm2, tau, beta, scale);
     return;
   }
   const double rn = fast_rsqrt(a2);

@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_zipup(Args a) {
   // real scalars (a.jreg): dynamic shared memory = [Rp (packed R; also the cta_gemm staging and
   // the Jacobi scratch, never live at the same time)] [Bk / Jacobi matrix, 128 x kLdA] [Ysm] [tau]
   double *Rp = reinterpret_cast<double *>(zsm_raw + a.jsm_off);
-  double *Bk = Rp + kRpDoubles, *Ysm = Bk + kSmall * kLdA, *tauq = Ysm + 16 * kYld;
+  double *Bk = Rp + kRpDoubles, *Ysm = Bk + kQBkDoubles, *tauq = Ysm + 16 * kYld;
   double *gsm = Rp;
   S *zsm = reinterpret_cast<S *>(zsm_raw);
   S *w0 = static_cast<S *>(a.ws) + (size_t)b * a.ws_member;
@@ -828,7 +828,7 @@ qtt_status_t member_zipup(const Shape &S, const qtt_trains_t *op, const qtt_trai
     a.jreg = 1;
     a.smem = 0;
     a.jsm_off = 0;
-    smem = (size_t)(kRpDoubles + kSmall * kLdA + 16 * kYld + kSmall) * sizeof(double);
+    smem = (size_t)(kRpDoubles + kQBkDoubles + 16 * kYld + kSmall) * sizeof(double);
   }
   if (complex_dt) {       // dynamic-smem opt-in every call (per-device attribute; thread-safe)
     if (a.smem)

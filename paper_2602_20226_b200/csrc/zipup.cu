@@ -41,7 +41,7 @@ qtt_status_t cuda_status(cudaError_t e, const char *what) {
 
 constexpr int kMaxSites = 64;
 constexpr int kBkDoubles = kRpDoubles;                  // staged MPO core limit
-constexpr int kSiteSmemDoubles = kRpDoubles + kSmall * kLdA + kSmall + 16 + 8 + kSmall + 16 * 136;
+constexpr int kSiteSmemDoubles = kRpDoubles + kQBkDoubles + kSmall + 16 + 8 + kSmall + 16 * 136;
 constexpr size_t kSiteSmemBytes = kSiteSmemDoubles * sizeof(double) + (kSmall + 8) * sizeof(int);
 constexpr int kOrthSmemDoubles = 26000;  // a1 staging budget (~203 KB)
 
@@ -299,7 +299,7 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
   double *Rp = smem;                         // packed R (QR) / GEMM staging / scratch
   double *Rs = Rp + kRpDoubles;              // kSmall x kLdA: QR block, then A (col-major)
   double *Bk = Rp;                           // staging alias
-  double *sg = Rs + kSmall * kLdA;           // sigma^2 per column
+  double *sg = Rs + kQBkDoubles;           // sigma^2 per column
   double *red = sg + kSmall;                 // block-reduction scratch
   double *scal = red + 16;                   // scalars
   double *tau = scal + 8;                    // Householder tau per column
@@ -829,8 +829,8 @@ using namespace qtt;
 #if QTT_JAC_PROFILE
 extern "C" int qtt_debug_jprof(unsigned long long *host, int reset) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(host, qtt::g_jprof, sizeof(unsigned long long) * 4);
-  if (reset) { unsigned long long z[4] = {0, 0, 0, 0}; cudaMemcpyToSymbol(qtt::g_jprof, z, sizeof(z)); }
+  cudaMemcpyFromSymbol(host, qtt::g_jprof, sizeof(unsigned long long) * 16);
+  if (reset) { unsigned long long z[16] = {}; cudaMemcpyToSymbol(qtt::g_jprof, z, sizeof(z)); }
   return 0;
 }
 #endif
