@@ -143,6 +143,9 @@ __device__ int orth_site_reg(double *core, int c, int r, double *prev, int rows_
   for (int i = tid; i < k * r; i += kThreads) Rb[i] = 0.0;
   if (warp == 0) orth_form_reflector<RPL, NCW>(X, 0, c, vbuf, taus);
   __syncthreads();
+#if QTT_JAC_PROFILE
+  const long long op0 = clock64();
+#endif
   // The owner of column j+1 applies reflector j to that column only, forms reflector j+1 and
   // defers reflector j on its other columns to the next step (where it is not the owner), so
   // the per-step critical path is one column update + one reflector, not a full update more.
@@ -169,6 +172,9 @@ __device__ int orth_site_reg(double *core, int c, int r, double *prev, int rows_
     const double tp = taus[pend];
     if (tp != 0.0) orth_apply<RPL, NCW>(X, pend, vbuf, tp, -2 - pend_slot, wbuf);
   }
+#if QTT_JAC_PROFILE
+  const long long op1 = clock64();
+#endif
   // R: column col holds R[i][col] in rows i <= min(col, k-1)
 #pragma unroll
   for (int ss = 0; ss < NCW; ++ss) {
@@ -192,6 +198,9 @@ __device__ int orth_site_reg(double *core, int c, int r, double *prev, int rows_
     if (tau != 0.0) orth_apply<RPL, NCW, true>(X, j, vbuf, tau, -1, wbuf);
   }
   __syncthreads();                                   // Rb complete; reflectors no longer read
+#if QTT_JAC_PROFILE
+  const long long op2 = clock64();
+#endif
   // core q <- Q^T: row kk = column kk of Q (coalesced along rows of Q)
 #pragma unroll
   for (int ss = 0; ss < NCW; ++ss) {
@@ -209,6 +218,13 @@ __device__ int orth_site_reg(double *core, int c, int r, double *prev, int rows_
            [&](int a, int kk) { return Rb[(size_t)kk * r + a]; },
            [&](int i, int kk, double v) { prev[(size_t)i * k + kk] = v; }, gst);
   __syncthreads();
+#if QTT_JAC_PROFILE
+  const long long op3 = clock64();
+  if (threadIdx.x == 0 && c == 128 && r == 64) {
+    atomicAdd(&g_jprof[12], (unsigned long long)(op1 - op0)); atomicAdd(&g_jprof[13], (unsigned long long)(op2 - op1));
+    atomicAdd(&g_jprof[14], (unsigned long long)(op3 - op2)); atomicAdd(&g_jprof[15], 1ull);
+  }
+#endif
   return k;
 }
 

@@ -92,12 +92,12 @@ __device__ __forceinline__ void qr_panel(double *Rp, double *Bk, double *tau, in
       const double alpha = Rp[rp_idx(j, j, m)];
       double rjc[kPanel];
 #pragma unroll
-      for (int cc = jj + 1; cc < kPanel; ++cc) rjc[cc] = (j0 + cc < m) ? Rp[rp_idx(j, j0 + cc, m)] : 0.0;
+      for (int cc = 0; cc < kPanel; ++cc) rjc[cc] = (cc > jj && j0 + cc < m) ? Rp[rp_idx(j, j0 + cc, m)] : 0.0;
       halve<kPanel, 16, kPanel>(v, lane);
       // every broadcast at once, unconditionally (no divergence guard between them)
       double bc[kPanel];
 #pragma unroll
-      for (int cc = jj; cc < kPanel; ++cc) bc[cc] = __shfl_sync(0xffffffffu, v[0], cc << kPanelSh);
+      for (int cc = 0; cc < kPanel; ++cc) bc[cc] = (cc >= jj) ? __shfl_sync(0xffffffffu, v[0], cc << kPanelSh) : 0.0;
       double tj, beta, scale;
       householder_fast<QTT_QR_OOL>(alpha, bc[jj], tj, beta, scale);
 #pragma unroll
@@ -106,11 +106,13 @@ __device__ __forceinline__ void qr_panel(double *Rp, double *Bk, double *tau, in
       // straight-line update of the remaining panel columns: tau = 0 (zero column) gives w = 0;
       // padding columns (c >= m) are zero, so their w is 0 as well
 #pragma unroll
-      for (int cc = jj + 1; cc < kPanel; ++cc) {
-        const double w = tj * fma(scale, bc[cc], rjc[cc]);
+      for (int cc = 0; cc < kPanel; ++cc) {
+        if (cc > jj) {                             // (jj-independent bounds: fully unrolled)
+          const double w = tj * fma(scale, bc[cc], rjc[cc]);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) P[cc][t] = fma(-w, P[jj][t], P[cc][t]);
-        if (lane == 0 && j0 + cc < m) Rp[rp_idx(j, j0 + cc, m)] = rjc[cc] - w;
+          for (int t = 0; t < 4; ++t) P[cc][t] = fma(-w, P[jj][t], P[cc][t]);
+          if (lane == 0 && j0 + cc < m) Rp[rp_idx(j, j0 + cc, m)] = rjc[cc] - w;
+        }
       }
       __syncwarp();
     }

@@ -19,6 +19,15 @@
 #include "large.cuh"
 #include "orth.cuh"
 #include "qr_small.cuh"
+#include "qr_std.cuh"
+
+#ifndef QTT_A1_BLK
+#define QTT_A1_BLK 1          // a1 wide sites by the blocked QR of qr_std.cuh
+#endif
+#ifndef QTT_A1_BLK_MINR
+#define QTT_A1_BLK_MINR 17
+#endif
+static_assert(qtt::orth_blk_smem() <= 27904, "a1 blocked path exceeds the k_orth shared memory");
 
 
 
@@ -43,7 +52,7 @@ constexpr int kMaxSites = 64;
 constexpr int kBkDoubles = kRpDoubles;                  // staged MPO core limit
 constexpr int kSiteSmemDoubles = kRpDoubles + kQBkDoubles + kSmall + 16 + 8 + kSmall + 16 * 136;
 constexpr size_t kSiteSmemBytes = kSiteSmemDoubles * sizeof(double) + (kSmall + 8) * sizeof(int);
-constexpr int kOrthSmemDoubles = 26000;  // a1 staging budget (~203 KB)
+constexpr int kOrthSmemDoubles = 27904;  // a1 staging budget (218 KB; >= orth_blk_smem())
 
 
 // ======================================================================= a1: pre-pass
@@ -151,6 +160,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_orth(OrthArgs a) {
     double *core = base + a.off[q];
     {  // register-resident QR (orth.cuh) when the site fits; else the shared-memory path below
       const int rows_prev = a.r0[q - 1] * a.legs[q - 1];
+#if QTT_A1_BLK
+      // wide sites: blocked Householder with DMMA WY updates and explicit Q (qr_std.cuh)
+      if (c > 64 && c <= 128 && r >= QTT_A1_BLK_MINR && r <= 64 && rows_prev <= 128) {
+        orth_site_blk(core, c, r, base + a.off[q - 1], rows_prev, smem);
+        if (tid == 0) rk[q] = k;
+        rr = k;
+        continue;
+      }
+#endif
       const int rpl = (c <= 32) ? 1 : (c <= 64) ? 2 : (c <= 128) ? 4 : 0;
       const int ncw = (r <= 8) ? 1 : (r <= 16) ? 2 : (r <= 32) ? 4 : (r <= 64) ? 8 : 0;
       if (rpl && ncw && orth_reg_smem(rpl, c, r, rows_prev) <= kOrthSmemDoubles) {

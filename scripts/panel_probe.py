@@ -11,3 +11,24 @@ for mode, name in ((0, "16 panels (one warp)"), (1, "qr_of_TH 128x256")):
     lib.qtt_probe_panel(ctypes.c_void_p(T.data_ptr()), out, mode, 20)
     lib.qtt_probe_panel(ctypes.c_void_p(T.data_ptr()), out, mode, 20)
     print(name, out[0], "cycles")
+c0 = torch.randn(64, 128, generator=g, dtype=torch.float64).cuda()
+p0 = torch.randn(128, 64, generator=g, dtype=torch.float64).cuda()
+c1, p1 = torch.empty_like(c0), torch.empty_like(p0)
+for _ in range(2):
+    lib.qtt_probe_orth(ctypes.c_void_p(c0.data_ptr()), ctypes.c_void_p(p0.data_ptr()), ctypes.c_void_p(c1.data_ptr()),
+                       ctypes.c_void_p(p1.data_ptr()), out, 10)
+print("a1 site 64x128 (orth_site_reg<4,8>)", out[0], "cycles")
+# check: rows of the new core orthonormal, prev' core' == prev core
+Q = c1.cpu(); print("  |Q Q^T - I| =", float((Q @ Q.T - torch.eye(64, dtype=torch.float64)).abs().max()),
+                    " |P'Q' - P C| =", float((p1.cpu() @ Q - p0.cpu() @ c0.cpu()).abs().max()))
+for _ in range(2):
+    lib.qtt_probe_orthblk(ctypes.c_void_p(c0.data_ptr()), ctypes.c_void_p(p0.data_ptr()), ctypes.c_void_p(c1.data_ptr()),
+                          ctypes.c_void_p(p1.data_ptr()), out, 10)
+print("a1 site 64x128 (orth_site_blk)", out[0], "cycles")
+Q = c1.cpu(); print("  |Q Q^T - I| =", float((Q @ Q.T - torch.eye(64, dtype=torch.float64)).abs().max()),
+                    " |P'Q' - P C| =", float((p1.cpu() @ Q - p0.cpu() @ c0.cpu()).abs().max()))
+tr = (ctypes.c_longlong * 128)()
+lib.qtt_probe_blktrace(tr)
+for st in range(8):
+    o = tr[st * 8: st * 8 + 8]
+    print(f"  step {st}: panel-warp small {o[0]:6d} panel {o[1]:6d} wait {o[2]:6d} | warp0 small {o[4]:6d} big {o[5]:6d} wait {o[6]:6d}")

@@ -19,4 +19,6 @@ n = max(buf[10], 1)
 r = max(buf[3], 1)
 print({"qr_calls": n, "qr_total": buf[11] / n, "staging": buf[4] / n, "w0_small_trailing": buf[6] / n,
        "w0_panel": buf[5] / n, "w0_wait": buf[8] / n, "w1_big_trailing": buf[7] / n, "w1_wait": buf[9] / n})
+no = max(buf[15], 1)
+print({"orth_sites_128x64": buf[15], "factor": buf[12] / no, "form_q": buf[13] / no, "absorb_gemm": buf[14] / no})
 print({"jac_rounds": r, "dots_reduce": buf[0] / r, "params": buf[1] / r, "rotation": buf[2] / r})
