@@ -33,7 +33,11 @@ __device__ unsigned long long g_jprof[16];   // [4..11]: qr_of_TH phases (qr_sma
 #define QTT_JPROF_ADD(i, d)
 #endif
 #ifndef QTT_JAC_SCALED
-#define QTT_JAC_SCALED 0
+// scaled (fast-Givens, Anda-Park) rotations: two DFMA per row and pair instead of two DMUL + two
+// DFMA; the rotation phase of a round runs both warps of an SMSP on the FP64 pipe at once, so
+// halving its FP64 instructions shortens the round (round 2: 131.2k -> 133.4k site-steps/s on
+// cfg5; round 1, before the division-free angles and the Halley rsqrt, measured no change)
+#define QTT_JAC_SCALED 1
 #endif
 #ifndef QTT_JAC_GRAMCHECK
 #define QTT_JAC_GRAMCHECK 1
