@@ -25,7 +25,7 @@ constexpr int kJacobiMaxSweeps = 60;
 #if QTT_JAC_PROFILE
 // diagnostics build only: cycles per jac_round phase summed over warp 0 of every CTA
 // [0] dots + reduce-scatter, [1] rotation parameters, [2] rotation, [3] rounds
-__device__ unsigned long long g_jprof[16];   // [4..11]: qr_of_TH phases (qr_small.cuh)
+__device__ unsigned long long g_jprof[24];   // [4..11]: qr_of_TH phases (qr_small.cuh), [12..15] a1, [16..19] a2
 #define QTT_JPROF_T(v) const long long v = clock64()
 #define QTT_JPROF_ADD(i, d) if (threadIdx.x == 0) atomicAdd(&g_jprof[i], (unsigned long long)(d))
 #else
