@@ -273,3 +273,22 @@ def test_maximum_sites_and_refusal(lib):
     with pytest.raises(lib.QttError) as e:
         lib.ZipupPlan("i->i", None, xd, 1e-8, 4)
     assert e.value.status == 8
+
+
+@pytest.mark.parametrize("kind", ["truncate", "matvec"])
+def test_a1_blocked_rank_deficient(lib, kind):
+    """a1's blocked Householder path (qr_std.cuh: M^T with 65..128 rows, 17..64 columns) on
+    rank-deficient cores: a core whose M^T has duplicated columns (zero pivots in R, reflectors
+    with tau = 0 further on), one with zero rows of M (zero columns of M^T), one tiny core.  The
+    result must match the oracle like any other input (c-A3)."""
+    dims = [2] * 12
+    x = gen.random_mps(dims, 48, np.random.default_rng(77)).cores
+    assert any(c.shape[0] >= 17 and c.shape[1] * c.shape[2] > 64 for c in x)
+    x[5] = x[5].copy(); x[5][: x[5].shape[0] // 2] = x[5][x[5].shape[0] // 2: 2 * (x[5].shape[0] // 2)]
+    x[7] = x[7].copy(); x[7][::3] = 0.0
+    x[8] = x[8] * 1e-9
+    op = gen.random_mpo(dims, 2, np.random.default_rng(78), 0.5).cores
+    if kind == "truncate":
+        check(lib, "truncate", None, x, 1e-10, 0, dense=True)
+    else:
+        check(lib, "matvec", op, x, 1e-10, 40, dense=True)
