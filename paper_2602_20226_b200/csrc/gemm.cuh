@@ -165,17 +165,25 @@ __global__ void __launch_bounds__(256, 1) k_gemm_dmma(const GemmSpec *spec, int 
     }
   }
   cp_async_wait<0>();
+  // epilogue: a lane's two adjacent outputs as one 16-byte store when C is N-contiguous and
+  // aligned (two 8-byte stores from separate instructions leave every 32-byte sector half
+  // written in between: partial-sector writes in L2)
+  const bool vec = g.scn == 1 && (g.scm & 1) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int gm = m0 + wm * 32 + i * 8 + gr;
     if (gm >= g.M) continue;
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < 8; ++j) {
+      const int gn = n0 + wn * 64 + j * 8 + 2 * gc;
+      if (vec && gn + 1 < g.N) {
+        *reinterpret_cast<double2 *>(C + (long long)gm * g.scm + gn) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else {
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int gn = n0 + wn * 64 + j * 8 + 2 * gc + e;
-        if (gn < g.N) C[(long long)gm * g.scm + (long long)gn * g.scn] = acc[i][j][e];
+        for (int e = 0; e < 2; ++e)
+          if (gn + e < g.N) C[(long long)gm * g.scm + (long long)(gn + e) * g.scn] = acc[i][j][e];
       }
+    }
   }
 }
 

@@ -303,12 +303,21 @@ __device__ __forceinline__ int orth_site_blk(double *core, int c, int r, double 
 #if QTT_JAC_PROFILE
   const long long op2 = clock64();
 #endif
+#ifdef QTT_BLK_TRACE
+  const long long tq0 = clock64();
+#endif
   // core q <- Q^T
   for (int idx = tid; idx < k * c; idx += kST) {
     const int kk = idx / c, i = idx % c;
     core[idx] = Qm[i * kLdQm + kk];
   }
   __syncthreads();
+#if QTT_JAC_PROFILE
+  const long long opa = clock64();
+#endif
+#ifdef QTT_BLK_TRACE
+  const long long opa_t = clock64();
+#endif
   // prev <- prev R^T   (rows_prev x r) (r x k); R[kk][a] = A[kk][a], a >= kk.  DMMA over 8 x 8
   // output tiles (two per warp at a time), prev staged with row stride kLdQm
   double *Ps = Qm;                                   // staging (rows_prev x r, stride kLdQm)
@@ -335,45 +344,74 @@ __device__ __forceinline__ int orth_site_blk(double *core, int c, int r, double 
     }
   }
   __syncthreads();
+#if QTT_JAC_PROFILE
+  const long long opb = clock64();
+#endif
+#ifdef QTT_BLK_TRACE
+  const long long opb_t = clock64();
+#endif
   {
     const int lane = tid & 31, gr = lane >> 2, gc = lane & 3;
     const int tm = rp8 >> 3, tn = (k + 7) >> 3, nt = tm * tn;
-    for (int t0 = warp * 2; t0 < nt; t0 += 2 * kSW) {
-      double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll 4
-      for (int a0 = 0; a0 < r4; a0 += 4) {
-        const int a = a0 + gc;
+    // four tiles per warp at a time, K split over two accumulators: eight independent DMMA
+    // chains (one chain per tile leaves the warp waiting on the DMMA latency)
+    constexpr int UT = 4;
+    for (int t0 = warp * UT; t0 < nt; t0 += UT * kSW) {
+      double c[UT][2][2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int t = t0 + u;
-          if (t < nt) {
-            const int i0 = (t / tn) * 8, n0 = (t % tn) * 8;
-            const double av = Ps[(i0 + gr) * kLdQm + a];
-            const int kk = n0 + gr;
+      for (int u = 0; u < UT; ++u) c[u][0][0] = c[u][0][1] = c[u][1][0] = c[u][1][1] = 0.0;
+      int i0[UT], n0[UT];
+#pragma unroll
+      for (int u = 0; u < UT; ++u) { const int t = min(t0 + u, nt - 1); i0[u] = (t / tn) * 8; n0[u] = (t % tn) * 8; }
+#pragma unroll 2
+      for (int a0 = 0; a0 < r4; a0 += 8) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int a = a0 + 4 * h + gc;
+#pragma unroll
+          for (int u = 0; u < UT; ++u) {
+            const double av = (a < r4) ? Ps[(i0[u] + gr) * kLdQm + a] : 0.0;
+            const int kk = n0[u] + gr;
             const double bv = (kk < k && a >= kk && a < r) ? A[kk * kLdQ + a] : 0.0;
-            dmma884(c[u][0], c[u][1], av, bv);
+            dmma884(c[u][h][0], c[u][h][1], av, bv);
           }
         }
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < UT; ++u) {
         const int t = t0 + u;
         if (t < nt) {
-          const int row = (t / tn) * 8 + gr, kk = (t % tn) * 8 + 2 * gc;
+          const int row = i0[u] + gr, kk = n0[u] + 2 * gc;
           if (row < rows_prev) {
-            if (kk < k) prev[(size_t)row * k + kk] = c[u][0];
-            if (kk + 1 < k) prev[(size_t)row * k + kk + 1] = c[u][1];
+            const double v0 = c[u][0][0] + c[u][1][0], v1 = c[u][0][1] + c[u][1][1];
+            double *dst = prev + (size_t)row * k + kk;
+            if (kk + 1 < k && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+              *reinterpret_cast<double2 *>(dst) = make_double2(v0, v1);     // whole 16-byte pieces
+            } else {
+              if (kk < k) dst[0] = v0;
+              if (kk + 1 < k) dst[1] = v1;
+            }
           }
         }
       }
     }
   }
+#ifdef QTT_BLK_TRACE
+  const long long tq3 = clock64();
+#endif
   __syncthreads();
+#ifdef QTT_BLK_TRACE
+  if ((threadIdx.x & 31) == 0 && warp < 8) {
+    long long *o = QTT_BLK_TRACE + 64 + warp * 8;
+    o[0] = opa_t - tq0; o[1] = opb_t - opa_t; o[2] = tq3 - opb_t; o[3] = clock64() - tq3;
+  }
+#endif
 #if QTT_JAC_PROFILE
   const long long op3 = clock64();
   if (threadIdx.x == 0 && c == 128 && r == 64) {
     atomicAdd(&g_jprof[12], (unsigned long long)(op1 - op0)); atomicAdd(&g_jprof[13], (unsigned long long)(op2 - op1));
     atomicAdd(&g_jprof[14], (unsigned long long)(op3 - op2)); atomicAdd(&g_jprof[15], 1ull);
+    atomicAdd(&g_jprof[20], (unsigned long long)(opa - op2)); atomicAdd(&g_jprof[21], (unsigned long long)(opb - opa));
   }
 #endif
   return k;

@@ -866,8 +866,8 @@ using namespace qtt;
 #if QTT_JAC_PROFILE
 extern "C" int qtt_debug_jprof(unsigned long long *host, int reset) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(host, qtt::g_jprof, sizeof(unsigned long long) * 16);
-  if (reset) { unsigned long long z[16] = {}; cudaMemcpyToSymbol(qtt::g_jprof, z, sizeof(z)); }
+  cudaMemcpyFromSymbol(host, qtt::g_jprof, sizeof(unsigned long long) * 24);
+  if (reset) { unsigned long long z[24] = {}; cudaMemcpyToSymbol(qtt::g_jprof, z, sizeof(z)); }
   return 0;
 }
 #endif

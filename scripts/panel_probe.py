@@ -32,3 +32,7 @@ lib.qtt_probe_blktrace(tr)
 for st in range(8):
     o = tr[st * 8: st * 8 + 8]
     print(f"  step {st}: panel-warp small {o[0]:6d} panel {o[1]:6d} wait {o[2]:6d} | warp0 small {o[4]:6d} big {o[5]:6d} wait {o[6]:6d}")
+lib.qtt_probe_blktrace(tr)
+for w in range(8):
+    o = tr[64 + w * 8: 64 + w * 8 + 4]
+    print(f"  absorb warp {w}: Q^T out {o[0]:6d} staging {o[1]:6d} gemm+stores {o[2]:6d} final barrier {o[3]:6d}")

@@ -20,7 +20,8 @@ r = max(buf[3], 1)
 print({"qr_calls": n, "qr_total": buf[11] / n, "staging": buf[4] / n, "w0_small_trailing": buf[6] / n,
        "w0_panel": buf[5] / n, "w0_wait": buf[8] / n, "w1_big_trailing": buf[7] / n, "w1_wait": buf[9] / n})
 no = max(buf[15], 1)
-print({"orth_sites_128x64": buf[15], "factor": buf[12] / no, "form_q": buf[13] / no, "absorb_gemm": buf[14] / no})
+print({"orth_sites_128x64": buf[15], "factor": buf[12] / no, "form_q": buf[13] / no, "absorb_gemm": buf[14] / no,
+       "  of which Q^T out": buf[20] / no, "prev staging": buf[21] / no})
 nc = max(buf[18], 1)
 print({"a2_warp_tiles": buf[18], "a2_total_per_warp": buf[16] / nc, "a2_dmma_per_warp": buf[17] / nc, "a2_staging_per_site": buf[19] / max(buf[18] / 8, 1)})
 print({"jac_rounds": r, "dots_reduce": buf[0] / r, "params": buf[1] / r, "rotation": buf[2] / r})
