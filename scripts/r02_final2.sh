@@ -1,7 +1,7 @@
 # round 2 (session 2) evidence: full GPU suite, smoke, every bench line, reference arm, cfg5 launch
 # list, ncu --set full of k_sweep and k_orth (512 members) for the traffic figures
 set -x
-O=gpurun_out/r02final2; mkdir -p $O
+O=gpurun_out/${R02_OUT:-r02final2}; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $O/gpu.txt
 timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 600 --durations 15 > $O/pytest_gpu.log 2>&1; echo pytest_rc=$?
 tail -4 $O/pytest_gpu.log
