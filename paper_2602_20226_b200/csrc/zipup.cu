@@ -353,8 +353,15 @@ __device__ __forceinline__ void site_step(const SweepArgs &a, int b, int q, doub
   const int d = a.d[q], dj = a.dj[q];
   const int m = chi * d, n = w2 * r2;
   double *G = a.G + (size_t)b * a.G_bs;
-  double *T = a.T + (size_t)b * a.T_bs;
-  double *X = a.X + (size_t)b * a.X_bs;
+  // T and X live only inside one task: one slot per CTA (grid <= B), so the ~148 slots in use
+  // stay L2-resident and are rewritten in place instead of walking a B-slot footprint
+  // (per-member slots made the dirty lines of finished tasks get written back to HBM)
+#ifndef QTT_CTA_SCRATCH
+#define QTT_CTA_SCRATCH 1
+#endif
+  const size_t slot = QTT_CTA_SCRATCH ? (size_t)blockIdx.x : (size_t)b;
+  double *T = a.T + slot * a.T_bs;
+  double *X = a.X + slot * a.X_bs;
   const double *Xq = a.Xo + (size_t)b * a.Xo_bs + a.xoff[q];
   const double *Oq = a.Oo ? a.Oo + (a.shared_op ? 0 : (size_t)b * a.Oo_bs) + a.ooff[q] : nullptr;
   double *Cq = a.Cq[q] + (size_t)b * a.Cq_bs[q];
@@ -1074,7 +1081,9 @@ qtt_status_t qtt_zipup(const char *subscripts, const qtt_trains_t *op, const qtt
     int dev = 0, sms = 0;
     QTT_CUDA_TRY(cudaGetDevice(&dev));
     QTT_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int grid = std::max(1, std::min(sms, S.B * S.L));
+    // at most B tasks are runnable at once (a member's sites are sequential), and the per-CTA
+    // T / X slots of the workspace number B
+    const int grid = std::max(1, std::min(sms, S.B));
     QTT_CUDA_TRY(record(2));
     k_sweep<<<grid, kST, kSiteSmemBytes, s>>>(a);
     QTT_CUDA_TRY(cudaGetLastError());
