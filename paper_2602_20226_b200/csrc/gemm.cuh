@@ -14,6 +14,17 @@
 // 32 x 64 = 4 x 8 DMMA fragments (64 fp64 accumulators per lane).  Shared-memory leading
 // dimensions are chosen so every fragment load hits each 8-byte bank pair exactly twice per
 // warp (the minimum two wavefronts of a 256-byte request).
+//
+// TMA = true (measured, not the product's feed -- DESIGN.md section 6): an interior tile (all 128 rows /
+// columns inside the matrix, K a multiple of 16) of a view whose contiguous dimension has unit
+// stride and whose rows start 16-byte aligned (even leading stride, aligned base) is staged by
+// TMA bulk copies (`cp.async.bulk` ... `mbarrier::complete_tx`: one 128-byte or 1 KB row per
+// copy into the padded fragment layout, issued by warp 0, one mbarrier per stage); every other
+// tile (ragged edges, odd strides -- ranks are decided on the device and need not be even --
+// and the transposing K-contiguous B) keeps cp.async.  The decision is per CTA and operand and
+// both feeds share the stages and the one __syncthreads per K chunk.  On B200 the row-wise bulk
+// copies lose to cp.async (cfg3 314 vs 289 ms per zip-up), so libqtt instantiates TMA = false;
+// tests/test_gpu_gemm.py checks both.
 #pragma once
 #include "common.cuh"
 
@@ -40,7 +51,7 @@ constexpr int LDA_M = TM + 8;      // As[k][m] (A M-contiguous): 136 == 8 mod 16
 constexpr int LDB = TN + 8;        // Bs[k][n]: 136
 constexpr int A_STAGE = TM * LDA_K > TK * LDA_M ? TM * LDA_K : TK * LDA_M;   // 2560 doubles
 constexpr int B_STAGE = TK * LDB;                                            // 2176 doubles
-constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
+constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double) + STAGES * sizeof(uint64_t);
 }  // namespace dgemm
 
 __device__ __forceinline__ void cp_async8(double *dst, const double *src, bool pred) {
@@ -59,7 +70,7 @@ __device__ __forceinline__ void dmma_884(double &c0, double &c1, double a, doubl
 
 // grid: x = tiles_m * tiles_n (capacity), z = nz1cap * nz2cap; block = 256 threads.
 // B_KCONTIG: B is K-contiguous (sbk == 1, e.g. the transposed operand of a Gram matrix T T^T).
-template <bool A_KCONTIG, bool B_KCONTIG = false>
+template <bool A_KCONTIG, bool B_KCONTIG = false, bool TMA = false>
 __global__ void __launch_bounds__(256, 1) k_gemm_dmma(const GemmSpec *spec, int tiles_n, int nz2_cap) {
   using namespace dgemm;
   extern __shared__ double gsm[];
@@ -92,10 +103,44 @@ __global__ void __launch_bounds__(256, 1) k_gemm_dmma(const GemmSpec *spec, int 
   double *As = gsm, *Bs = gsm + STAGES * A_STAGE;
   const int nk = (g.K + TK - 1) / TK;
 
+  // TMA feed of interior, 16-byte aligned tiles (CTA-uniform decisions)
+  uint64_t *bars = reinterpret_cast<uint64_t *>(gsm + STAGES * (A_STAGE + B_STAGE));
+  const bool kfull = TMA && (g.K % TK) == 0;
+  const bool tmaA = kfull && m0 + TM <= g.M && (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
+                    (A_KCONTIG ? (g.sam & 1) == 0 : (g.sam == 1 && (g.sak & 1) == 0));
+  const bool tmaB = kfull && !B_KCONTIG && n0 + TN <= g.N && (reinterpret_cast<uintptr_t>(B) & 15) == 0 &&
+                    g.sbn == 1 && (g.sbk & 1) == 0;
+  if (tmaA || tmaB) {
+    if (tid == 0)
+      for (int st = 0; st < STAGES; ++st) tma_mbar_init(&bars[st]);
+    __syncthreads();
+  }
+
   auto load_stage = [&](int st, int kc) {
     const int k0 = kc * TK;
     double *as = As + st * A_STAGE, *bs = Bs + st * B_STAGE;
-    if (A_KCONTIG) {          // As[m][k]: thread -> row m = tid/2, 8 consecutive k
+    if ((tmaA || tmaB) && warp == 0) {
+      if (lane == 0)
+        tma_expect_tx(&bars[st], (uint32_t)((tmaA ? TM * TK : 0) + (tmaB ? TK * TN : 0)) * (uint32_t)sizeof(double));
+      __syncwarp();
+      if (tmaA) {
+        if (A_KCONTIG) {      // As[m][k]: 128 rows of 16 doubles
+#pragma unroll
+          for (int e = 0; e < TM / 32; ++e) {
+            const int m = e * 32 + lane;
+            tma_load_1d(as + m * LDA_K, A + (long long)(m0 + m) * g.sam + k0, TK * sizeof(double), &bars[st]);
+          }
+        } else if (lane < TK) {   // As[k][m]: 16 rows of 128 doubles
+          tma_load_1d(as + lane * LDA_M, A + (long long)(k0 + lane) * g.sak + m0, TM * sizeof(double), &bars[st]);
+        }
+      }
+      if (tmaB && lane >= 32 - TK) {   // Bs[k][n]: 16 rows of 128 doubles
+        const int k = lane - (32 - TK);
+        tma_load_1d(bs + k * LDB, B + (long long)(k0 + k) * g.sbk + n0, TN * sizeof(double), &bars[st]);
+      }
+    }
+    if (tmaA) {
+    } else if (A_KCONTIG) {   // As[m][k]: thread -> row m = tid/2, 8 consecutive k
       const int m = tid >> 1, kh = (tid & 1) * 8, gm = m0 + m;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
@@ -112,7 +157,8 @@ __global__ void __launch_bounds__(256, 1) k_gemm_dmma(const GemmSpec *spec, int 
         cp_async8(as + k * LDA_M + mh + e, ok ? A + (long long)gm * g.sam + (long long)gk * g.sak : A, ok);
       }
     }
-    if (B_KCONTIG) {          // Bs[k][n] from K-contiguous B: thread -> n = tid/2, 8 consecutive k
+    if (tmaB) {
+    } else if (B_KCONTIG) {   // Bs[k][n] from K-contiguous B: thread -> n = tid/2, 8 consecutive k
       const int n = tid >> 1, kh = (tid & 1) * 8, gn = n0 + n;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
@@ -144,6 +190,7 @@ __global__ void __launch_bounds__(256, 1) k_gemm_dmma(const GemmSpec *spec, int 
   }
   for (int kc = 0; kc < nk; ++kc) {
     cp_async_wait<STAGES - 2>();
+    if (tmaA || tmaB) tma_wait(&bars[kc % STAGES], (uint32_t)(kc / STAGES) & 1u);
     __syncthreads();                                   // stage kc visible; stage kc-1 consumed
     if (kc + STAGES - 1 < nk) load_stage((kc + STAGES - 1) % STAGES, kc + STAGES - 1);
     cp_async_commit();
